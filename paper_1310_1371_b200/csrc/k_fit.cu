@@ -1,0 +1,149 @@
+// k_fit.cu — K3: canonical ordering of the peaks, non-exclusive annulus classification
+// of the ridge pixels and the Kasa circle fit, one CTA per frame, one warp per ring.
+//
+// Rows A9-A11 of DESIGN.md §2 ("for each peak an annulus mask is formed
+// and a best fitting circle is found for all ridge coordinates within the annulus";
+// SI step 5).  Membership is an exact integer test
+// (r-w)_+^2 <= d^2 <= (r+w)^2 over the ridge bins the annulus overlaps; the moments are
+// int64 sums (order-free, hence bit-exact); the 3x3 normal equations are solved by
+// Cramer's rule with exact int128 determinants and one rounding per unknown.
+#include "rd_internal.cuh"
+
+namespace rd {
+
+struct Ring {  // == rd_ring (64 B)
+  int32_t cx, cy, r, raw_votes;
+  int64_t score_fixed;
+  int32_t inliers, fit_ok;
+  double fx, fy, fr, rms;
+};
+
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ __int128 det3(__int128 a, __int128 b, __int128 c, __int128 d, __int128 e, __int128 f,
+                                         __int128 g, __int128 h, __int128 i) {
+  return a * (e * i - f * h) - b * (d * i - f * g) + c * (d * h - e * g);
+}
+
+__global__ void __launch_bounds__(K3_THREADS) k_fit(Params P, Ring* __restrict__ rings, int* __restrict__ counts) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  Peak* sp = reinterpret_cast<Peak*>(smem);                    // [ring_cap]
+  int* order = reinterpret_cast<int*>(sp + P.ring_cap);         // [ring_cap]
+  const int f = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int npk = P.peak_count[f];
+  const int flags = P.flags[f];
+  if (flags != 0 || npk > P.ring_cap) {
+    if (tid == 0) counts[f] = -1;
+    return;
+  }
+  for (int i = tid; i < npk; i += K3_THREADS) sp[i] = P.peaks[(int64_t)f * P.ring_cap + i];
+  __syncthreads();
+  // canonical (r, cy, cx) order: rank of each (unique) key
+  for (int i = tid; i < npk; i += K3_THREADS) {
+    const Peak a = sp[i];
+    int rank = 0;
+    for (int j = 0; j < npk; ++j) {
+      const Peak b = sp[j];
+      rank += (b.r < a.r) || (b.r == a.r && (b.y < a.y || (b.y == a.y && b.x < a.x)));
+    }
+    order[rank] = i;
+  }
+  __syncthreads();
+  const int64_t fbins = (int64_t)f * P.nbx * P.nby;
+  for (int p = warp; p < npk; p += K3_THREADS / 32) {
+    const Peak pk = sp[order[p]];
+    const int w = P.lvlAnn[pk.r - P.r_lo];
+    const long long lo = max(pk.r - w, 0), hi = (long long)pk.r + w;
+    const long long lo2 = lo * lo, hi2 = hi * hi;
+    const int bx0 = max((pk.x - (int)hi) / T1, 0), bx1 = min((pk.x + (int)hi) / T1, P.nbx - 1);
+    const int by0 = max((pk.y - (int)hi) / T1, 0), by1 = min((pk.y + (int)hi) / T1, P.nby - 1);
+    long long n = 0, Su = 0, Sv = 0, Suu = 0, Svv = 0, Suv = 0, Sz = 0, Suz = 0, Svz = 0;
+    for (int by = by0; by <= by1; ++by)
+      for (int bx = bx0; bx <= bx1; ++bx) {
+        const int64_t b = fbins + by * P.nbx + bx;
+        const int cnt = P.bin_count[b];
+        const uint32_t* xy = P.bin_xy + b * P.ridge_cap;
+        for (int k = lane; k < cnt; k += 32) {
+          uint32_t v = xy[k];
+          long long u = (long long)(v & 0xFFFFu) - pk.x, vv = (long long)(v >> 16) - pk.y;
+          long long z = u * u + vv * vv;
+          if (z < lo2 || z > hi2) continue;
+          ++n; Su += u; Sv += vv; Suu += u * u; Svv += vv * vv; Suv += u * vv; Sz += z; Suz += u * z; Svz += vv * z;
+        }
+      }
+    n = warp_sum_ll(n); Su = warp_sum_ll(Su); Sv = warp_sum_ll(Sv); Suu = warp_sum_ll(Suu); Svv = warp_sum_ll(Svv);
+    Suv = warp_sum_ll(Suv); Sz = warp_sum_ll(Sz); Suz = warp_sum_ll(Suz); Svz = warp_sum_ll(Svz);
+    // Kasa: [Suu Suv Su; Suv Svv Sv; Su Sv n] [D E F]^T = -[Suz Svz Sz]^T
+    bool ok = false;
+    double uc = 0, vc = 0, R = 0;
+    if (n >= 3) {
+      __int128 det = det3(Suu, Suv, Su, Suv, Svv, Sv, Su, Sv, n);
+      if (det != 0) {
+        __int128 nD = det3(-Suz, Suv, Su, -Svz, Svv, Sv, -Sz, Sv, n);
+        __int128 nE = det3(Suu, -Suz, Su, Suv, -Svz, Sv, Su, -Sz, n);
+        __int128 nF = det3(Suu, Suv, -Suz, Suv, Svv, -Svz, Su, Sv, -Sz);
+        double dd = (double)det;
+        double D = (double)nD / dd, E = (double)nE / dd, F = (double)nF / dd;
+        uc = -0.5 * D;
+        vc = -0.5 * E;
+        double R2 = uc * uc + vc * vc - F;
+        if (R2 >= 0.0) { R = sqrt(R2); ok = true; }
+      }
+    }
+    double rms = 0.0;
+    if (ok) {
+      double acc = 0.0;
+      for (int by = by0; by <= by1; ++by)
+        for (int bx = bx0; bx <= bx1; ++bx) {
+          const int64_t b = fbins + by * P.nbx + bx;
+          const int cnt = P.bin_count[b];
+          const uint32_t* xy = P.bin_xy + b * P.ridge_cap;
+          for (int k = lane; k < cnt; k += 32) {
+            uint32_t v = xy[k];
+            long long u = (long long)(v & 0xFFFFu) - pk.x, vv = (long long)(v >> 16) - pk.y;
+            long long z = u * u + vv * vv;
+            if (z < lo2 || z > hi2) continue;
+            double du = (double)u - uc, dv = (double)vv - vc;
+            double e = sqrt(du * du + dv * dv) - R;
+            acc += e * e;
+          }
+        }
+      acc = warp_sum_d(acc);
+      rms = sqrt(acc / (double)n);
+    }
+    if (lane == 0) {
+      Ring g;
+      g.cx = pk.x; g.cy = pk.y; g.r = pk.r; g.raw_votes = pk.raw; g.score_fixed = pk.S;
+      g.inliers = (int32_t)n; g.fit_ok = ok ? 1 : 0;
+      g.fx = ok ? pk.x + uc : (double)pk.x;
+      g.fy = ok ? pk.y + vc : (double)pk.y;
+      g.fr = ok ? R : (double)pk.r;
+      g.rms = rms;
+      rings[(int64_t)f * P.ring_cap + p] = g;
+    }
+  }
+  if (tid == 0) {
+    counts[f] = npk;
+    P.stats[f].peaks = (unsigned long long)npk;
+  }
+}
+
+size_t k_fit_smem(const Params& P) { return (size_t)P.ring_cap * (sizeof(Peak) + sizeof(int)); }
+
+cudaError_t launch_fit(int n_frames, const Params& P, void* rings, int* counts, cudaStream_t st) {
+  size_t sm = k_fit_smem(P);
+  cudaFuncSetAttribute(k_fit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_fit<<<n_frames, K3_THREADS, sm, st>>>(P, reinterpret_cast<Ring*>(rings), counts);
+  return cudaGetLastError();
+}
+
+}  // namespace rd

@@ -1,0 +1,529 @@
+// rd_api.cu — the C ABI of librd.so (include/rd.h): validation, host-side level
+// tables, device scratch arena, launch sequence K1 -> K2 -> K3, and the pipelined
+// host-buffer entry point.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "rd.h"
+#include "rd_internal.cuh"
+
+namespace rd {
+size_t k_ridges_smem(int Ks);
+cudaError_t launch_ridges(const void* frames, int64_t pitch, int64_t fstride, int n_frames, const Params& P,
+                          cudaStream_t st);
+cudaError_t launch_eigen(const double* abc, int64_t n, double* out, int* deg, cudaStream_t st);
+size_t k_hough_smem(const Params& P, int max_bins);
+int k_hough_max_bins(const Params& P);
+cudaError_t launch_hough(int n_frames, const Params& P, bool wide, cudaStream_t st);
+size_t k_fit_smem(const Params& P);
+cudaError_t launch_fit(int n_frames, const Params& P, void* rings, int* counts, cudaStream_t st);
+}  // namespace rd
+
+using namespace rd;
+
+static thread_local char g_err[512] = "";
+
+static rd_status cuda_fail(cudaError_t e, const char* where) {
+  snprintf(g_err, sizeof g_err, "%s: %s", where, cudaGetErrorString(e));
+  return RD_ERR_CUDA;
+}
+#define CK(call)                                   \
+  do {                                             \
+    cudaError_t e__ = (call);                      \
+    if (e__ != cudaSuccess) return cuda_fail(e__, #call); \
+  } while (0)
+
+struct rd_detector {
+  rd_config cfg;
+  int device;
+  int max_batch;
+  Params P;
+  bool wide;
+  // device allocations
+  void* d_tables = nullptr;
+  void* d_bins_count = nullptr;
+  void* d_bins_xy = nullptr;
+  void* d_bins_d = nullptr;
+  void* d_peaks = nullptr;
+  void* d_counters = nullptr;  // stats | peak_count | flags | dbg_count
+  size_t counters_bytes = 0;
+  void* d_dbg = nullptr;
+  // host-path staging
+  int chunk = 0;
+  void* d_stage[2] = {nullptr, nullptr};
+  void* d_rings_stage[2] = {nullptr, nullptr};
+  int* d_counts_stage[2] = {nullptr, nullptr};
+  cudaStream_t s_comp = nullptr, s_h2d = nullptr, s_d2h = nullptr;
+  cudaEvent_t ev_h2d[2], ev_done[2], ev_d2h[2];
+  cudaEvent_t ev_last = nullptr;
+  bool timing = false;
+  std::vector<cudaEvent_t> tev;  // 4 per timed call
+  int n_timed = 0;
+  bool have_last = false;
+  int last_n = 0;
+};
+
+extern "C" {
+
+int32_t rd_abi_version(void) { return RD_ABI_VERSION; }
+
+const char* rd_status_string(rd_status s) {
+  switch (s) {
+    case RD_OK: return "ok";
+    case RD_ERR_PARAM: return "invalid parameter";
+    case RD_ERR_DIM: return "unsupported frame dimensions";
+    case RD_ERR_CONFIG: return "inconsistent configuration";
+    case RD_ERR_CAPACITY: return "device capacity overflow (see rd_query_overflow)";
+    case RD_ERR_CUDA: return "CUDA error (see rd_last_error)";
+    case RD_ERR_STATE: return "call out of order";
+  }
+  return "unknown status";
+}
+
+const char* rd_last_error(void) { return g_err; }
+
+rd_status rd_config_init(rd_config* c, int32_t width, int32_t height, int32_t pixel) {
+  if (!c) return RD_ERR_PARAM;
+  memset(c, 0, sizeof *c);
+  c->width = width;
+  c->height = height;
+  c->pixel = pixel;
+  c->max_value = pixel == RD_U8 ? 255 : 65535;
+  c->smoothing_sigma = 1.5;
+  c->curvature_threshold = -10.0;
+  c->r_min = 8;
+  c->r_max = 70;
+  c->vote_threshold_raw = 3;
+  c->vote_threshold_norm = 0.5;
+  c->sig_a = 1;
+  c->sig_b = 5;
+  c->sig_den = 20;
+  c->annulus_halfwidth = 0;
+  c->max_rings_per_frame = 1024;
+  c->max_ridges_per_tile = 512;
+  c->max_entries_per_tile = 2048;
+  c->max_hotspots_per_level = 512;
+  c->debug = 0;
+  return RD_OK;
+}
+
+static rd_status validate(const rd_config* c) {
+  if (c->width < 8 || c->height < 8 || c->width > 16384 || c->height > 16384) return RD_ERR_DIM;
+  if (c->pixel != RD_U8 && c->pixel != RD_U16) return RD_ERR_PARAM;
+  if (c->max_value < 1 || c->max_value > (c->pixel == RD_U8 ? 255 : 65535)) return RD_ERR_PARAM;
+  if (!(c->smoothing_sigma > 0.0) || !(c->smoothing_sigma <= 5.0)) return RD_ERR_PARAM;
+  if (!(c->curvature_threshold <= 0.0) || !std::isfinite(c->curvature_threshold)) return RD_ERR_PARAM;
+  if (c->r_min < 2 || c->r_max <= c->r_min || c->r_max > 1000) return RD_ERR_PARAM;
+  if (c->vote_threshold_raw < 1 || c->vote_threshold_raw > 60000) return RD_ERR_PARAM;
+  if (!(c->vote_threshold_norm > 0.0) || !std::isfinite(c->vote_threshold_norm)) return RD_ERR_PARAM;
+  if (c->sig_a < 0 || c->sig_den < 1 || (int64_t)c->sig_a * (c->r_min - 1) + c->sig_b <= 0) return RD_ERR_PARAM;
+  if (c->annulus_halfwidth < 0) return RD_ERR_PARAM;
+  if (c->max_rings_per_frame < 0 || c->max_ridges_per_tile < 0 || c->max_entries_per_tile < 0 ||
+      c->max_hotspots_per_level < 0)
+    return RD_ERR_PARAM;
+  return RD_OK;
+}
+
+rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_detector** out) {
+  if (!cin || !out || max_batch < 1) return RD_ERR_PARAM;
+  *out = nullptr;
+  rd_status st = validate(cin);
+  if (st != RD_OK) return st;
+  rd_config c = *cin;
+  if (!c.max_rings_per_frame) c.max_rings_per_frame = 1024;
+  if (!c.max_ridges_per_tile) c.max_ridges_per_tile = 512;
+  if (!c.max_entries_per_tile) c.max_entries_per_tile = 2048;
+  if (!c.max_hotspots_per_level) c.max_hotspots_per_level = 512;
+  if (c.max_ridges_per_tile > T1 * T1) c.max_ridges_per_tile = T1 * T1;
+  if (c.max_hotspots_per_level > 65535) return RD_ERR_PARAM;
+
+  // ---- host tables (DESIGN.md §2 A1, A5, A7, A8, A9)
+  Params P;
+  memset(&P, 0, sizeof P);
+  P.W = c.width;
+  P.H = c.height;
+  P.pixel_bytes = c.pixel == RD_U8 ? 1 : 2;
+  const double s = c.smoothing_sigma;
+  P.Ks = (int)std::ceil(3.0 * s);
+  if (P.Ks > KS_MAX) return RD_ERR_PARAM;
+  int64_t sq = 0;
+  for (int i = -P.Ks; i <= P.Ks; ++i) {
+    P.q[i + P.Ks] = (int)llround(1024.0 * std::exp(-(double)(i * i) / (2.0 * s * s)));
+    sq += P.q[i + P.Ks];
+  }
+  // exactness bounds: int32 row pass, fp64-exact smoothing and Hessian
+  if ((int64_t)c.max_value * sq >= (int64_t(1) << 31)) return RD_ERR_CONFIG;
+  if ((double)c.max_value * (double)sq * (double)sq * 64.0 >= 9007199254740992.0) return RD_ERR_CONFIG;
+  P.t_int = c.curvature_threshold * (64.0 * (double)sq * (double)sq);
+  P.r_min = c.r_min;
+  P.r_max = c.r_max;
+  P.r_lo = c.r_min - 1;
+  P.r_hi = c.r_max + 1;
+  P.n_levels = P.r_hi - P.r_lo + 1;
+  P.T_raw = c.vote_threshold_raw;
+  std::vector<int> lvlK(P.n_levels), lvlAnn(P.n_levels);
+  std::vector<double> lvlTn(P.n_levels);
+  int Kmax = 0;
+  for (int li = 0; li < P.n_levels; ++li) {
+    int r = P.r_lo + li;
+    int64_t sr = (int64_t)c.sig_a * r + c.sig_b;
+    lvlK[li] = (int)((3 * sr + c.sig_den - 1) / c.sig_den);
+    Kmax = std::max(Kmax, lvlK[li]);
+    lvlTn[li] = ((c.vote_threshold_norm * (2.0 * M_PI)) * 16777216.0) * (double)r;
+    if (c.annulus_halfwidth > 0) lvlAnn[li] = c.annulus_halfwidth;
+    else lvlAnn[li] = std::max<int>(2, (int)((2 * sr + c.sig_den - 1) / c.sig_den));
+  }
+  if (Kmax > 48) return RD_ERR_CONFIG;  // raw tile halo bound (shared memory)
+  P.K_max = Kmax;
+  P.hal = Kmax + 1;
+  P.wstride = Kmax + 1;
+  std::vector<int> lvlW((size_t)P.n_levels * P.wstride, 0);
+  double max_wsum = 0;
+  for (int li = 0; li < P.n_levels; ++li) {
+    int r = P.r_lo + li;
+    int64_t sr = (int64_t)c.sig_a * r + c.sig_b;
+    double den = 2.0 * (double)(sr * sr);
+    double wsum = 0;
+    for (int d = 0; d <= lvlK[li]; ++d) {
+      double num = (double)((int64_t)d * d * c.sig_den * c.sig_den);
+      int w = (int)llround(4096.0 * std::exp(-num / den));
+      lvlW[(size_t)li * P.wstride + d] = w;
+      wsum += (d ? 2.0 : 1.0) * w;
+    }
+    max_wsum = std::max(max_wsum, wsum);
+  }
+  bool wide = 65535.0 * max_wsum >= 4294967296.0;
+
+  rd_detector* det = new rd_detector();
+  det->cfg = c;
+  det->device = device;
+  det->max_batch = max_batch;
+  det->wide = wide;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) { delete det; return cuda_fail(e, "cudaSetDevice"); }
+
+  P.nbx = (c.width + T1 - 1) / T1;
+  P.nby = (c.height + T1 - 1) / T1;
+  P.ridge_cap = c.max_ridges_per_tile;
+  P.ntx = (c.width + T2 - 1) / T2;
+  P.nty = (c.height + T2 - 1) / T2;
+  P.entry_cap = c.max_entries_per_tile;
+  P.hot_cap = c.max_hotspots_per_level;
+  P.ring_cap = c.max_rings_per_frame;
+  P.debug = c.debug;
+  P.dbg_cap = c.debug ? (1 << 20) : 0;
+
+  // shared-memory feasibility
+  cudaDeviceProp prop;
+  e = cudaGetDeviceProperties(&prop, device);
+  if (e != cudaSuccess) { delete det; return cuda_fail(e, "cudaGetDeviceProperties"); }
+  size_t smax = prop.sharedMemPerBlockOptin;
+  if (k_ridges_smem(P.Ks) > smax || k_hough_smem(P, k_hough_max_bins(P)) > smax || k_fit_smem(P) > smax) {
+    delete det;
+    snprintf(g_err, sizeof g_err, "shared memory: K1 %zu K2 %zu K3 %zu > %zu", k_ridges_smem(P.Ks),
+             k_hough_smem(P, k_hough_max_bins(P)), k_fit_smem(P), smax);
+    return RD_ERR_CONFIG;
+  }
+
+  const int64_t B = max_batch, nbins = (int64_t)P.nbx * P.nby;
+  size_t tb = sizeof(int) * P.n_levels * 2 + sizeof(double) * P.n_levels + sizeof(int) * lvlW.size() + 64;
+#define ALLOC(ptr, bytes)                                          \
+  do {                                                             \
+    e = cudaMalloc(&(ptr), (bytes));                               \
+    if (e != cudaSuccess) { rd_destroy(det); return cuda_fail(e, "cudaMalloc " #ptr); } \
+  } while (0)
+  ALLOC(det->d_tables, tb);
+  ALLOC(det->d_bins_count, sizeof(int) * B * nbins);
+  ALLOC(det->d_bins_xy, sizeof(uint32_t) * B * nbins * P.ridge_cap);
+  ALLOC(det->d_bins_d, sizeof(double2) * B * nbins * P.ridge_cap);
+  ALLOC(det->d_peaks, sizeof(Peak) * B * P.ring_cap);
+  det->counters_bytes = sizeof(Stats) * B + sizeof(int) * 3 * B;
+  ALLOC(det->d_counters, det->counters_bytes);
+  if (c.debug) ALLOC(det->d_dbg, sizeof(HotRec) * B * P.dbg_cap);
+  // tables
+  {
+    std::vector<unsigned char> h(tb, 0);
+    size_t o = 0;
+    memcpy(h.data() + o, lvlTn.data(), sizeof(double) * P.n_levels);
+    P.lvlTn = reinterpret_cast<const double*>((char*)det->d_tables + o);
+    o += sizeof(double) * P.n_levels;
+    memcpy(h.data() + o, lvlK.data(), sizeof(int) * P.n_levels);
+    P.lvlK = reinterpret_cast<const int*>((char*)det->d_tables + o);
+    o += sizeof(int) * P.n_levels;
+    memcpy(h.data() + o, lvlAnn.data(), sizeof(int) * P.n_levels);
+    P.lvlAnn = reinterpret_cast<const int*>((char*)det->d_tables + o);
+    o += sizeof(int) * P.n_levels;
+    memcpy(h.data() + o, lvlW.data(), sizeof(int) * lvlW.size());
+    P.lvlW = reinterpret_cast<const int*>((char*)det->d_tables + o);
+    e = cudaMemcpy(det->d_tables, h.data(), tb, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) { rd_destroy(det); return cuda_fail(e, "cudaMemcpy tables"); }
+  }
+  P.bin_count = (int*)det->d_bins_count;
+  P.bin_xy = (uint32_t*)det->d_bins_xy;
+  P.bin_d = (double2*)det->d_bins_d;
+  P.peaks = (Peak*)det->d_peaks;
+  P.stats = (Stats*)det->d_counters;
+  P.peak_count = (int*)((char*)det->d_counters + sizeof(Stats) * B);
+  P.flags = P.peak_count + B;
+  P.dbg_count = P.flags + B;
+  P.dbg_hot = (HotRec*)det->d_dbg;
+  det->P = P;
+  e = cudaEventCreateWithFlags(&det->ev_last, cudaEventDisableTiming);
+  if (e != cudaSuccess) { rd_destroy(det); return cuda_fail(e, "cudaEventCreate"); }
+  *out = det;
+  return RD_OK;
+}
+
+rd_status rd_destroy(rd_detector* det) {
+  if (!det) return RD_OK;
+  cudaSetDevice(det->device);
+  cudaFree(det->d_tables);
+  cudaFree(det->d_bins_count);
+  cudaFree(det->d_bins_xy);
+  cudaFree(det->d_bins_d);
+  cudaFree(det->d_peaks);
+  cudaFree(det->d_counters);
+  cudaFree(det->d_dbg);
+  for (int i = 0; i < 2; ++i) {
+    cudaFree(det->d_stage[i]);
+    cudaFree(det->d_rings_stage[i]);
+    cudaFree(det->d_counts_stage[i]);
+  }
+  if (det->s_comp) {
+    cudaStreamDestroy(det->s_comp);
+    cudaStreamDestroy(det->s_h2d);
+    cudaStreamDestroy(det->s_d2h);
+    for (int i = 0; i < 2; ++i) {
+      cudaEventDestroy(det->ev_h2d[i]);
+      cudaEventDestroy(det->ev_done[i]);
+      cudaEventDestroy(det->ev_d2h[i]);
+    }
+  }
+  if (det->ev_last) cudaEventDestroy(det->ev_last);
+  for (cudaEvent_t e : det->tev) cudaEventDestroy(e);
+  delete det;
+  return RD_OK;
+}
+
+static rd_status detect_impl(rd_detector* det, const void* d_frames, int64_t pitch, int64_t fstride, int n,
+                             void* d_rings, int* d_counts, cudaStream_t st) {
+  const Params& P = det->P;
+  cudaEvent_t* ev = nullptr;
+  if (det->timing) {
+    size_t need = 4 * (size_t)(det->n_timed + 1);
+    while (det->tev.size() < need) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      det->tev.push_back(e);
+    }
+    ev = &det->tev[4 * (size_t)det->n_timed];
+    det->n_timed++;
+  }
+  CK(cudaMemsetAsync(det->d_counters, 0, det->counters_bytes, st));
+  if (ev) CK(cudaEventRecord(ev[0], st));
+  CK(launch_ridges(d_frames, pitch, fstride, n, P, st));
+  if (ev) CK(cudaEventRecord(ev[1], st));
+  CK(launch_hough(n, P, det->wide, st));
+  if (ev) CK(cudaEventRecord(ev[2], st));
+  CK(launch_fit(n, P, d_rings, d_counts, st));
+  if (ev) CK(cudaEventRecord(ev[3], st));
+  CK(cudaEventRecord(det->ev_last, st));
+  det->have_last = true;
+  det->last_n = n;
+  return RD_OK;
+}
+
+static rd_status check_frames(rd_detector* det, const void* frames, int64_t pitch, int64_t fstride, int n) {
+  if (!det || !frames) return RD_ERR_PARAM;
+  const int pb = det->P.pixel_bytes;
+  if (pitch < (int64_t)det->cfg.width * pb || (pitch % pb)) return RD_ERR_PARAM;
+  if (n > 1 && fstride < pitch * det->cfg.height) return RD_ERR_PARAM;
+  if (((uintptr_t)frames % pb) || (fstride % pb)) return RD_ERR_PARAM;
+  return RD_OK;
+}
+
+rd_status rd_detect(rd_detector* det, const void* d_frames, int64_t pitch, int64_t fstride, int32_t n,
+                    rd_ring* d_rings, int32_t* d_counts, void* stream) {
+  if (!det || n < 1 || n > det->max_batch || !d_rings || !d_counts) return RD_ERR_PARAM;
+  rd_status s = check_frames(det, d_frames, pitch, fstride, n);
+  if (s != RD_OK) return s;
+  CK(cudaSetDevice(det->device));
+  return detect_impl(det, d_frames, pitch, fstride, n, d_rings, d_counts, (cudaStream_t)stream);
+}
+
+static rd_status ensure_host_path(rd_detector* det) {
+  if (det->s_comp) return RD_OK;
+  det->chunk = std::min(det->max_batch, 32);
+  const size_t fbytes = (size_t)det->cfg.width * det->cfg.height * det->P.pixel_bytes;
+  for (int i = 0; i < 2; ++i) {
+    CK(cudaMalloc(&det->d_stage[i], fbytes * det->chunk));
+    CK(cudaMalloc(&det->d_rings_stage[i], sizeof(rd_ring) * det->chunk * det->P.ring_cap));
+    CK(cudaMalloc(&det->d_counts_stage[i], sizeof(int) * det->chunk));
+    CK(cudaEventCreateWithFlags(&det->ev_h2d[i], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&det->ev_done[i], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&det->ev_d2h[i], cudaEventDisableTiming));
+  }
+  CK(cudaStreamCreateWithFlags(&det->s_comp, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&det->s_h2d, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&det->s_d2h, cudaStreamNonBlocking));
+  return RD_OK;
+}
+
+rd_status rd_detect_host(rd_detector* det, const void* h_frames, int64_t pitch, int64_t fstride, int32_t n,
+                         rd_ring* h_rings, int32_t* h_counts) {
+  if (!det || n < 1 || !h_rings || !h_counts) return RD_ERR_PARAM;
+  rd_status s = check_frames(det, h_frames, pitch, fstride, n);
+  if (s != RD_OK) return s;
+  CK(cudaSetDevice(det->device));
+  s = ensure_host_path(det);
+  if (s != RD_OK) return s;
+  const int W = det->cfg.width, H = det->cfg.height, pb = det->P.pixel_bytes;
+  const size_t row = (size_t)W * pb, fbytes = row * H;
+  const int C = det->chunk, rc = det->P.ring_cap;
+  const int nchunks = (n + C - 1) / C;
+  rd_status result = RD_OK;
+  for (int k = 0; k < nchunks; ++k) {
+    const int b = k & 1, f0 = k * C, m = std::min(C, n - f0);
+    // H2D of chunk k may overwrite stage b only after chunk k-2 finished computing
+    if (k >= 2) CK(cudaStreamWaitEvent(det->s_h2d, det->ev_done[b], 0));
+    const char* src = (const char*)h_frames + (size_t)f0 * fstride;
+    if (pitch == (int64_t)row && fstride == (int64_t)fbytes) {
+      CK(cudaMemcpyAsync(det->d_stage[b], src, fbytes * m, cudaMemcpyHostToDevice, det->s_h2d));
+    } else {
+      for (int i = 0; i < m; ++i)
+        CK(cudaMemcpy2DAsync((char*)det->d_stage[b] + fbytes * i, row, src + (size_t)i * fstride, pitch, row, H,
+                             cudaMemcpyHostToDevice, det->s_h2d));
+    }
+    CK(cudaEventRecord(det->ev_h2d[b], det->s_h2d));
+    CK(cudaStreamWaitEvent(det->s_comp, det->ev_h2d[b], 0));
+    // the ring stage b is reused only after its previous D2H completed
+    if (k >= 2) CK(cudaStreamWaitEvent(det->s_comp, det->ev_d2h[b], 0));
+    s = detect_impl(det, det->d_stage[b], row, fbytes, m, det->d_rings_stage[b], det->d_counts_stage[b],
+                    det->s_comp);
+    if (s != RD_OK) return s;
+    CK(cudaEventRecord(det->ev_done[b], det->s_comp));
+    CK(cudaStreamWaitEvent(det->s_d2h, det->ev_done[b], 0));
+    CK(cudaMemcpyAsync(h_rings + (size_t)f0 * rc, det->d_rings_stage[b], sizeof(rd_ring) * (size_t)m * rc,
+                       cudaMemcpyDeviceToHost, det->s_d2h));
+    CK(cudaMemcpyAsync(h_counts + f0, det->d_counts_stage[b], sizeof(int) * m, cudaMemcpyDeviceToHost,
+                       det->s_d2h));
+    CK(cudaEventRecord(det->ev_d2h[b], det->s_d2h));
+  }
+  CK(cudaStreamSynchronize(det->s_d2h));
+  CK(cudaStreamSynchronize(det->s_comp));
+  for (int i = 0; i < n; ++i)
+    if (h_counts[i] < 0) result = RD_ERR_CAPACITY;
+  return result;
+}
+
+rd_status rd_sync(rd_detector* det) {
+  if (!det) return RD_ERR_PARAM;
+  if (!det->have_last) return RD_ERR_STATE;
+  CK(cudaSetDevice(det->device));
+  CK(cudaEventSynchronize(det->ev_last));
+  std::vector<int> fl(det->last_n);
+  CK(cudaMemcpy(fl.data(), det->P.flags, sizeof(int) * det->last_n, cudaMemcpyDeviceToHost));
+  for (int v : fl)
+    if (v) return RD_ERR_CAPACITY;
+  return RD_OK;
+}
+
+rd_status rd_query_overflow(rd_detector* det, int32_t n, int32_t* h_flags) {
+  if (!det || !h_flags || n < 1 || n > det->max_batch) return RD_ERR_PARAM;
+  if (!det->have_last) return RD_ERR_STATE;
+  CK(cudaSetDevice(det->device));
+  CK(cudaEventSynchronize(det->ev_last));
+  CK(cudaMemcpy(h_flags, det->P.flags, sizeof(int) * n, cudaMemcpyDeviceToHost));
+  return RD_OK;
+}
+
+rd_status rd_get_stats(rd_detector* det, int32_t n, rd_frame_stats* h) {
+  if (!det || !h || n < 1 || n > det->max_batch) return RD_ERR_PARAM;
+  if (!det->have_last) return RD_ERR_STATE;
+  static_assert(sizeof(rd_frame_stats) == sizeof(Stats), "stats layout");
+  CK(cudaSetDevice(det->device));
+  CK(cudaEventSynchronize(det->ev_last));
+  CK(cudaMemcpy(h, det->P.stats, sizeof(Stats) * n, cudaMemcpyDeviceToHost));
+  return RD_OK;
+}
+
+rd_status rd_dump_ridges(rd_detector* det, int32_t frame, rd_ridge* h_out, int64_t cap, int64_t* n_out) {
+  if (!det || !n_out || frame < 0 || frame >= det->max_batch || (cap > 0 && !h_out)) return RD_ERR_PARAM;
+  if (!det->have_last) return RD_ERR_STATE;
+  CK(cudaSetDevice(det->device));
+  CK(cudaEventSynchronize(det->ev_last));
+  const Params& P = det->P;
+  const int64_t nb = (int64_t)P.nbx * P.nby;
+  std::vector<int> cnt(nb);
+  std::vector<uint32_t> xy((size_t)nb * P.ridge_cap);
+  std::vector<double2> d((size_t)nb * P.ridge_cap);
+  CK(cudaMemcpy(cnt.data(), P.bin_count + frame * nb, sizeof(int) * nb, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(xy.data(), P.bin_xy + frame * nb * P.ridge_cap, sizeof(uint32_t) * xy.size(),
+                cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(d.data(), P.bin_d + frame * nb * P.ridge_cap, sizeof(double2) * d.size(), cudaMemcpyDeviceToHost));
+  int64_t k = 0;
+  for (int64_t b = 0; b < nb; ++b)
+    for (int i = 0; i < cnt[b]; ++i, ++k)
+      if (k < cap) {
+        uint32_t v = xy[b * P.ridge_cap + i];
+        h_out[k].x = (int32_t)(v & 0xFFFFu);
+        h_out[k].y = (int32_t)(v >> 16);
+        h_out[k].dx = d[b * P.ridge_cap + i].x;
+        h_out[k].dy = d[b * P.ridge_cap + i].y;
+      }
+  *n_out = k;
+  return RD_OK;
+}
+
+rd_status rd_dump_hotspots(rd_detector* det, int32_t frame, rd_hotspot* h_out, int64_t cap, int64_t* n_out) {
+  if (!det || !n_out || frame < 0 || frame >= det->max_batch || (cap > 0 && !h_out)) return RD_ERR_PARAM;
+  if (!det->have_last || !det->cfg.debug) return RD_ERR_STATE;
+  static_assert(sizeof(rd_hotspot) == sizeof(HotRec), "hotspot layout");
+  CK(cudaSetDevice(det->device));
+  CK(cudaEventSynchronize(det->ev_last));
+  int n = 0;
+  CK(cudaMemcpy(&n, det->P.dbg_count + frame, sizeof(int), cudaMemcpyDeviceToHost));
+  int64_t m = std::min<int64_t>(std::min<int64_t>(n, det->P.dbg_cap), cap);
+  if (m > 0)
+    CK(cudaMemcpy(h_out, det->P.dbg_hot + (int64_t)frame * det->P.dbg_cap, sizeof(HotRec) * m,
+                  cudaMemcpyDeviceToHost));
+  *n_out = n;
+  return RD_OK;
+}
+
+rd_status rd_set_timing(rd_detector* det, int32_t on) {
+  if (!det) return RD_ERR_PARAM;
+  CK(cudaSetDevice(det->device));
+  if (det->n_timed) CK(cudaDeviceSynchronize());
+  det->timing = on != 0;
+  det->n_timed = 0;
+  return RD_OK;
+}
+
+rd_status rd_kernel_times(rd_detector* det, float* h_ms, int32_t* n_calls) {
+  if (!det || !h_ms || !n_calls) return RD_ERR_PARAM;
+  CK(cudaSetDevice(det->device));
+  float acc[3] = {0, 0, 0};
+  for (int c = 0; c < det->n_timed; ++c) {
+    cudaEvent_t* ev = &det->tev[4 * (size_t)c];
+    CK(cudaEventSynchronize(ev[3]));
+    for (int k = 0; k < 3; ++k) {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, ev[k], ev[k + 1]));
+      acc[k] += ms;
+    }
+  }
+  for (int k = 0; k < 3; ++k) h_ms[k] = acc[k];
+  *n_calls = det->n_timed;
+  return RD_OK;
+}
+
+rd_status rd_eigen(const double* d_abc, int64_t n, double* d_out, int32_t* d_deg, void* stream) {
+  if (n < 0 || (n > 0 && (!d_abc || !d_out || !d_deg))) return RD_ERR_PARAM;
+  CK(launch_eigen(d_abc, n, d_out, d_deg, (cudaStream_t)stream));
+  return RD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,96 @@
+// rd_internal.cuh — shared definitions of the librd.so kernels (sm_100a).
+// Product code: independent of oracle/ (no shared source, tables or constants).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rd {
+
+constexpr int T1 = 32;          // K1 (ridge) tile: 32x32 output pixels; also the ridge-bin size
+constexpr int T2 = 64;          // K2 (Hough) tile: 64x64 accumulator cells (2x2 ridge bins)
+constexpr int KS_MAX = 15;      // smoothing half-width limit (sigma_s <= 5)
+constexpr int K1_THREADS = 256;
+constexpr int K2_THREADS = 256;
+constexpr int K3_THREADS = 256;
+
+// Per-frame overflow flag bits (rd_query_overflow)
+constexpr int OVF_RIDGES = 1, OVF_ENTRIES = 2, OVF_HOTSPOTS = 4, OVF_RINGS = 8, OVF_DEBUG = 16;
+
+struct Peak {          // peak record produced by K2, consumed by K3 (24 B)
+  int32_t x, y, r, raw;
+  int64_t S;
+};
+
+struct HotRec {        // debug hotspot record (24 B), same layout as rd_hotspot
+  int32_t r, y, x, raw;
+  int64_t S;
+};
+
+struct Stats {         // per-frame counters (same layout as rd_frame_stats)
+  unsigned long long ridges, votes, hotspots, peaks;
+};
+
+// Everything the kernels need, passed by value (< 4 KB).
+struct Params {
+  int W, H, pixel_bytes;
+  int Ks;
+  int q[2 * KS_MAX + 1];        // smoothing taps, 2^10 fixed point (A1)
+  double t_int;                 // curvature threshold in integer-Hessian units
+  int r_lo, r_hi, r_min, r_max, n_levels;
+  int T_raw;
+  int K_max;                    // largest level half-width
+  int hal;                      // K2 raw halo = K_max + 1
+  // level tables (device, n_levels entries, index r - r_lo)
+  const int* lvlK;              // K_r
+  const int* lvlW;              // [n_levels][WSTRIDE] w_r(0..K_r), 2^12 fixed point
+  const double* lvlTn;          // T_norm(r) in S units
+  const int* lvlAnn;            // annulus half-width w(r)
+  int wstride;
+  // ridge bins (K1 output)
+  int nbx, nby;                 // 32x32 bins per frame
+  int ridge_cap;                // per bin
+  int* bin_count;               // [F][nby*nbx]
+  uint32_t* bin_xy;             // [F][bins][ridge_cap] x | y<<16
+  double2* bin_d;               // [F][bins][ridge_cap] (dx, dy)
+  // Hough tiles (K2)
+  int ntx, nty;                 // 64x64 tiles per frame
+  int entry_cap, hot_cap;
+  int ring_cap;
+  Peak* peaks;                  // [F][ring_cap]
+  int* peak_count;              // [F]
+  int* flags;                   // [F] overflow bits
+  Stats* stats;                 // [F]
+  int debug;
+  int dbg_cap;
+  HotRec* dbg_hot;              // [F][dbg_cap]
+  int* dbg_count;               // [F]
+};
+
+// ---------------------------------------------------------------- fp64 recipe (A3)
+// kappa = 0.5*(T - sqrt(e*e + 4*(b*b))) and the unit eigenvector, each operation
+// rounded separately (no FMA contraction): DESIGN.md A3 / PAPER.md:301-303.
+__device__ __forceinline__ double kappa_of(double a, double b, double c, double* s_out, double* e_out) {
+  double T = __dadd_rn(a, c);
+  double e = __dsub_rn(a, c);
+  double D = __dadd_rn(__dmul_rn(e, e), __dmul_rn(4.0, __dmul_rn(b, b)));
+  double s = __dsqrt_rn(D);
+  *s_out = s;
+  *e_out = e;
+  return __dmul_rn(0.5, __dsub_rn(T, s));
+}
+// returns false if degenerate (e == 0 and b == 0)
+__device__ __forceinline__ bool direction_of(double b, double e, double s, double* dx, double* dy) {
+  if (e == 0.0 && b == 0.0) { *dx = 0.0; *dy = 0.0; return false; }
+  double vx, vy;
+  if (e >= 0.0) { vx = -b; vy = __dmul_rn(0.5, __dadd_rn(e, s)); }
+  else { vx = __dmul_rn(0.5, __dsub_rn(s, e)); vy = -b; }
+  double n = __dsqrt_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)));
+  *dx = __ddiv_rn(vx, n);
+  *dy = __ddiv_rn(vy, n);
+  return true;
+}
+
+// round half away from zero of an exactly computed double (llround semantics)
+__device__ __forceinline__ int round_half_away(double v) { return (int)llround(v); }
+
+}  // namespace rd

@@ -1,0 +1,155 @@
+"""Detector: Python face of rd_create / rd_detect / rd_detect_host (include/rd.h)."""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _rd
+from ._rd import HOT_DTYPE, RIDGE_DTYPE, RING_DTYPE, STATS_DTYPE, check, lib
+
+_CFG_KEYS = ("max_value", "smoothing_sigma", "curvature_threshold", "r_min", "r_max", "vote_threshold_raw",
+             "vote_threshold_norm", "sig_a", "sig_b", "sig_den", "annulus_halfwidth", "max_rings_per_frame",
+             "max_ridges_per_tile", "max_entries_per_tile", "max_hotspots_per_level", "debug")
+
+
+class Detector:
+    """One rd_detector on one CUDA device.
+
+    params: width, height, pixel_bytes plus any rd_config field (see include/rd.h).
+    """
+
+    def __init__(self, params: dict, max_batch: int = 1, device: int = 0):
+        self.params = dict(params)
+        self.width, self.height = int(params["width"]), int(params["height"])
+        self.pixel_bytes = int(params["pixel_bytes"])
+        self.max_batch = int(max_batch)
+        self.device = int(device)
+        self.cfg = _rd.make_config(self.width, self.height, self.pixel_bytes,
+                                   **{k: params[k] for k in _CFG_KEYS if k in params})
+        self.ring_cap = self.cfg.max_rings_per_frame or 1024
+        h = C.c_void_p()
+        check(lib().rd_create(C.byref(self.cfg), self.max_batch, self.device, C.byref(h)), "rd_create")
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().rd_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def frame_dtype(self):
+        return torch.uint8 if self.pixel_bytes == 1 else torch.uint16
+
+    def alloc_outputs(self, n: int):
+        dev = torch.device("cuda", self.device)
+        rings = torch.empty((n, self.ring_cap, RING_DTYPE.itemsize), dtype=torch.uint8, device=dev)
+        counts = torch.empty((n,), dtype=torch.int32, device=dev)
+        return rings, counts
+
+    def detect(self, frames: torch.Tensor, rings: torch.Tensor | None = None, counts: torch.Tensor | None = None,
+               stream: torch.cuda.Stream | None = None):
+        """frames: CUDA tensor [N, H, W] (uint8/uint16, row-contiguous).  Asynchronous on `stream`
+        (default: torch's current stream).  Returns (rings [N, cap, 64] uint8, counts [N] int32)."""
+        if frames.dim() == 2:
+            frames = frames.unsqueeze(0)
+        n, H, W = frames.shape
+        assert (H, W) == (self.height, self.width) and frames.dtype == self.frame_dtype and frames.is_cuda
+        assert frames.stride(2) == 1
+        if rings is None or counts is None:
+            rings, counts = self.alloc_outputs(n)
+        st = stream if stream is not None else torch.cuda.current_stream(frames.device)
+        es = frames.element_size()
+        check(lib().rd_detect(self._h, frames.data_ptr(), frames.stride(1) * es, frames.stride(0) * es, n,
+                              rings.data_ptr(), counts.data_ptr(), C.c_void_p(st.cuda_stream)), "rd_detect")
+        return rings, counts
+
+    def detect_host(self, frames, rings: np.ndarray | None = None, counts: np.ndarray | None = None):
+        """End-to-end on host buffers (numpy or CPU torch tensor, pinned recommended): the library
+        copies frames in, detects and copies rings back, overlapping copies with compute."""
+        if isinstance(frames, torch.Tensor):
+            assert not frames.is_cuda
+            ptr, n = frames.data_ptr(), frames.shape[0]
+            es = frames.element_size()
+            pitch, fstride = frames.stride(1) * es, frames.stride(0) * es
+        else:
+            frames = np.ascontiguousarray(frames)
+            ptr, n = frames.ctypes.data, frames.shape[0]
+            pitch, fstride = frames.strides[1], frames.strides[0]
+        if rings is None:
+            rings = np.empty((n, self.ring_cap), dtype=RING_DTYPE)
+        if counts is None:
+            counts = np.empty(n, dtype=np.int32)
+        rptr = rings.data_ptr() if isinstance(rings, torch.Tensor) else rings.ctypes.data
+        cptr = counts.data_ptr() if isinstance(counts, torch.Tensor) else counts.ctypes.data
+        st = lib().rd_detect_host(self._h, ptr, pitch, fstride, n, rptr, cptr)
+        if st not in (_rd.RD_OK, _rd.RD_ERR_CAPACITY):
+            check(st, "rd_detect_host")
+        return rings, counts
+
+    def sync(self, raise_on_overflow=True):
+        st = lib().rd_sync(self._h)
+        if st == _rd.RD_ERR_CAPACITY and not raise_on_overflow:
+            return st
+        check(st, "rd_sync")
+        return st
+
+    def overflow(self, n: int) -> np.ndarray:
+        out = np.zeros(n, np.int32)
+        check(lib().rd_query_overflow(self._h, n, out.ctypes.data), "rd_query_overflow")
+        return out
+
+    def stats(self, n: int) -> np.ndarray:
+        out = np.zeros(n, STATS_DTYPE)
+        check(lib().rd_get_stats(self._h, n, out.ctypes.data), "rd_get_stats")
+        return out
+
+    def dump_ridges(self, frame: int) -> np.ndarray:
+        n = C.c_int64()
+        check(lib().rd_dump_ridges(self._h, frame, None, 0, C.byref(n)), "rd_dump_ridges")
+        out = np.zeros(n.value, RIDGE_DTYPE)
+        check(lib().rd_dump_ridges(self._h, frame, out.ctypes.data if n.value else None, n.value, C.byref(n)),
+              "rd_dump_ridges")
+        return out
+
+    def dump_hotspots(self, frame: int) -> np.ndarray:
+        n = C.c_int64()
+        check(lib().rd_dump_hotspots(self._h, frame, None, 0, C.byref(n)), "rd_dump_hotspots")
+        out = np.zeros(n.value, HOT_DTYPE)
+        check(lib().rd_dump_hotspots(self._h, frame, out.ctypes.data if n.value else None, n.value, C.byref(n)),
+              "rd_dump_hotspots")
+        return out
+
+    def set_timing(self, on: bool):
+        check(lib().rd_set_timing(self._h, 1 if on else 0), "rd_set_timing")
+
+    def kernel_times(self):
+        """(ms per kernel [K1 ridges, K2 hough, K3 fit] summed over timed calls, n_calls)."""
+        ms = (C.c_float * 3)()
+        n = C.c_int32()
+        check(lib().rd_kernel_times(self._h, ms, C.byref(n)), "rd_kernel_times")
+        return [ms[0], ms[1], ms[2]], n.value
+
+    @staticmethod
+    def rings_to_numpy(rings: torch.Tensor, counts: torch.Tensor) -> list[np.ndarray]:
+        r = rings.cpu().numpy().reshape(rings.shape[0], -1).view(RING_DTYPE)
+        c = counts.cpu().numpy()
+        return [r[i, : c[i]].copy() if c[i] >= 0 else None for i in range(len(c))]
+
+
+def eigen(abc: torch.Tensor):
+    """Step A3 on device: abc [n, 3] float64 CUDA (Ixx, Ixy, Iyy) -> (kappa_dxdy [n,3], degenerate [n])."""
+    assert abc.is_cuda and abc.dtype == torch.float64 and abc.is_contiguous() and abc.shape[-1] == 3
+    n = abc.shape[0]
+    out = torch.empty_like(abc)
+    deg = torch.empty(n, dtype=torch.int32, device=abc.device)
+    st = torch.cuda.current_stream(abc.device)
+    check(lib().rd_eigen(abc.data_ptr(), n, out.data_ptr(), deg.data_ptr(), C.c_void_p(st.cuda_stream)), "rd_eigen")
+    return out, deg

@@ -1,0 +1,247 @@
+"""GPU parity: the CUDA path (librd.so via the C ABI) against the CPU oracle (-m gpu).
+
+Integer outputs (ridge set incl. the bits of rho, hotspot counts and S, peaks, inlier
+counts, stats) must be bit-identical; fitted centre/radius/rms within 1e-4 px
+(BASELINE.json north_star).  Inputs: seeded synthetic frames (synth/), the same for
+both sides.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+FIT_TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def rdmod():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1310_1371_b200 as rd
+    return rd
+
+
+def _det(rdmod, params, max_batch=1, **extra):
+    p = dict(params)
+    p.update(extra)
+    return rdmod.Detector(p, max_batch=max_batch)
+
+
+def _ridge_set(a, with_kappa=False):
+    return {(int(r["x"]), int(r["y"]), float(r["dx"]).hex(), float(r["dy"]).hex()) for r in a}
+
+
+def _hot_set(a):
+    return {(int(h["r"]), int(h["y"]), int(h["x"]), int(h["raw"]), int(h["S"])) for h in a}
+
+
+def _compare_rings(got, exp):
+    assert len(got) == len(exp), (len(got), len(exp))
+    for g, e in zip(got, exp):
+        for k in ("cx", "cy", "r", "raw_votes", "score_fixed", "inliers", "fit_ok"):
+            assert g[k] == e[k], (k, g, e)
+        for k in ("fx", "fy", "fr", "rms"):
+            assert abs(g[k] - e[k]) <= FIT_TOL, (k, g, e)
+
+
+def _run(rdmod, params, frames, debug=1, **extra):
+    det = _det(rdmod, params, max_batch=len(frames), debug=debug, **extra)
+    dev = torch.from_numpy(np.ascontiguousarray(frames)).cuda()
+    rings, counts = det.detect(dev)
+    det.sync()
+    return det, det.rings_to_numpy(rings, counts)
+
+
+def _check_frame(rdmod, det, i, params, frame, rings_gpu, full=True):
+    p = oracle.params(**params)
+    exp_rings, st, rid, hot = oracle.detect(p, frame, want_debug=True)
+    _compare_rings(rings_gpu, exp_rings)
+    gst = det.stats(i + 1)[i]
+    assert (gst["ridges"], gst["votes"], gst["hotspots"], gst["peaks"]) == \
+        (st["ridges"], st["votes"], st["hotspots"], st["peaks"])
+    if full:
+        assert _ridge_set(det.dump_ridges(i)) == _ridge_set(rid)
+        assert _hot_set(det.dump_hotspots(i)) == _hot_set(hot)
+
+
+# ---------------------------------------------------------------- A3 recipe
+def test_eigen_recipe_bit_exact(rdmod):
+    rng = np.random.default_rng(0)
+    M = rng.integers(-10 ** 13, 10 ** 13, size=(10000, 3)).astype(np.float64)
+    M[:50] = rng.integers(-3, 4, size=(50, 3))            # small / degenerate-prone
+    M[50] = (5.0, 0.0, 5.0)                               # isotropic
+    M[51] = (0.0, 1.0, 0.0)
+    M[52] = (-2.0, 0.0, -1.0)
+    out, deg = rdmod.eigen(torch.from_numpy(M).cuda())
+    out, deg = out.cpu().numpy(), deg.cpu().numpy()
+    for i, (a, b, c) in enumerate(M):
+        k, dx, dy, d = oracle.eigen(a, b, c)
+        assert bool(deg[i]) == d
+        assert out[i, 0].tobytes() == np.float64(k).tobytes()
+        if not d:
+            assert out[i, 1].tobytes() == np.float64(dx).tobytes() and out[i, 2].tobytes() == np.float64(dy).tobytes()
+
+
+# ---------------------------------------------------------------- configs, stage by stage
+@pytest.mark.parametrize("cfg", [1, 11])
+def test_parity_cfg1(rdmod, cfg):
+    params = synth.preset(cfg)
+    frames = np.stack([synth.frame(cfg, 0, i)[0] for i in range(4)])
+    det, rings = _run(rdmod, params, frames)
+    for i in range(4):
+        _check_frame(rdmod, det, i, params, frames[i], rings[i])
+
+
+def test_parity_cfg2_batch16(rdmod):
+    params = synth.preset(2)
+    frames = synth.batch(2, 0, 0, 16)
+    det, rings = _run(rdmod, params, frames)
+    for i in range(16):
+        _check_frame(rdmod, det, i, params, frames[i], rings[i], full=(i < 4))
+
+
+def test_parity_cfg3_sample(rdmod):
+    params = synth.preset(3)
+    frames = synth.batch(3, 0, 0, 4)
+    det, rings = _run(rdmod, params, frames)
+    for i in range(4):
+        _check_frame(rdmod, det, i, params, frames[i], rings[i], full=(i < 2))
+
+
+def test_parity_cfg4_sample(rdmod):
+    params = synth.preset(4)
+    frames = synth.batch(4, 0, 0, 2)
+    det, rings = _run(rdmod, params, frames, max_entries_per_tile=4096)
+    for i in range(2):
+        _check_frame(rdmod, det, i, params, frames[i], rings[i], full=(i < 1))
+
+
+# ---------------------------------------------------------------- edge cases
+def _random_small(seed, W, H, pb):
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(0, 5))
+    rings = synth.make_rings([(rng.uniform(0, W), rng.uniform(0, H), rng.uniform(4, 25), rng.uniform(200, 1500))
+                              for _ in range(n)])
+    sc = synth.scene(W, H, pixel_bytes=pb, max_value=255 if pb == 1 else 4095, background=50,
+                     sigma_p=rng.uniform(1.0, 2.0), read_sigma=rng.uniform(0, 8), poisson=0)
+    return synth.render(sc, rings, noise_key=seed)
+
+
+@pytest.mark.parametrize("W,H", [(8, 8), (13, 29), (37, 41), (100, 75), (129, 65), (200, 33)])
+def test_ragged_and_tiny_frames(rdmod, W, H):
+    for pb in (1, 2):
+        params = dict(width=W, height=H, pixel_bytes=pb, max_value=255 if pb == 1 else 4095, smoothing_sigma=1.3,
+                      curvature_threshold=-4.0 if pb == 1 else -10.0, r_min=3, r_max=min(40, max(W, H)),
+                      vote_threshold_raw=2, vote_threshold_norm=0.3, sig_a=1, sig_b=5, sig_den=20,
+                      annulus_halfwidth=0)
+        frames = np.stack([_random_small(100 * W + H + s + pb, W, H, pb) for s in range(3)])
+        det, rings = _run(rdmod, params, frames)
+        for i in range(3):
+            _check_frame(rdmod, det, i, params, frames[i], rings[i])
+
+
+def test_blank_and_saturated_frames(rdmod):
+    params = synth.preset(2)
+    frames = np.stack([np.zeros((480, 640), np.uint8), np.full((480, 640), 255, np.uint8),
+                       np.full((480, 640), 17, np.uint8)])
+    det, rings = _run(rdmod, params, frames)
+    for i in range(3):
+        assert len(rings[i]) == 0
+        st = det.stats(3)[i]
+        assert st["ridges"] == 0 and st["votes"] == 0
+
+
+def test_rings_at_border_and_fixed_annulus(rdmod):
+    params = dict(width=160, height=120, pixel_bytes=2, max_value=4095, smoothing_sigma=1.5,
+                  curvature_threshold=-10.0, r_min=6, r_max=50, vote_threshold_raw=3, vote_threshold_norm=0.4,
+                  sig_a=1, sig_b=5, sig_den=20, annulus_halfwidth=3)
+    sc = synth.scene(160, 120, pixel_bytes=2, max_value=4095, background=100, sigma_p=1.5, read_sigma=4)
+    fr = [synth.render(sc, synth.make_rings(spec), noise_key=k) for k, spec in enumerate([
+        [(5, 60, 20, 1500), (150, 5, 30, 1500), (80, 118, 15, 1000)],
+        [(0, 0, 40, 2000), (159, 119, 25, 2000), (80, 60, 45, 900)],
+        [(64, 64, 30, 1500), (64, 64, 12, 1500), (100, 40, 20, 1500, 1.0, 2.5)]])]
+    frames = np.stack(fr)
+    det, rings = _run(rdmod, params, frames)
+    for i in range(3):
+        _check_frame(rdmod, det, i, params, frames[i], rings[i])
+
+
+def test_random_small_frames(rdmod):
+    rng = np.random.default_rng(42)
+    W, H = 96, 80
+    params = dict(width=W, height=H, pixel_bytes=2, max_value=4095, smoothing_sigma=1.5, curvature_threshold=-6.0,
+                  r_min=4, r_max=36, vote_threshold_raw=3, vote_threshold_norm=0.35, sig_a=1, sig_b=5, sig_den=20,
+                  annulus_halfwidth=0)
+    frames = np.stack([_random_small(int(s), W, H, 2) for s in rng.integers(0, 10 ** 6, 24)])
+    det, rings = _run(rdmod, params, frames)
+    for i in range(len(frames)):
+        _check_frame(rdmod, det, i, params, frames[i], rings[i], full=(i < 6))
+
+
+# ---------------------------------------------------------------- capacities fail loudly
+def test_capacity_overflow_reported(rdmod):
+    params = synth.preset(2)
+    frames = synth.batch(2, 0, 0, 2)
+    for extra, bit in ((dict(max_rings_per_frame=2), 8), (dict(max_ridges_per_tile=2), 1),
+                       (dict(max_entries_per_tile=16), 2), (dict(max_hotspots_per_level=1), 4)):
+        det = _det(rdmod, params, max_batch=2, **extra)
+        rings, counts = det.detect(torch.from_numpy(frames).cuda())
+        with pytest.raises(rdmod.RDError):
+            det.sync()
+        fl = det.overflow(2)
+        assert np.all(fl & bit) and np.all(counts.cpu().numpy() == -1)
+
+
+def test_invalid_config_rejected(rdmod):
+    base = synth.preset(2)
+    for bad in (dict(smoothing_sigma=0.0), dict(curvature_threshold=1.0), dict(r_min=1), dict(r_max=3, r_min=5),
+                dict(vote_threshold_raw=0), dict(vote_threshold_norm=-1.0), dict(width=4)):
+        with pytest.raises(rdmod.RDError):
+            _det(rdmod, base, **bad)
+
+
+# ---------------------------------------------------------------- full size, bench launch configuration
+def test_full_batch_cfg3_bench_config(rdmod):
+    """cfg3 at BASELINE size (256 frames, the bench step): sampled frames vs the oracle,
+    all frames checked for canonical order, range and determinism."""
+    params = synth.preset(3)
+    frames = synth.batch(3, 0, 0, 256)
+    det = _det(rdmod, params, max_batch=256)
+    dev = torch.from_numpy(frames).cuda()
+    rings, counts = det.detect(dev)
+    det.sync()
+    out = det.rings_to_numpy(rings, counts)
+    rings2, counts2 = det.detect(dev)
+    det.sync()
+    out2 = det.rings_to_numpy(rings2, counts2)
+    assert all(a.tobytes() == b.tobytes() for a, b in zip(out, out2))  # deterministic
+    for i in (0, 97, 255):
+        _check_frame(rdmod, det, i, params, frames[i], out[i], full=False)
+    for g in out:
+        assert g is not None and len(g) > 20
+        key = list(zip(g["r"], g["cy"], g["cx"]))
+        assert key == sorted(key) and len(set(key)) == len(key)
+        assert np.all((g["r"] >= params["r_min"]) & (g["r"] <= params["r_max"]))
+        assert np.all(g["score_fixed"] > 0.5 * 2 * math.pi * 2 ** 24 * g["r"])
+    st = det.stats(256)
+    assert np.all(st["votes"] > 10 ** 6)
+
+
+def test_detect_host_matches_device(rdmod):
+    params = synth.preset(3)
+    frames = synth.batch(3, 0, 300, 70)
+    det = _det(rdmod, params, max_batch=70)
+    rings, counts = det.detect(torch.from_numpy(frames).cuda())
+    det.sync()
+    dev_out = det.rings_to_numpy(rings, counts)
+    pinned = torch.from_numpy(frames).pin_memory()
+    hr, hc = det.detect_host(pinned)
+    for i in range(70):
+        assert hc[i] == len(dev_out[i])
+        assert hr[i, : hc[i]].tobytes() == dev_out[i].tobytes()

@@ -57,7 +57,7 @@ def build_rd(force=False):
     if not (force or _stale(out, deps)):
         return out
     cmd = [NVCC, "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-           "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off", "-shared", "-fmad=false",
+           "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off", "-shared",
            "-Xptxas", "-v", "-I", os.path.join(ROOT, "include"), "-o", out] + srcs + ["-lcudart"]
     r = _run(cmd)
     with open(os.path.join(pkg, "build_ptxas.log"), "w") as f:
