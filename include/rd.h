@@ -63,7 +63,7 @@ typedef struct rd_config {
   int32_t max_rings_per_frame;    /* output capacity per frame (default 1024) */
   int32_t max_ridges_per_tile;    /* ridges per 32x32 tile (default 512) */
   int32_t max_entries_per_tile;   /* voting rays per 64x64 Hough tile (default 2048) */
-  int32_t max_hotspots_per_level; /* hotspots per Hough tile per level (default 512) */
+  int32_t max_hotspots_per_level; /* hotspots per Hough tile per level (default 256) */
   int32_t debug;                  /* 1: keep hotspot records for rd_dump_hotspots */
 } rd_config;
 
@@ -143,6 +143,13 @@ rd_status rd_dump_hotspots(rd_detector* det, int32_t frame, rd_hotspot* h_out, i
  * rd_detect calls into *n_calls.  Disabled by default (no events recorded). */
 rd_status rd_set_timing(rd_detector* det, int32_t on);
 rd_status rd_kernel_times(rd_detector* det, float* h_ms, int32_t* n_calls);
+
+/* Profiling aid: per-phase SM-cycle counters of the Hough kernel, accumulated by one
+ * thread per CTA at its barriers when enabled (on = 1 clears and enables; 0 disables).
+ * h_cycles[0..15]: [0] ray gathering, [1] first step setup, [2] votes, [3] window sums,
+ * [4] candidate bookkeeping + undo, [5] peaks + next setup, [15] number of CTAs.
+ * Synchronous read; counters cost a few instructions per barrier while enabled. */
+rd_status rd_phase_cycles(rd_detector* det, int32_t on, uint64_t* h_cycles);
 
 /* Step A3 in isolation: the fp64 kappa / rho recipe on n
  * Hessians d_abc[3i..3i+2] = (Ixx, Ixy, Iyy) -> d_out[3i..3i+2] = (kappa, dx, dy),

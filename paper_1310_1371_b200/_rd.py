@@ -38,7 +38,7 @@ assert RING_DTYPE.itemsize == 64
 
 EXPORTS = ("rd_abi_version", "rd_status_string", "rd_last_error", "rd_config_init", "rd_create", "rd_destroy",
            "rd_detect", "rd_detect_host", "rd_sync", "rd_query_overflow", "rd_get_stats", "rd_dump_ridges",
-           "rd_dump_hotspots", "rd_eigen", "rd_set_timing", "rd_kernel_times")
+           "rd_dump_hotspots", "rd_eigen", "rd_set_timing", "rd_kernel_times", "rd_phase_cycles")
 
 
 class RDError(RuntimeError):
@@ -77,6 +77,7 @@ def lib():
         L.rd_eigen.argtypes = [vp, i64, vp, vp, vp]
         L.rd_set_timing.argtypes = [vp, i32]
         L.rd_kernel_times.argtypes = [vp, vp, C.POINTER(i32)]
+        L.rd_phase_cycles.argtypes = [vp, i32, vp]
         for n in EXPORTS:
             if n not in ("rd_abi_version", "rd_status_string", "rd_last_error"):
                 getattr(L, n).restype = C.c_int

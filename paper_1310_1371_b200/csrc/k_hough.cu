@@ -3,73 +3,97 @@
 //
 // Rows A5-A8 of DESIGN.md §2 (SI steps 2-4, PAPER.md:931-978;
 // range extension PAPER.md:998-1001).  The CTA owns the accumulator cells of its tile and
-// sweeps r upward through the Hough range, keeping on chip:
-//   raw(r)  — one level of packed uint16 counters over tile + (K_r + 1) halo,
-//             filled with warp-issued shared-memory atomics;
-//   three rolling levels (r-2, r-1, r) of hotspot lists + a cell->hotspot index map over
-//             tile + 1 (the paper's r mod 3 recycling, re-expressed
-//             for shared memory), holding the exact fixed-point window sums S.
-// A hotspot is registered by the one atomic that lifts its counter past T_raw (the
-// paper's "surpassed" test at increment time).  S is computed for
-// hotspots only; NMS of level r-1 runs once level r is complete.
-// Nothing but the peak records (and optional debug hotspots) leaves the SM.
+// sweeps r upward through the Hough range G levels at a time, keeping on chip:
+//   raw(r..r+G-1) — G levels of packed uint16 counters over tile + (K_r + 1) halo, filled
+//                  with shared-memory atomics;
+//   hotspot lists (cell, raw, S) and candidate lists of the last G + 2 levels — the
+//                  paper's rolling level window, 3 levels -> G + 2.
+// Voting rays (a ridge pixel, a sense of rho and the level interval in which its votes can
+// land in the tile's level boxes) are gathered once per CTA.  Each G-level step compacts
+// the rays active in it and walks them entry-major over the levels they reach.
+// A hotspot is registered by the one atomic that lifts its counter past T_raw (the paper's
+// "surpassed" test at increment time).  S is computed for hotspots only:
+// every (hotspot, window row) pair is one thread's row sum, reduced with 64-bit shared
+// atomics (integer sums: order-free, exact).  NMS of a level runs once the level above is
+// complete, one warp per candidate scanning three neighbouring lists.
+// Counters are cleared by undoing exactly the cells this CTA incremented (the paper's
+// register-and-undo).  Only peak records (and optional debug hotspots)
+// leave the SM.
 #include "rd_internal.cuh"
 
 namespace rd {
 
 namespace {
-constexpr int IDXS = T2 + 2;      // index-map side: tile + 1 ring
+constexpr int RING = T2 + 2;      // tile + 1 ring side (hotspot registration region)
+constexpr int NT = 512;           // threads per CTA
+constexpr int NW = NT / 32;
 
 struct K2Smem {
-  // computed on host and device identically
-  int raws, rawp;                 // raw side and row pitch (uint16 units, even)
-  size_t off_hS, off_ed, off_raw, off_idx, off_hcell, off_hraw, off_exy, off_err, off_hcnt, off_w, off_bins, total;
+  int raws, rawp;                 // raw side and row pitch (uint16 units)
+  size_t off_hS, off_ed, off_raw, off_exy, off_err, off_act, off_hcell, off_hraw, off_cand, off_hcnt, off_ccnt,
+      off_w, off_k, off_tn, off_box, total;
 };
 
 __host__ __device__ inline size_t align16(size_t v) { return (v + 15) & ~size_t(15); }
 
-__host__ __device__ inline K2Smem k2_layout(int hal, int entry_cap, int hot_cap, int n_levels, int wstride,
-                                            int max_bins) {
+__host__ __device__ inline K2Smem k2_layout(int G, int hal, int entry_cap, int hot_cap, int n_levels, int wstride) {
+  const int NSLOT = G + 2;
   K2Smem L;
   L.raws = T2 + 2 * hal;
-  L.rawp = (L.raws + 7) & ~7;
+  // row pitch with an odd number of 32-bit words: the rows of a window fall in distinct banks
+  L.rawp = ((L.raws / 2) & 1) ? L.raws : L.raws + 2;
   size_t o = 0;
-  L.off_hS = o;    o = align16(o + sizeof(long long) * 3 * hot_cap);
+  L.off_hS = o;    o = align16(o + sizeof(unsigned long long) * NSLOT * hot_cap);
   L.off_ed = o;    o = align16(o + sizeof(double2) * entry_cap);
-  L.off_raw = o;   o = align16(o + 2 * (size_t)L.raws * L.rawp);
-  L.off_idx = o;   o = align16(o + 2 * 3 * IDXS * IDXS);
-  L.off_hcell = o; o = align16(o + 2 * 3 * hot_cap);
-  L.off_hraw = o;  o = align16(o + 2 * 3 * hot_cap);
-  L.off_exy = o;   o = align16(o + 4 * entry_cap);
-  L.off_err = o;   o = align16(o + 4 * entry_cap);
-  L.off_hcnt = o;  o = align16(o + 4 * (n_levels + 8));
-  L.off_w = o;     o = align16(o + 4 * wstride);
-  L.off_bins = o;  o = align16(o + 4 * (max_bins + 1));
+  L.off_raw = o;   o = align16(o + 2 * (size_t)G * L.raws * L.rawp);
+  L.off_exy = o;   o = align16(o + 4 * (size_t)entry_cap);
+  L.off_err = o;   o = align16(o + 4 * (size_t)entry_cap);
+  L.off_act = o;   o = align16(o + 2 * (size_t)entry_cap);
+  L.off_hcell = o; o = align16(o + 2 * (size_t)NSLOT * hot_cap);
+  L.off_hraw = o;  o = align16(o + 2 * (size_t)NSLOT * hot_cap);
+  L.off_cand = o;  o = align16(o + 2 * (size_t)NSLOT * hot_cap);
+  L.off_hcnt = o;  o = align16(o + 4 * (size_t)(n_levels + G + 8));
+  L.off_ccnt = o;  o = align16(o + 4 * (size_t)(n_levels + G));
+  L.off_w = o;     o = align16(o + 4 * (size_t)n_levels * wstride);   // level tables, resident
+  L.off_k = o;     o = align16(o + 4 * (size_t)n_levels);
+  L.off_tn = o;    o = align16(o + 8 * (size_t)n_levels);
+  L.off_box = o;   o = align16(o + 16 * (size_t)G);
   L.total = o;
   return L;
 }
+
+// a r >= b restricted to [lo, hi]
+__device__ __forceinline__ void half_ge(float a, float b, float& lo, float& hi) {
+  if (a > 0.f) lo = fmaxf(lo, __fdividef(b, a));
+  else if (a < 0.f) hi = fminf(hi, __fdividef(b, a));
+  else if (b > 0.f) hi = -1e30f;
+}
 }  // namespace
 
-template <bool kWide>
-__global__ void __launch_bounds__(K2_THREADS, 2) k_hough(Params P, int max_bins) {
+template <bool kWide, int G>
+__global__ void __launch_bounds__(NT, 1) k_hough(Params P) {
+  constexpr int NSLOT = G + 2;
   extern __shared__ __align__(16) unsigned char smem[];
-  const K2Smem L = k2_layout(P.hal, P.entry_cap, P.hot_cap, P.n_levels, P.wstride, max_bins);
-  long long* hS = reinterpret_cast<long long*>(smem + L.off_hS);        // [3][hot_cap]
+  const K2Smem L = k2_layout(G, P.hal, P.entry_cap, P.hot_cap, P.n_levels, P.wstride);
+  unsigned long long* hS = reinterpret_cast<unsigned long long*>(smem + L.off_hS);  // [NSLOT][hot_cap]
   double2* eD = reinterpret_cast<double2*>(smem + L.off_ed);             // [entry_cap] (s*dx, s*dy)
-  uint32_t* raw32 = reinterpret_cast<uint32_t*>(smem + L.off_raw);       // packed uint16 counters
+  uint32_t* raw32 = reinterpret_cast<uint32_t*>(smem + L.off_raw);       // [G] packed uint16 levels
   uint16_t* raw16 = reinterpret_cast<uint16_t*>(smem + L.off_raw);
-  uint16_t* idx = reinterpret_cast<uint16_t*>(smem + L.off_idx);         // [3][IDXS*IDXS]
-  uint16_t* hcell = reinterpret_cast<uint16_t*>(smem + L.off_hcell);     // [3][hot_cap]
-  uint16_t* hraw = reinterpret_cast<uint16_t*>(smem + L.off_hraw);       // [3][hot_cap]
   uint32_t* eXY = reinterpret_cast<uint32_t*>(smem + L.off_exy);         // [entry_cap] x | y<<16
-  uint32_t* eR = reinterpret_cast<uint32_t*>(smem + L.off_err);          // [entry_cap] ra | rb<<16
-  int* hcnt = reinterpret_cast<int*>(smem + L.off_hcnt);                 // [n_levels] + misc
-  int* wl = reinterpret_cast<int*>(smem + L.off_w);                      // current level weights
-  int* binpre = reinterpret_cast<int*>(smem + L.off_bins);               // bin prefix sums
-  int* s_ecnt = hcnt + P.n_levels;
+  uint32_t* eR = reinterpret_cast<uint32_t*>(smem + L.off_err);          // [entry_cap] ra | rb<<16 (level idx)
+  uint16_t* act = reinterpret_cast<uint16_t*>(smem + L.off_act);         // active entries of the step
+  uint16_t* hcell = reinterpret_cast<uint16_t*>(smem + L.off_hcell);     // [NSLOT][hot_cap] ring-local cell
+  uint16_t* hraw = reinterpret_cast<uint16_t*>(smem + L.off_hraw);       // [NSLOT][hot_cap]
+  uint16_t* cand = reinterpret_cast<uint16_t*>(smem + L.off_cand);       // [NSLOT][hot_cap] candidate hotspots
+  int* hcnt = reinterpret_cast<int*>(smem + L.off_hcnt);                 // [n_levels + G] + misc
+  int* ccnt = reinterpret_cast<int*>(smem + L.off_ccnt);                 // [n_levels + G]
+  int* tW = reinterpret_cast<int*>(smem + L.off_w);                      // [n_levels][wstride] w_r(d)
+  int* tK = reinterpret_cast<int*>(smem + L.off_k);                      // [n_levels] K_r
+  double* tTn = reinterpret_cast<double*>(smem + L.off_tn);              // [n_levels] T_norm(r)
+  int4* box = reinterpret_cast<int4*>(smem + L.off_box);                 // [G] vote box per level
+  int* s_ecnt = hcnt + P.n_levels + G;
   int* s_flags = s_ecnt + 1;
-  unsigned long long* s_votes = reinterpret_cast<unsigned long long*>(hcnt + P.n_levels + 2);
-  int* s_nhot = hcnt + P.n_levels + 4;
+  int* s_nact = s_ecnt + 2;                                              // [2], by step parity
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int f = blockIdx.y;
@@ -78,220 +102,357 @@ __global__ void __launch_bounds__(K2_THREADS, 2) k_hough(Params P, int max_bins)
   const int X0 = txi * T2, Y0 = tyi * T2;
   const int W = P.W, H = P.H, hal = P.hal;
   const int RX0 = X0 - hal, RY0 = Y0 - hal;   // raw buffer origin
-  const int rawp = L.rawp, raws = L.raws;
-
-  for (int i = tid; i < 3 * IDXS * IDXS; i += K2_THREADS) idx[i] = 0;
-  for (int i = tid; i < P.n_levels + 8; i += K2_THREADS) hcnt[i] = 0;
-
-  // ---------------- phase 0: voting rays that can reach tile + max halo
-  // box E = (tile + hal) intersected with the frame
-  const int bx0 = max(X0 - hal, 0), bx1 = min(X0 + T2 - 1 + hal, W - 1);
-  const int by0 = max(Y0 - hal, 0), by1 = min(Y0 + T2 - 1 + hal, H - 1);
+  const int rawp = L.rawp;
+  const int lvl_cells = L.raws * rawp;       // uint16 cells per raw level
+  const int hot_cap = P.hot_cap, nlev = P.n_levels;
   const int rhi = P.r_hi, rlo = P.r_lo;
-  const int nbx = P.nbx;
-  const int cbx0 = max((bx0 - rhi) / T1, 0), cbx1 = min((bx1 + rhi) / T1, P.nbx - 1);
-  const int cby0 = max((by0 - rhi) / T1, 0), cby1 = min((by1 + rhi) / T1, P.nby - 1);
-  const int nbw = cbx1 - cbx0 + 1, nbins = nbw * (cby1 - cby0 + 1);
-  const int64_t fbins = (int64_t)f * P.nbx * P.nby;
-  for (int i = tid; i < nbins; i += K2_THREADS) {
-    int by = cby0 + i / nbw, bx = cbx0 + i % nbw;
-    binpre[i + 1] = P.bin_count[fbins + by * nbx + bx];
-  }
-  __syncthreads();
-  if (tid == 0) {
-    binpre[0] = 0;
-    for (int i = 1; i <= nbins; ++i) binpre[i] += binpre[i - 1];
-  }
-  __syncthreads();
-  const int nrid = binpre[nbins];
-  for (int k = tid; k < 2 * nrid; k += K2_THREADS) {
-    int rk = k >> 1;
-    double sgn = (k & 1) ? -1.0 : 1.0;
-    int lo = 0, hi = nbins - 1;  // bin containing ridge rk
-    while (lo < hi) {
-      int mid = (lo + hi + 1) >> 1;
-      if (binpre[mid] <= rk) lo = mid; else hi = mid - 1;
-    }
-    int by = cby0 + lo / nbw, bx = cbx0 + lo % nbw;
-    int64_t g = (fbins + by * nbx + bx) * P.ridge_cap + (rk - binpre[lo]);
-    uint32_t xy = P.bin_xy[g];
-    double2 d = P.bin_d[g];
-    int x = (int)(xy & 0xFFFFu), y = (int)(xy >> 16);
-    double u = sgn * d.x, v = sgn * d.y;
-    // conservative interval of r with target inside E (exactness restored per vote)
-    float rl = (float)rlo, rh = (float)rhi;
-    float fu = (float)u, fv = (float)v;
-    if (fu > 0.f) { rl = fmaxf(rl, (bx0 - x - 0.5f) / fu); rh = fminf(rh, (bx1 - x + 0.5f) / fu); }
-    else if (fu < 0.f) { rl = fmaxf(rl, (bx1 - x + 0.5f) / fu); rh = fminf(rh, (bx0 - x - 0.5f) / fu); }
-    else if (x < bx0 || x > bx1) continue;
-    if (fv > 0.f) { rl = fmaxf(rl, (by0 - y - 0.5f) / fv); rh = fminf(rh, (by1 - y + 0.5f) / fv); }
-    else if (fv < 0.f) { rl = fmaxf(rl, (by1 - y + 0.5f) / fv); rh = fminf(rh, (by0 - y - 0.5f) / fv); }
-    else if (y < by0 || y > by1) continue;
-    int ra = max((int)floorf(rl) - 1, rlo), rb = min((int)ceilf(rh) + 1, rhi);
-    if (ra > rb) continue;
-    int e = atomicAdd(s_ecnt, 1);
-    if (e < P.entry_cap) {
-      eD[e] = make_double2(u, v);
-      eXY[e] = xy;
-      eR[e] = (uint32_t)(ra - rlo) | ((uint32_t)(rb - rlo) << 16);
-    } else {
-      atomicOr(s_flags, OVF_ENTRIES);
-    }
-  }
-  __syncthreads();
-  const int ne = min(*s_ecnt, P.entry_cap);
-  unsigned long long my_votes = 0;
-  int my_hot = 0;
-  const uint32_t raw_words = (uint32_t)(raws * rawp) >> 1;
 
-  // ---------------- level sweep
-  for (int li = 0; li < P.n_levels; ++li) {
-    const int r = rlo + li;
-    const int slot = li % 3;
-    const int K = P.lvlK[li];
-    // (a) clear raw, clear the index-map entries of level li-3 (same slot), load weights
-    {
-      uint4* r4 = reinterpret_cast<uint4*>(raw32);
-      for (uint32_t i = tid; i < raw_words / 4; i += K2_THREADS) r4[i] = make_uint4(0, 0, 0, 0);
-      for (uint32_t i = (raw_words / 4) * 4 + tid; i < raw_words; i += K2_THREADS) raw32[i] = 0;
-      if (li >= 3) {
-        int nold = min(hcnt[li - 3], P.hot_cap);
-        uint16_t* im = idx + slot * IDXS * IDXS;
-        const uint16_t* hc = hcell + slot * P.hot_cap;
-        for (int k = tid; k < nold; k += K2_THREADS) im[hc[k]] = 0;
-      }
-      for (int i = tid; i <= K; i += K2_THREADS) wl[i] = P.lvlW[li * P.wstride + i];
-    }
+  // optional per-phase cycle accounting (thread 0, after each barrier; rd_phase_cycles)
+  unsigned long long t_acc[6] = {0, 0, 0, 0, 0, 0};
+  long long t_last = clock64();
+#define PMARK(i)                                      \
+  if (P.prof && tid == 0) {                           \
+    const long long t_ = clock64();                   \
+    t_acc[i] += (unsigned long long)(t_ - t_last);    \
+    t_last = t_;                                      \
+  }
+  for (int i = tid; i < nlev + G + 8; i += NT) hcnt[i] = 0;
+  for (int i = tid; i < nlev + G; i += NT) ccnt[i] = 0;
+  for (int i = tid; i < nlev * P.wstride; i += NT) tW[i] = P.lvlW[i];
+  for (int i = tid; i < nlev; i += NT) {
+    tK[i] = P.lvlK[i];
+    tTn[i] = P.lvlTn[i];
+  }
+  {  // zero all raw levels once; afterwards cells are restored to zero by undo
+    uint4* r4 = reinterpret_cast<uint4*>(raw32);
+    const int n4 = (G * lvl_cells) / 8;
+    for (int i = tid; i < n4; i += NT) r4[i] = make_uint4(0, 0, 0, 0);
+    for (int i = n4 * 8 + tid; i < G * lvl_cells; i += NT) raw16[i] = 0;
+  }
+
+  // ---------------- phase 0: voting rays that can reach the tile's level boxes
+  {
+    const int hmax = hal;  // level boxes are inside tile + hal
+    const int bx0 = max(X0 - hmax, 0), bx1 = min(X0 + T2 - 1 + hmax, W - 1);
+    const int by0 = max(Y0 - hmax, 0), by1 = min(Y0 + T2 - 1 + hmax, H - 1);
+    const int nbx = P.nbx;
+    const int cbx0 = max((bx0 - rhi) / T1, 0), cbx1 = min((bx1 + rhi) / T1, P.nbx - 1);
+    const int cby0 = max((by0 - rhi) / T1, 0), cby1 = min((by1 + rhi) / T1, P.nby - 1);
+    const int nbw = cbx1 - cbx0 + 1, nbins = nbw * (cby1 - cby0 + 1);
+    const int64_t fbins = (int64_t)f * P.nbx * P.nby;
+    const float m = P.k_slope, c = P.k_icpt;
     __syncthreads();
-    // (b) votes of level r into raw(r) over tile + (K_r + 1)
-    {
-      const int vx0 = max(X0 - K - 1, 0), vx1 = min(X0 + T2 + K, W - 1);
-      const int vy0 = max(Y0 - K - 1, 0), vy1 = min(Y0 + T2 + K, H - 1);
-      const double rd = (double)r;
-      uint16_t* im = idx + slot * IDXS * IDXS;
-      uint16_t* hc = hcell + slot * P.hot_cap;
-      const uint32_t T_raw = (uint32_t)P.T_raw;
-      for (int e = tid; e < ne; e += K2_THREADS) {
-        uint32_t rr = eR[e];
-        if (li < (int)(rr & 0xFFFFu) || li > (int)(rr >> 16)) continue;
-        double2 d = eD[e];
-        uint32_t xy = eXY[e];
-        int tx = (int)(xy & 0xFFFFu) + (int)llround(__dmul_rn(rd, d.x));
-        int ty = (int)(xy >> 16) + (int)llround(__dmul_rn(rd, d.y));
-        if (tx < vx0 || tx > vx1 || ty < vy0 || ty > vy1) continue;
-        int cell = (ty - RY0) * rawp + (tx - RX0);
-        uint32_t sh = (cell & 1) << 4;
-        uint32_t old = atomicAdd(&raw32[cell >> 1], 1u << sh);
-        uint32_t oc = (old >> sh) & 0xFFFFu;
-        int ix = tx - (X0 - 1), iy = ty - (Y0 - 1);
-        bool in_ring = (unsigned)ix < (unsigned)IDXS && (unsigned)iy < (unsigned)IDXS;
-        if (oc == T_raw && in_ring) {
-          int k = atomicAdd(&hcnt[li], 1);
-          if (k < P.hot_cap) {
-            uint16_t c16 = (uint16_t)(iy * IDXS + ix);
-            hc[k] = c16;
-            im[c16] = (uint16_t)(k + 1);
-          } else {
-            atomicOr(s_flags, OVF_HOTSPOTS);
-          }
+    for (int b = warp; b < nbins; b += NW) {  // warp per ridge bin, lanes over (ridge, sense)
+      const int by = cby0 + b / nbw, bx = cbx0 + b % nbw;
+      const int64_t bin = fbins + by * nbx + bx;
+      const int cnt = P.bin_count[bin];
+      for (int j = lane; j < 2 * cnt; j += 32) {
+        const int64_t g = bin * P.ridge_cap + (j >> 1);
+        const uint32_t xy = P.bin_xy[g];
+        const double2 d = P.bin_d[g];
+        const double sgn = (j & 1) ? -1.0 : 1.0;
+        const int x = (int)(xy & 0xFFFFu), y = (int)(xy >> 16);
+        const double u = sgn * d.x, v = sgn * d.y;
+        // necessary conditions for a vote in the level-r box (K_r <= m r + c), linear in r;
+        // conservative by +-1 level, exactness restored per vote
+        const float fu = (float)u, fv = (float)v, fx = (float)x, fy = (float)y;
+        float lo = (float)rlo, hi = (float)rhi;
+        half_ge(fu + m, (float)X0 - 1.5f - c - fx, lo, hi);
+        half_ge(m - fu, fx - (float)(X0 + T2) - 0.5f - c, lo, hi);
+        half_ge(fu, -0.5f - fx, lo, hi);
+        half_ge(-fu, fx - (float)W + 0.5f, lo, hi);
+        half_ge(fv + m, (float)Y0 - 1.5f - c - fy, lo, hi);
+        half_ge(m - fv, fy - (float)(Y0 + T2) - 0.5f - c, lo, hi);
+        half_ge(fv, -0.5f - fy, lo, hi);
+        half_ge(-fv, fy - (float)H + 0.5f, lo, hi);
+        if (hi < lo - 2.f) continue;
+        const int ra = max((int)floorf(lo) - 1, rlo), rb = min((int)ceilf(hi) + 1, rhi);
+        if (ra > rb) continue;
+        const int e = atomicAdd(s_ecnt, 1);
+        if (e < P.entry_cap) {
+          eD[e] = make_double2(u, v);
+          eXY[e] = xy;
+          eR[e] = (uint32_t)(ra - rlo) | ((uint32_t)(rb - rlo) << 16);
+        } else {
+          atomicOr(s_flags, OVF_ENTRIES);
         }
-        my_votes += (ix >= 1 && ix <= T2 && iy >= 1 && iy <= T2);
       }
     }
-    __syncthreads();
-    // (c) S = sum_{|i|,|j|<=K} w(i) w(j) raw(y+i, x+j) at each hotspot
-    {
-      const int nh = min(hcnt[li], P.hot_cap);
-      const uint16_t* hc = hcell + slot * P.hot_cap;
-      long long* hs = hS + slot * P.hot_cap;
-      uint16_t* hr = hraw + slot * P.hot_cap;
-      for (int h = warp; h < nh; h += K2_THREADS / 32) {
-        int c16 = hc[h];
-        int iy = c16 / IDXS, ix = c16 - iy * IDXS;
-        int ly = iy - 1 + hal, lx = ix - 1 + hal;   // raw-local coordinates
-        unsigned long long acc = 0;
-        for (int i = lane - K; i <= K; i += 32) {
-          const uint16_t* row = raw16 + (ly + i) * rawp + lx;
-          if (kWide) {
-            unsigned long long rs = 0;
-            for (int j = -K; j <= K; ++j) rs += (unsigned long long)wl[j < 0 ? -j : j] * row[j];
-            acc += rs * (unsigned long long)wl[i < 0 ? -i : i];
-          } else {
-            uint32_t rs = 0;
-            for (int j = -K; j <= K; ++j) rs += (uint32_t)wl[j < 0 ? -j : j] * row[j];
-            acc += (unsigned long long)rs * (unsigned long long)wl[i < 0 ? -i : i];
-          }
-        }
+  }
+  __syncthreads();
+  PMARK(0);
+  const int ne = min(*s_ecnt, P.entry_cap);
+  int my_votes = 0, my_hot = 0;
+  const uint32_t T_raw = (uint32_t)P.T_raw;
+
+  // per-step setup: weights, level boxes, compacted active rays (into parity buffer)
+  auto setup = [&](int L0s) {
+    const int Lhs = min(L0s + G - 1, nlev - 1);
+    if (tid < G) {
+      const int K = (L0s + tid < nlev) ? tK[L0s + tid] : 0;
+      box[tid] = make_int4(max(X0 - K - 1, 0), min(X0 + T2 + K, W - 1), max(Y0 - K - 1, 0), min(Y0 + T2 + K, H - 1));
+    }
+    int* cnt = s_nact + ((L0s / G) & 1);
+    for (int e0 = 0; e0 < ne; e0 += NT) {
+      const int e = e0 + tid;
+      bool a = false;
+      if (e < ne) {
+        const uint32_t rr = eR[e];
+        a = (int)(rr & 0xFFFFu) <= Lhs && (int)(rr >> 16) >= L0s;
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, a);
+      int base = 0;
+      if (lane == 0 && bal) base = atomicAdd(cnt, __popc(bal));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (a) act[base + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)e;
+    }
+  };
+  if (tid == 0) { s_nact[0] = 0; s_nact[1] = 0; }
+  __syncthreads();
+  setup(0);
+  __syncthreads();
+  PMARK(1);
+
+  // ---------------- level sweep, G levels per step
+  for (int L0 = 0; L0 < nlev; L0 += G) {
+    const int Lhi = min(L0 + G - 1, nlev - 1);
+    const int par = (L0 / G) & 1;
+    const int nact = s_nact[par];
+    // (a) votes of levels L0..Lhi: per active ray, the G
+    //     targets are computed first and their atomics issued back to back (ILP)
+    for (int i = tid; i < nact; i += NT) {
+      const int e = act[i];
+      const uint32_t rr = eR[e];
+      const int l0 = max((int)(rr & 0xFFFFu), L0), l1 = min((int)(rr >> 16), Lhi);
+      const double2 d = eD[e];
+      const uint32_t xy = eXY[e];
+      const int x = (int)(xy & 0xFFFFu), y = (int)(xy >> 16);
+      const double rd0 = (double)(rlo + L0);
+      int cell[G], txs[G], tys[G];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) {
-          hs[h] = (long long)acc;
-          uint16_t c = raw16[ly * rawp + lx];
-          hr[h] = c;
-          bool interior = ix >= 1 && ix <= T2 && iy >= 1 && iy <= T2;
-          if (interior) {
-            ++my_hot;
-            if (P.debug) {
-              int k = atomicAdd(&P.dbg_count[f], 1);
-              if (k < P.dbg_cap) {
-                HotRec rec;
-                rec.r = r; rec.y = Y0 - 1 + iy; rec.x = X0 - 1 + ix; rec.raw = c; rec.S = (long long)acc;
-                P.dbg_hot[(int64_t)f * P.dbg_cap + k] = rec;
-              } else {
-                atomicOr(&P.flags[f], OVF_DEBUG);
-              }
+      for (int g = 0; g < G; ++g) {
+        cell[g] = -1;
+        if (L0 + g < l0 || L0 + g > l1) continue;
+        const double rd = rd0 + (double)g;
+        const int tx = x + (int)llround(__dmul_rn(rd, d.x));
+        const int ty = y + (int)llround(__dmul_rn(rd, d.y));
+        const int4 bb = box[g];
+        if (tx < bb.x || tx > bb.y || ty < bb.z || ty > bb.w) continue;
+        cell[g] = g * lvl_cells + (ty - RY0) * rawp + (tx - RX0);
+        txs[g] = tx;
+        tys[g] = ty;
+      }
+      uint32_t old[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g)
+        if (cell[g] >= 0) old[g] = atomicAdd(&raw32[cell[g] >> 1], 1u << ((cell[g] & 1) << 4));
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        if (cell[g] < 0) continue;
+        const int tx = txs[g], ty = tys[g];
+        const uint32_t oc = (old[g] >> ((cell[g] & 1) << 4)) & 0xFFFFu;
+        if (oc == T_raw) {
+          const int ix = tx - (X0 - 1), iy = ty - (Y0 - 1);
+          if ((unsigned)ix < (unsigned)RING && (unsigned)iy < (unsigned)RING) {
+            const int li = L0 + g;
+            const int h = atomicAdd(&hcnt[li], 1);
+            if (h < hot_cap) hcell[(li % NSLOT) * hot_cap + h] = (uint16_t)(iy * RING + ix);
+            else atomicOr(s_flags, OVF_HOTSPOTS);
+          }
+        }
+        my_votes += ((unsigned)(tx - X0) < (unsigned)T2) & ((unsigned)(ty - Y0) < (unsigned)T2);
+      }
+    }
+    if (tid == 0) s_nact[par ^ 1] = 0;   // counter of the next step (last read a barrier ago)
+    __syncthreads();
+    PMARK(2);
+    // (b) S = sum_i w(i) sum_j w(j) raw(y+i, x+j) at each hotspot:
+    //     a sub-warp of SUB >= 2K+1 lanes per hotspot, lanes over window rows, shuffle sum;
+    //     the hotspots of all G levels are processed concurrently
+    {
+      int pre = 0;
+      if (lane < G) pre = (L0 + lane < nlev) ? min(hcnt[L0 + lane], hot_cap) : 0;
+#pragma unroll
+      for (int o = 1; o < G; o <<= 1) {
+        const int nn = __shfl_up_sync(0xffffffffu, pre, o);
+        if (lane >= o) pre += nn;
+      }
+      int pg[G];
+#pragma unroll
+      for (int q = 0; q < G; ++q) pg[q] = __shfl_sync(0xffffffffu, pre, q);
+      const int Rmx = 2 * tK[Lhi] + 1;   // K_r is non-decreasing in r
+      const int SUB = Rmx <= 4 ? 4 : Rmx <= 8 ? 8 : Rmx <= 16 ? 16 : 32;
+      const int per = 32 / SUB, sub = lane / SUB, sl_ = lane - sub * SUB;
+      const int total = pg[G - 1];
+      for (int tb = warp * per; tb < total; tb += NW * per) {
+        const int t = tb + sub;
+        int g = 0, base = 0;
+#pragma unroll
+        for (int q = 0; q < G - 1; ++q)
+          if (t >= pg[q]) { g = q + 1; base = pg[q]; }
+        const int li = min(L0 + g, nlev - 1), h = t - base;
+        const int K = tK[li], R = 2 * K + 1;
+        const int sl = li % NSLOT;
+        const int* w = tW + li * P.wstride;
+        const uint16_t* lvl = raw16 + g * lvl_cells;
+        unsigned long long acc = 0;
+        int ly = 0, lx = 0;
+        if (t < total) {
+          const int c16 = hcell[sl * hot_cap + h];
+          const int iy = c16 / RING, ix = c16 - iy * RING;
+          ly = iy - 1 + hal;
+          lx = ix - 1 + hal;
+          for (int row = sl_; row < R; row += SUB) {
+            const uint16_t* rowp = lvl + (ly + row - K) * rawp + lx;
+            if (kWide) {
+              unsigned long long rs = (unsigned long long)w[0] * rowp[0];
+              for (int j = 1; j <= K; ++j) rs += (unsigned long long)w[j] * (uint32_t)(rowp[-j] + rowp[j]);
+              acc += rs * (unsigned long long)w[abs(row - K)];
+            } else {
+              uint32_t rs = (uint32_t)w[0] * rowp[0];
+#pragma unroll 4
+              for (int j = 1; j <= K; ++j) rs += (uint32_t)w[j] * (uint32_t)(rowp[-j] + rowp[j]);
+              acc += (unsigned long long)rs * (unsigned long long)w[abs(row - K)];
             }
           }
+        }
+        for (int o = SUB >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (t < total && sl_ == 0) {
+          hS[sl * hot_cap + h] = acc;
+          hraw[sl * hot_cap + h] = lvl[ly * rawp + lx];
         }
       }
     }
     __syncthreads();
-    // (d) peaks of level rc = r - 1: candidates S > T_norm(rc), 3x3x3 maxima of S/r (R14)
-    if (li >= 2 && r - 1 >= P.r_min && r - 1 <= P.r_max) {
-      const int lc = li - 1, sc = lc % 3, rc = r - 1;
-      const int nh = min(hcnt[lc], P.hot_cap);
-      const double Tn = P.lvlTn[lc];
-      const uint16_t* hc = hcell + sc * P.hot_cap;
-      for (int h = tid; h < nh; h += K2_THREADS) {
-        int c16 = hc[h];
-        int iy = c16 / IDXS, ix = c16 - iy * IDXS;
-        if (ix < 1 || ix > T2 || iy < 1 || iy > T2) continue;    // interior cells only
-        long long S = hS[sc * P.hot_cap + h];
-        if (!((double)S > Tn)) continue;
-        int gy = Y0 - 1 + iy, gx = X0 - 1 + ix;
-        bool peak = true;
-        for (int dl = -1; dl <= 1 && peak; ++dl) {
-          const int l = lc + dl, sl = l % 3;
-          const long long ru = rlo + l;
-          const uint16_t* im = idx + sl * IDXS * IDXS;
-          const long long* hs = hS + sl * P.hot_cap;
-          for (int dy = -1; dy <= 1 && peak; ++dy) {
-            if (gy + dy < 0 || gy + dy >= H) continue;
-            for (int dx = -1; dx <= 1; ++dx) {
-              if (!dl && !dy && !dx) continue;
-              if (gx + dx < 0 || gx + dx >= W) continue;
-              int k = im[(iy + dy) * IDXS + ix + dx];
-              long long Su = k ? hs[k - 1] : 0;
-              long long lhs = S * ru, rhs = Su * (long long)rc;
-              bool v_first = dl > 0 || (dl == 0 && (dy > 0 || (dy == 0 && dx > 0)));
-              if (!(lhs > rhs || (lhs == rhs && v_first))) { peak = false; break; }
-            }
+    PMARK(3);
+    // (c0) hotspot bookkeeping: interior count, debug records, candidates S > T_norm(r)
+    //       for r in [r_min, r_max]
+    {
+      int pre = 0;
+      if (lane < G) pre = (L0 + lane < nlev) ? min(hcnt[L0 + lane], hot_cap) : 0;
+#pragma unroll
+      for (int o = 1; o < G; o <<= 1) {
+        const int n = __shfl_up_sync(0xffffffffu, pre, o);
+        if (lane >= o) pre += n;
+      }
+      int pg[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) pg[g] = __shfl_sync(0xffffffffu, pre, g);
+      for (int p = tid; p < pg[G - 1]; p += NT) {
+        int g = 0, base = 0;
+#pragma unroll
+        for (int q = 0; q < G - 1; ++q)
+          if (p >= pg[q]) { g = q + 1; base = pg[q]; }
+        const int li = L0 + g, sl = li % NSLOT, h = p - base;
+        const int c16 = hcell[sl * hot_cap + h];
+        const int iy = c16 / RING, ix = c16 - iy * RING;
+        if (ix < 1 || ix > T2 || iy < 1 || iy > T2) continue;     // interior cells only
+        ++my_hot;
+        const unsigned long long S = hS[sl * hot_cap + h];
+        if (P.debug) {
+          int kd = atomicAdd(&P.dbg_count[f], 1);
+          if (kd < P.dbg_cap) {
+            HotRec rec;
+            rec.r = rlo + li; rec.y = Y0 - 1 + iy; rec.x = X0 - 1 + ix; rec.raw = hraw[sl * hot_cap + h];
+            rec.S = (long long)S;
+            P.dbg_hot[(int64_t)f * P.dbg_cap + kd] = rec;
+          } else {
+            atomicOr(&P.flags[f], OVF_DEBUG);
           }
         }
-        if (peak) {
-          int k = atomicAdd(&P.peak_count[f], 1);
-          if (k < P.ring_cap) {
+        if (li >= 1 && li <= nlev - 2 && (double)(long long)S > tTn[li]) {
+          const int k = atomicAdd(&ccnt[li], 1);
+          cand[sl * hot_cap + k] = (uint16_t)h;   // k < hot_cap: candidates are hotspots
+        }
+      }
+    }
+    // (c1) undo: restore the counters touched in this step to zero
+    for (int i = tid; i < nact; i += NT) {
+      const int e = act[i];
+      const uint32_t rr = eR[e];
+      const int l0 = max((int)(rr & 0xFFFFu), L0), l1 = min((int)(rr >> 16), Lhi);
+      const double2 d = eD[e];
+      const uint32_t xy = eXY[e];
+      const int x = (int)(xy & 0xFFFFu), y = (int)(xy >> 16);
+      const double rd0 = (double)(rlo + L0);
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        if (L0 + g < l0 || L0 + g > l1) continue;
+        const double rd = rd0 + (double)g;
+        const int tx = x + (int)llround(__dmul_rn(rd, d.x));
+        const int ty = y + (int)llround(__dmul_rn(rd, d.y));
+        const int4 bb = box[g];
+        if (tx < bb.x || tx > bb.y || ty < bb.z || ty > bb.w) continue;
+        raw16[g * lvl_cells + (ty - RY0) * rawp + (tx - RX0)] = 0;
+      }
+    }
+    __syncthreads();
+    PMARK(4);
+    // (d) peaks of levels lc in [L0-1, Lhi-1]: 3x3x3 maxima of N = S/r (R14), one warp per
+    //     candidate; meanwhile the next step's setup (reads only static ray data)
+    {
+      const int lc0 = max(L0 - 1, 1), lc1 = min(Lhi - 1, nlev - 2);
+      int pre = 0;
+      if (lane < G) pre = (lc0 + lane <= lc1) ? ccnt[lc0 + lane] : 0;
+#pragma unroll
+      for (int o = 1; o < G; o <<= 1) {
+        const int n = __shfl_up_sync(0xffffffffu, pre, o);
+        if (lane >= o) pre += n;
+      }
+      int pg[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) pg[g] = __shfl_sync(0xffffffffu, pre, g);
+      for (int p = warp; p < pg[G - 1]; p += NW) {
+        int q = 0, base = 0;
+#pragma unroll
+        for (int t = 0; t < G - 1; ++t)
+          if (p >= pg[t]) { q = t + 1; base = pg[t]; }
+        const int lc = lc0 + q, sc = lc % NSLOT;
+        const int h = cand[sc * hot_cap + (p - base)];
+        const int c16 = hcell[sc * hot_cap + h];
+        const int iy = c16 / RING, ix = c16 - iy * RING;
+        const long long S = (long long)hS[sc * hot_cap + h];
+        const long long rc = rlo + lc;
+        bool beaten = false;
+#pragma unroll
+        for (int dl = -1; dl <= 1; ++dl) {
+          const int l = lc + dl, sl = l % NSLOT;
+          const int n = min(hcnt[l], hot_cap);
+          const long long ru = rlo + l;
+          for (int j = lane; j < n; j += 32) {
+            const int u16 = hcell[sl * hot_cap + j];
+            const int uy = u16 / RING, ux = u16 - uy * RING;
+            const int dy = uy - iy, dx = ux - ix;
+            if (dy < -1 || dy > 1 || dx < -1 || dx > 1 || (dl == 0 && dy == 0 && dx == 0)) continue;
+            const long long Su = (long long)hS[sl * hot_cap + j];
+            const long long lhs = S * ru, rhs = Su * rc;
+            const bool v_first = dl > 0 || (dl == 0 && (dy > 0 || (dy == 0 && dx > 0)));
+            if (!(lhs > rhs || (lhs == rhs && v_first))) beaten = true;
+          }
+        }
+        if (__any_sync(0xffffffffu, beaten)) continue;
+        if (lane == 0) {
+          const int kk = atomicAdd(&P.peak_count[f], 1);
+          if (kk < P.ring_cap) {
             Peak pk;
-            pk.x = gx; pk.y = gy; pk.r = rc; pk.raw = hraw[sc * P.hot_cap + h]; pk.S = S;
-            P.peaks[(int64_t)f * P.ring_cap + k] = pk;
+            pk.x = X0 - 1 + ix; pk.y = Y0 - 1 + iy; pk.r = (int)rc; pk.raw = hraw[sc * hot_cap + h]; pk.S = S;
+            P.peaks[(int64_t)f * P.ring_cap + kk] = pk;
           } else {
             atomicOr(&P.flags[f], OVF_RINGS);
           }
         }
       }
     }
+    if (L0 + G < nlev) setup(L0 + G);
     __syncthreads();
+    PMARK(5);
   }
+  if (P.prof && tid == 0) {
+#pragma unroll
+    for (int i = 0; i < 6; ++i) atomicAdd(&P.prof[i], t_acc[i]);
+    atomicAdd(&P.prof[15], 1ull);
+  }
+#undef PMARK
   // ---------------- counters
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -299,34 +460,43 @@ __global__ void __launch_bounds__(K2_THREADS, 2) k_hough(Params P, int max_bins)
     my_hot += __shfl_xor_sync(0xffffffffu, my_hot, o);
   }
   if (lane == 0) {
-    if (my_votes) atomicAdd(&P.stats[f].votes, my_votes);
+    if (my_votes) atomicAdd(&P.stats[f].votes, (unsigned long long)my_votes);
     if (my_hot) atomicAdd(&P.stats[f].hotspots, (unsigned long long)my_hot);
   }
   if (tid == 0 && *s_flags) atomicOr(&P.flags[f], *s_flags);
-  (void)s_votes;
-  (void)s_nhot;
 }
 
-size_t k_hough_smem(const Params& P, int max_bins) {
-  return k2_layout(P.hal, P.entry_cap, P.hot_cap, P.n_levels, P.wstride, max_bins).total;
+// Largest level-group size G whose shared-memory footprint fits the device.
+int k_hough_group(const Params& P, size_t smem_limit) {
+  for (int G : {8, 6, 4, 2})
+    if (k2_layout(G, P.hal, P.entry_cap, P.hot_cap, P.n_levels, P.wstride).total <= smem_limit) return G;
+  return 0;
 }
 
-int k_hough_max_bins(const Params& P) {
-  int span = T2 + 2 * P.hal + 2 * P.r_hi;
-  int n = span / T1 + 2;
-  return n * n;
+size_t k_hough_smem(const Params& P, int G) {
+  return k2_layout(G, P.hal, P.entry_cap, P.hot_cap, P.n_levels, P.wstride).total;
 }
 
-cudaError_t launch_hough(int n_frames, const Params& P, bool wide, cudaStream_t st) {
-  int mb = k_hough_max_bins(P);
-  size_t sm = k_hough_smem(P, mb);
-  dim3 grid(P.ntx * P.nty, n_frames);
-  if (wide) {
-    cudaFuncSetAttribute(k_hough<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_hough<true><<<grid, K2_THREADS, sm, st>>>(P, mb);
-  } else {
-    cudaFuncSetAttribute(k_hough<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_hough<false><<<grid, K2_THREADS, sm, st>>>(P, mb);
+int k_hough_max_entries() { return 65535; }
+
+template <bool Wd, int Gv>
+static void launch_one(int n_frames, const Params& P, cudaStream_t st) {
+  const size_t sm = k_hough_smem(P, Gv);
+  cudaFuncSetAttribute(k_hough<Wd, Gv>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_hough<Wd, Gv><<<dim3(P.ntx * P.nty, n_frames), NT, sm, st>>>(P);
+}
+
+cudaError_t launch_hough(int n_frames, const Params& P, bool wide, int G, cudaStream_t st) {
+  switch (G * 2 + (wide ? 1 : 0)) {
+    case 16: launch_one<false, 8>(n_frames, P, st); break;
+    case 17: launch_one<true, 8>(n_frames, P, st); break;
+    case 12: launch_one<false, 6>(n_frames, P, st); break;
+    case 13: launch_one<true, 6>(n_frames, P, st); break;
+    case 8: launch_one<false, 4>(n_frames, P, st); break;
+    case 9: launch_one<true, 4>(n_frames, P, st); break;
+    case 4: launch_one<false, 2>(n_frames, P, st); break;
+    case 5: launch_one<true, 2>(n_frames, P, st); break;
+    default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
 }

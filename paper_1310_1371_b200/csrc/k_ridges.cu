@@ -11,100 +11,139 @@
 //   -> kappa (fixed fp64 recipe, no FMA), ridge test on the tile, warp-ballot compaction.
 // The integer stages are exact, so their evaluation order is free; only the kappa /
 // direction recipe is order-sensitive and it is written with explicit _rn intrinsics.
+// Every stencil pass is register-blocked: a thread produces a strip of 8 outputs from a
+// sliding window held in registers (one shared-memory load per input, not per tap).
 #include "rd_internal.cuh"
 
 namespace rd {
 
-template <typename PixT>
+namespace {
+constexpr int GRS = T1 + 6;     // G region side (tile + 3)
+constexpr int KRS = T1 + 2;     // kappa region side (tile + 1)
+constexpr int SB = 8;           // strip length of the register-blocked passes
+}  // namespace
+
+template <typename PixT, int KS>
 __global__ void __launch_bounds__(K1_THREADS, 2)
 k_ridges(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, Params P) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int Ks = P.Ks;
-  const int IRS = T1 + 6 + 2 * Ks;      // input region side
-  constexpr int GRS = T1 + 6;           // G region side (tile + 3)
-  constexpr int KRS = T1 + 2;           // kappa region side (tile + 1)
-  double* sR = reinterpret_cast<double*>(smem);             // [IRS][GRS]
-  double* sG = sR + IRS * GRS;                               // [GRS][GRS]
-  double* sHA = sG + GRS * GRS;                              // [GRS][KRS]
+  constexpr int IRS = T1 + 6 + 2 * KS;  // input region side
+  constexpr int NTAP = 2 * KS + 1;
+  constexpr int RSTR = (GRS + SB - 1) / SB;   // row-pass strips per row
+  double* sR = reinterpret_cast<double*>(smem);              // [IRS][GRS]
+  double* sG = sR + IRS * GRS;                                // [GRS][GRS]
+  double* sHA = sG + GRS * GRS;                               // [GRS][KRS]
   double* sHB = sHA + GRS * KRS;
   double* sHC = sHB + GRS * KRS;
-  double* sK = sHC + GRS * KRS;                              // [KRS][KRS]
-  double2* sD = reinterpret_cast<double2*>(sK + KRS * KRS);  // [T1][T1]
-  int* sI = reinterpret_cast<int*>(sD + T1 * T1);            // [IRS][IRS]
-  int* sCnt = sI + IRS * IRS;                                // [32]
+  double* sK = sHC + GRS * KRS;                               // [KRS][KRS]
+  double2* sD = reinterpret_cast<double2*>(sK + KRS * KRS);   // [T1][T1]
+  int* sI = reinterpret_cast<int*>(sD + T1 * T1);             // [IRS][IRS + SB] (padded for strips)
+  int* sCnt = sI + IRS * (IRS + SB);                          // [33]
+  constexpr int IP = IRS + SB;                                // sI row pitch
 
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int f = blockIdx.z;
   const int x0 = blockIdx.x * T1, y0 = blockIdx.y * T1;
   const int W = P.W, H = P.H;
   const uint8_t* frame = frames + (int64_t)f * fstride;
+  int q[NTAP];
+#pragma unroll
+  for (int j = 0; j < NTAP; ++j) q[j] = P.q[j];
 
-  // 1. input region with replicate border
+  // 1. input region with replicate border (warp per row, lanes along the row)
   {
-    const int ox = x0 - 3 - Ks, oy = y0 - 3 - Ks;
-    for (int i = tid; i < IRS * IRS; i += K1_THREADS) {
-      int r = i / IRS, c = i - r * IRS;
-      int gy = min(max(oy + r, 0), H - 1), gx = min(max(ox + c, 0), W - 1);
-      sI[i] = (int)reinterpret_cast<const PixT*>(frame + (int64_t)gy * pitch)[gx];
+    const int ox = x0 - 3 - KS, oy = y0 - 3 - KS;
+    for (int r = warp; r < IRS; r += K1_THREADS / 32) {
+      const int gy = min(max(oy + r, 0), H - 1);
+      const PixT* row = reinterpret_cast<const PixT*>(frame + (int64_t)gy * pitch);
+      for (int c = lane; c < IRS; c += 32) sI[r * IP + c] = (int)__ldg(row + min(max(ox + c, 0), W - 1));
     }
   }
   __syncthreads();
   // 2. row pass (int32 exact: max_value * sum q < 2^31 checked at rd_create)
-  for (int i = tid; i < IRS * GRS; i += K1_THREADS) {
-    int r = i / GRS, c = i - r * GRS;
-    const int* row = sI + r * IRS + c;
-    int acc = 0;
-    for (int j = 0; j <= 2 * Ks; ++j) acc += P.q[j] * row[j];
-    sR[i] = (double)acc;
+  for (int it = tid; it < IRS * RSTR; it += K1_THREADS) {
+    const int r = it / RSTR, c0 = (it - r * RSTR) * SB;
+    const int* src = sI + r * IP + c0;
+    int v[SB + NTAP - 1];
+#pragma unroll
+    for (int j = 0; j < SB + NTAP - 1; ++j) v[j] = src[j];
+#pragma unroll
+    for (int o = 0; o < SB; ++o) {
+      int acc = 0;
+#pragma unroll
+      for (int j = 0; j < NTAP; ++j) acc += q[j] * v[o + j];
+      if (c0 + o < GRS) sR[r * GRS + c0 + o] = (double)acc;
+    }
   }
   __syncthreads();
-  // 3. column pass (fp64, exact)
-  for (int i = tid; i < GRS * GRS; i += K1_THREADS) {
-    int r = i / GRS, c = i - r * GRS;
-    const double* col = sR + r * GRS + c;
-    double acc = 0.0;
-    for (int k = 0; k <= 2 * Ks; ++k) acc = fma((double)P.q[k], col[k * GRS], acc);
-    sG[i] = acc;
+  // 3. column pass (fp64, exact): thread = (column, strip of SB rows)
+  for (int it = tid; it < GRS * ((GRS + SB - 1) / SB); it += K1_THREADS) {
+    const int c = it % GRS, r0 = (it / GRS) * SB;
+    double v[SB + NTAP - 1];
+#pragma unroll
+    for (int j = 0; j < SB + NTAP - 1; ++j) v[j] = (r0 + j < IRS) ? sR[(r0 + j) * GRS + c] : 0.0;
+#pragma unroll
+    for (int o = 0; o < SB; ++o) {
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < NTAP; ++j) acc = fma((double)q[j], v[o + j], acc);
+      if (r0 + o < GRS) sG[(r0 + o) * GRS + c] = acc;
+    }
   }
   __syncthreads();
-  // 4. horizontal Sobel passes on G (correlation; offsets -2..2)
-  for (int i = tid; i < GRS * KRS; i += K1_THREADS) {
-    int r = i / KRS, c = i - r * KRS;
-    const double* g = sG + r * GRS + c;
-    double g0 = g[0], g1 = g[1], g2 = g[2], g3 = g[3], g4 = g[4];
-    sHA[i] = (g0 + g4) - 2.0 * g2;                                  // d2 = [1,0,-2,0,1]
-    sHB[i] = (g0 + g4) + 4.0 * (g1 + g3) + 6.0 * g2;                // s5 = [1,4,6,4,1]
-    sHC[i] = (g4 - g0) + 2.0 * (g3 - g1);                           // d1 = [-1,-2,0,2,1]
+  // 4. horizontal Sobel passes on G (correlation; offsets -2..2): thread = (row, strip)
+  for (int it = tid; it < GRS * ((KRS + SB - 1) / SB); it += K1_THREADS) {
+    const int r = it / ((KRS + SB - 1) / SB), c0 = (it - r * ((KRS + SB - 1) / SB)) * SB;
+    double g[SB + 4];
+#pragma unroll
+    for (int j = 0; j < SB + 4; ++j) g[j] = (c0 + j < GRS) ? sG[r * GRS + c0 + j] : 0.0;
+#pragma unroll
+    for (int o = 0; o < SB; ++o) {
+      if (c0 + o >= KRS) break;
+      const double g0 = g[o], g1 = g[o + 1], g2 = g[o + 2], g3 = g[o + 3], g4 = g[o + 4];
+      sHA[r * KRS + c0 + o] = (g0 + g4) - 2.0 * g2;                       // d2 = [1,0,-2,0,1]
+      sHB[r * KRS + c0 + o] = (g0 + g4) + 4.0 * (g1 + g3) + 6.0 * g2;     // s5 = [1,4,6,4,1]
+      sHC[r * KRS + c0 + o] = (g4 - g0) + 2.0 * (g3 - g1);                // d1 = [-1,-2,0,2,1]
+    }
   }
   __syncthreads();
   // 5. vertical passes -> Ixx = s5_y (x) d2_x, Iyy = d2_y (x) s5_x, Ixy = d1_y (x) d1_x; kappa
   const double t_int = P.t_int;
-  for (int i = tid; i < KRS * KRS; i += K1_THREADS) {
-    int r = i / KRS, c = i - r * KRS;
-    int y = y0 - 1 + r, x = x0 - 1 + c;
-    double kap = HUGE_VAL;
-    double2 dir = make_double2(2.0, 2.0);  // 2.0 = "not a candidate"
-    if (x >= 2 && x <= W - 3 && y >= 2 && y <= H - 3) {
-      const double* a = sHA + r * KRS + c;
-      const double* b = sHB + r * KRS + c;
-      const double* d = sHC + r * KRS + c;
-      double Ixx = (a[0] + a[4 * KRS]) + 4.0 * (a[KRS] + a[3 * KRS]) + 6.0 * a[2 * KRS];
-      double Iyy = (b[0] + b[4 * KRS]) - 2.0 * b[2 * KRS];
-      double Ixy = (d[4 * KRS] - d[0]) + 2.0 * (d[3 * KRS] - d[KRS]);
-      double s, e;
-      kap = kappa_of(Ixx, Ixy, Iyy, &s, &e);
-      bool in_tile = r >= 1 && r <= T1 && c >= 1 && c <= T1;
-      if (in_tile && kap < t_int) {
-        double dx, dy;
-        if (direction_of(Ixy, e, s, &dx, &dy)) dir = make_double2(dx, dy);
-      }
+  for (int it = tid; it < KRS * ((KRS + SB - 1) / SB); it += K1_THREADS) {
+    const int c = it % KRS, r0 = (it / KRS) * SB;
+    double a[SB + 4], b[SB + 4], d[SB + 4];
+#pragma unroll
+    for (int j = 0; j < SB + 4; ++j) {
+      const bool ok = r0 + j < GRS;
+      a[j] = ok ? sHA[(r0 + j) * KRS + c] : 0.0;
+      b[j] = ok ? sHB[(r0 + j) * KRS + c] : 0.0;
+      d[j] = ok ? sHC[(r0 + j) * KRS + c] : 0.0;
     }
-    sK[i] = kap;
-    if (r >= 1 && r <= T1 && c >= 1 && c <= T1) sD[(r - 1) * T1 + (c - 1)] = dir;
+    const int x = x0 - 1 + c;
+#pragma unroll
+    for (int o = 0; o < SB; ++o) {
+      const int r = r0 + o;
+      if (r >= KRS) break;
+      const int y = y0 - 1 + r;
+      double kap = HUGE_VAL;
+      double2 dir = make_double2(2.0, 2.0);  // 2.0 = "not a candidate"
+      if (x >= 2 && x <= W - 3 && y >= 2 && y <= H - 3) {
+        const double Ixx = (a[o] + a[o + 4]) + 4.0 * (a[o + 1] + a[o + 3]) + 6.0 * a[o + 2];
+        const double Iyy = (b[o] + b[o + 4]) - 2.0 * b[o + 2];
+        const double Ixy = (d[o + 4] - d[o]) + 2.0 * (d[o + 3] - d[o + 1]);
+        double s, e;
+        kap = kappa_of(Ixx, Ixy, Iyy, &s, &e);
+        if (r >= 1 && r <= T1 && c >= 1 && c <= T1 && kap < t_int) {
+          double dx, dy;
+          if (direction_of(Ixy, e, s, &dx, &dy)) dir = make_double2(dx, dy);
+        }
+      }
+      sK[r * KRS + c] = kap;
+      if (r >= 1 && r <= T1 && c >= 1 && c <= T1) sD[(r - 1) * T1 + (c - 1)] = dir;
+    }
   }
   __syncthreads();
   // 6. ridge test (kappa_p <= kappa(after), kappa_p < kappa(before); R6) + compaction
-  const int warp = tid >> 5, lane = tid & 31;
   bool is_r[T1 * T1 / K1_THREADS];
   unsigned bal[T1 * T1 / K1_THREADS];
 #pragma unroll
@@ -163,23 +202,48 @@ k_ridges(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, Par
 }
 
 size_t k_ridges_smem(int Ks) {
-  const int IRS = T1 + 6 + 2 * Ks, GRS = T1 + 6, KRS = T1 + 2;
+  const int IRS = T1 + 6 + 2 * Ks;
   size_t dbl = (size_t)IRS * GRS + GRS * GRS + 3 * GRS * KRS + KRS * KRS + 2 * T1 * T1;
-  return dbl * 8 + (size_t)IRS * IRS * 4 + 33 * 4;
+  return dbl * 8 + (size_t)IRS * (IRS + SB) * 4 + 33 * 4;
+}
+
+template <typename PixT, int KS>
+static cudaError_t launch_t(const void* frames, int64_t pitch, int64_t fstride, int n_frames, const Params& P,
+                            cudaStream_t st) {
+  dim3 grid(P.nbx, P.nby, n_frames);
+  size_t sm = k_ridges_smem(KS);
+  cudaFuncSetAttribute(k_ridges<PixT, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_ridges<PixT, KS><<<grid, K1_THREADS, sm, st>>>((const uint8_t*)frames, pitch, fstride, P);
+  return cudaGetLastError();
+}
+
+template <typename PixT>
+static cudaError_t launch_p(const void* frames, int64_t pitch, int64_t fstride, int n, const Params& P,
+                            cudaStream_t st) {
+  switch (P.Ks) {
+    case 1: return launch_t<PixT, 1>(frames, pitch, fstride, n, P, st);
+    case 2: return launch_t<PixT, 2>(frames, pitch, fstride, n, P, st);
+    case 3: return launch_t<PixT, 3>(frames, pitch, fstride, n, P, st);
+    case 4: return launch_t<PixT, 4>(frames, pitch, fstride, n, P, st);
+    case 5: return launch_t<PixT, 5>(frames, pitch, fstride, n, P, st);
+    case 6: return launch_t<PixT, 6>(frames, pitch, fstride, n, P, st);
+    case 7: return launch_t<PixT, 7>(frames, pitch, fstride, n, P, st);
+    case 8: return launch_t<PixT, 8>(frames, pitch, fstride, n, P, st);
+    case 9: return launch_t<PixT, 9>(frames, pitch, fstride, n, P, st);
+    case 10: return launch_t<PixT, 10>(frames, pitch, fstride, n, P, st);
+    case 11: return launch_t<PixT, 11>(frames, pitch, fstride, n, P, st);
+    case 12: return launch_t<PixT, 12>(frames, pitch, fstride, n, P, st);
+    case 13: return launch_t<PixT, 13>(frames, pitch, fstride, n, P, st);
+    case 14: return launch_t<PixT, 14>(frames, pitch, fstride, n, P, st);
+    case 15: return launch_t<PixT, 15>(frames, pitch, fstride, n, P, st);
+  }
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_ridges(const void* frames, int64_t pitch, int64_t fstride, int n_frames, const Params& P,
                           cudaStream_t st) {
-  dim3 grid(P.nbx, P.nby, n_frames);
-  size_t sm = k_ridges_smem(P.Ks);
-  if (P.pixel_bytes == 1) {
-    cudaFuncSetAttribute(k_ridges<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_ridges<uint8_t><<<grid, K1_THREADS, sm, st>>>((const uint8_t*)frames, pitch, fstride, P);
-  } else {
-    cudaFuncSetAttribute(k_ridges<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_ridges<uint16_t><<<grid, K1_THREADS, sm, st>>>((const uint8_t*)frames, pitch, fstride, P);
-  }
-  return cudaGetLastError();
+  if (P.pixel_bytes == 1) return launch_p<uint8_t>(frames, pitch, fstride, n_frames, P, st);
+  return launch_p<uint16_t>(frames, pitch, fstride, n_frames, P, st);
 }
 
 // A3 in isolation (rd_eigen): the same recipe on caller-supplied Hessians.

@@ -14,9 +14,10 @@ size_t k_ridges_smem(int Ks);
 cudaError_t launch_ridges(const void* frames, int64_t pitch, int64_t fstride, int n_frames, const Params& P,
                           cudaStream_t st);
 cudaError_t launch_eigen(const double* abc, int64_t n, double* out, int* deg, cudaStream_t st);
-size_t k_hough_smem(const Params& P, int max_bins);
-int k_hough_max_bins(const Params& P);
-cudaError_t launch_hough(int n_frames, const Params& P, bool wide, cudaStream_t st);
+size_t k_hough_smem(const Params& P, int G);
+int k_hough_group(const Params& P, size_t smem_limit);
+int k_hough_max_entries();
+cudaError_t launch_hough(int n_frames, const Params& P, bool wide, int G, cudaStream_t st);
 size_t k_fit_smem(const Params& P);
 cudaError_t launch_fit(int n_frames, const Params& P, void* rings, int* counts, cudaStream_t st);
 }  // namespace rd
@@ -41,6 +42,7 @@ struct rd_detector {
   int max_batch;
   Params P;
   bool wide;
+  int G;
   // device allocations
   void* d_tables = nullptr;
   void* d_bins_count = nullptr;
@@ -61,6 +63,7 @@ struct rd_detector {
   bool timing = false;
   std::vector<cudaEvent_t> tev;  // 4 per timed call
   int n_timed = 0;
+  unsigned long long* d_prof = nullptr;
   bool have_last = false;
   int last_n = 0;
 };
@@ -104,7 +107,7 @@ rd_status rd_config_init(rd_config* c, int32_t width, int32_t height, int32_t pi
   c->max_rings_per_frame = 1024;
   c->max_ridges_per_tile = 512;
   c->max_entries_per_tile = 2048;
-  c->max_hotspots_per_level = 512;
+  c->max_hotspots_per_level = 256;
   c->debug = 0;
   return RD_OK;
 }
@@ -135,9 +138,10 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   if (!c.max_rings_per_frame) c.max_rings_per_frame = 1024;
   if (!c.max_ridges_per_tile) c.max_ridges_per_tile = 512;
   if (!c.max_entries_per_tile) c.max_entries_per_tile = 2048;
-  if (!c.max_hotspots_per_level) c.max_hotspots_per_level = 512;
+  if (!c.max_hotspots_per_level) c.max_hotspots_per_level = 256;
   if (c.max_ridges_per_tile > T1 * T1) c.max_ridges_per_tile = T1 * T1;
   if (c.max_hotspots_per_level > 65535) return RD_ERR_PARAM;
+  if (c.max_entries_per_tile > k_hough_max_entries()) c.max_entries_per_tile = k_hough_max_entries();
 
   // ---- host tables (DESIGN.md §2 A1, A5, A7, A8, A9)
   Params P;
@@ -177,6 +181,9 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   }
   if (Kmax > 48) return RD_ERR_CONFIG;  // raw tile halo bound (shared memory)
   P.K_max = Kmax;
+  // K_r = ceil(3 (a r + b) / den) <= (3a/den) r + 3b/den + 1 (+ margin): ray-interval bound in K2
+  P.k_slope = (float)(3.0 * c.sig_a / c.sig_den) * 1.0001f + 1e-6f;
+  P.k_icpt = (float)(3.0 * c.sig_b / c.sig_den + 1.0) + 0.01f;
   P.hal = Kmax + 1;
   P.wstride = Kmax + 1;
   std::vector<int> lvlW((size_t)P.n_levels * P.wstride, 0);
@@ -220,10 +227,11 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   e = cudaGetDeviceProperties(&prop, device);
   if (e != cudaSuccess) { delete det; return cuda_fail(e, "cudaGetDeviceProperties"); }
   size_t smax = prop.sharedMemPerBlockOptin;
-  if (k_ridges_smem(P.Ks) > smax || k_hough_smem(P, k_hough_max_bins(P)) > smax || k_fit_smem(P) > smax) {
+  det->G = k_hough_group(P, smax);
+  if (k_ridges_smem(P.Ks) > smax || det->G == 0 || k_fit_smem(P) > smax) {
     delete det;
-    snprintf(g_err, sizeof g_err, "shared memory: K1 %zu K2 %zu K3 %zu > %zu", k_ridges_smem(P.Ks),
-             k_hough_smem(P, k_hough_max_bins(P)), k_fit_smem(P), smax);
+    snprintf(g_err, sizeof g_err, "shared memory: K1 %zu K2(G=2) %zu K3 %zu > %zu", k_ridges_smem(P.Ks),
+             k_hough_smem(P, 2), k_fit_smem(P), smax);
     return RD_ERR_CONFIG;
   }
 
@@ -286,6 +294,7 @@ rd_status rd_destroy(rd_detector* det) {
   cudaFree(det->d_peaks);
   cudaFree(det->d_counters);
   cudaFree(det->d_dbg);
+  cudaFree(det->d_prof);
   for (int i = 0; i < 2; ++i) {
     cudaFree(det->d_stage[i]);
     cudaFree(det->d_rings_stage[i]);
@@ -325,7 +334,7 @@ static rd_status detect_impl(rd_detector* det, const void* d_frames, int64_t pit
   if (ev) CK(cudaEventRecord(ev[0], st));
   CK(launch_ridges(d_frames, pitch, fstride, n, P, st));
   if (ev) CK(cudaEventRecord(ev[1], st));
-  CK(launch_hough(n, P, det->wide, st));
+  CK(launch_hough(n, P, det->wide, det->G, st));
   if (ev) CK(cudaEventRecord(ev[2], st));
   CK(launch_fit(n, P, d_rings, d_counts, st));
   if (ev) CK(cudaEventRecord(ev[3], st));
@@ -517,6 +526,17 @@ rd_status rd_kernel_times(rd_detector* det, float* h_ms, int32_t* n_calls) {
   }
   for (int k = 0; k < 3; ++k) h_ms[k] = acc[k];
   *n_calls = det->n_timed;
+  return RD_OK;
+}
+
+rd_status rd_phase_cycles(rd_detector* det, int32_t on, uint64_t* h_cycles) {
+  if (!det) return RD_ERR_PARAM;
+  CK(cudaSetDevice(det->device));
+  if (!det->d_prof) CK(cudaMalloc(&det->d_prof, 16 * sizeof(unsigned long long)));
+  CK(cudaDeviceSynchronize());
+  if (h_cycles) CK(cudaMemcpy(h_cycles, det->d_prof, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  CK(cudaMemset(det->d_prof, 0, 16 * sizeof(unsigned long long)));
+  det->P.prof = on ? det->d_prof : nullptr;
   return RD_OK;
 }
 

@@ -40,6 +40,7 @@ struct Params {
   int T_raw;
   int K_max;                    // largest level half-width
   int hal;                      // K2 raw halo = K_max + 1
+  float k_slope, k_icpt;        // K_r <= k_slope * r + k_icpt (conservative, for ray intervals)
   // level tables (device, n_levels entries, index r - r_lo)
   const int* lvlK;              // K_r
   const int* lvlW;              // [n_levels][WSTRIDE] w_r(0..K_r), 2^12 fixed point
@@ -61,6 +62,7 @@ struct Params {
   int* flags;                   // [F] overflow bits
   Stats* stats;                 // [F]
   int debug;
+  unsigned long long* prof;     // optional per-phase cycle counters (rd_phase_cycles), may be null
   int dbg_cap;
   HotRec* dbg_hot;              // [F][dbg_cap]
   int* dbg_count;               // [F]

@@ -153,3 +153,10 @@ def eigen(abc: torch.Tensor):
     st = torch.cuda.current_stream(abc.device)
     check(lib().rd_eigen(abc.data_ptr(), n, out.data_ptr(), deg.data_ptr(), C.c_void_p(st.cuda_stream)), "rd_eigen")
     return out, deg
+
+
+def phase_cycles(det: Detector, on: bool) -> np.ndarray:
+    """Read-and-reset the Hough kernel's per-phase cycle counters; enable/disable them."""
+    out = np.zeros(16, np.uint64)
+    check(lib().rd_phase_cycles(det._h, 1 if on else 0, out.ctypes.data), "rd_phase_cycles")
+    return out

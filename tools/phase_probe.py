@@ -1,0 +1,36 @@
+"""Per-phase cycle breakdown of the Hough kernel and per-kernel event times on cfg3."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_1310_1371_b200 as rd  # noqa: E402
+from paper_1310_1371_b200.detector import phase_cycles  # noqa: E402
+import synth  # noqa: E402
+
+cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+B = int(sys.argv[2]) if len(sys.argv) > 2 else 128
+params = synth.preset(cfg)
+frames = torch.from_numpy(synth.batch(cfg, 0, 0, B)).cuda()
+det = rd.Detector(params, max_batch=B)
+for _ in range(2):
+    det.detect(frames)
+det.sync()
+det.set_timing(True)
+for _ in range(3):
+    det.detect(frames)
+det.sync()
+ms, n = det.kernel_times()
+print("kernel us/frame:", [round(1000 * m / n / B, 2) for m in ms])
+det.set_timing(False)
+phase_cycles(det, True)
+det.detect(frames)
+det.sync()
+c = phase_cycles(det, False)
+names = ["rays", "setup0", "votes", "S", "cand+undo", "nms+setup"]
+ncta = int(c[15])
+tot = sum(int(x) for x in c[:6])
+print("CTAs", ncta, "cycles/CTA", tot / max(ncta, 1))
+for i, nm in enumerate(names):
+    print(f"  {nm:10s} {int(c[i]) / max(ncta, 1):10.0f} cyc/CTA  {100 * int(c[i]) / max(tot, 1):5.1f}%")
