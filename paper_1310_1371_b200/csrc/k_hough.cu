@@ -1,5 +1,5 @@
 // k_hough.cu — K2: directed voting, hotspot registration, radius-dependent smoothing
-// with 1/r normalisation and 3x3x3 peak extraction, one CTA per (frame, 64x64 tile).
+// with 1/r normalisation and 3x3x3 peak extraction, one CTA per (frame, T x T tile).
 //
 // Rows A5-A8 of DESIGN.md §2 (SI steps 2-4, PAPER.md:931-978;
 // range extension PAPER.md:998-1001).  The CTA owns the accumulator cells of its tile and
@@ -10,23 +10,21 @@
 //                  paper's rolling level window, 3 levels -> G + 2.
 // Voting rays (a ridge pixel, a sense of rho and the level interval in which its votes can
 // land in the tile's level boxes) are gathered once per CTA.  Each G-level step compacts
-// the rays active in it and walks them entry-major over the levels they reach.
+// the rays active in it; the (ray, level) pairs of the step are dealt evenly to the threads
+// and processed four at a time (independent targets, then independent atomics).
 // A hotspot is registered by the one atomic that lifts its counter past T_raw (the paper's
-// "surpassed" test at increment time).  S is computed for hotspots only:
-// every (hotspot, window row) pair is one thread's row sum, reduced with 64-bit shared
-// atomics (integer sums: order-free, exact).  NMS of a level runs once the level above is
-// complete, one warp per candidate scanning three neighbouring lists.
-// Counters are cleared by undoing exactly the cells this CTA incremented (the paper's
-// register-and-undo).  Only peak records (and optional debug hotspots)
-// leave the SM.
+// "surpassed" test at increment time).  S is computed for hotspots only,
+// a sub-warp per hotspot with lanes over window rows.  NMS of a level runs once the level
+// above is complete, one warp per candidate scanning three neighbouring
+// lists.  Counters are cleared by undoing exactly the cells this CTA incremented (the
+// paper's register-and-undo).  Only peak records (and optional debug
+// hotspots) leave the SM.
 #include "rd_internal.cuh"
 
 namespace rd {
 
 namespace {
-constexpr int RING = T2 + 2;      // tile + 1 ring side (hotspot registration region)
-constexpr int NT = 512;           // threads per CTA
-constexpr int NW = NT / 32;
+constexpr int BATCH = 4;          // (ray, level) pairs in flight per thread
 
 struct K2Smem {
   int raws, rawp;                 // raw side and row pitch (uint16 units)
@@ -36,10 +34,11 @@ struct K2Smem {
 
 __host__ __device__ inline size_t align16(size_t v) { return (v + 15) & ~size_t(15); }
 
-__host__ __device__ inline K2Smem k2_layout(int G, int hal, int entry_cap, int hot_cap, int n_levels, int wstride) {
+__host__ __device__ inline K2Smem k2_layout(int G, int T, int hal, int entry_cap, int hot_cap, int n_levels,
+                                            int wstride) {
   const int NSLOT = G + 2;
   K2Smem L;
-  L.raws = T2 + 2 * hal;
+  L.raws = T + 2 * hal;
   // row pitch with an odd number of 32-bit words: the rows of a window fall in distinct banks
   L.rawp = ((L.raws / 2) & 1) ? L.raws : L.raws + 2;
   size_t o = 0;
@@ -52,7 +51,7 @@ __host__ __device__ inline K2Smem k2_layout(int G, int hal, int entry_cap, int h
   L.off_hcell = o; o = align16(o + 2 * (size_t)NSLOT * hot_cap);
   L.off_hraw = o;  o = align16(o + 2 * (size_t)NSLOT * hot_cap);
   L.off_cand = o;  o = align16(o + 2 * (size_t)NSLOT * hot_cap);
-  L.off_hcnt = o;  o = align16(o + 4 * (size_t)(n_levels + G + 8));
+  L.off_hcnt = o;  o = align16(o + 4 * (size_t)(n_levels + G + 16));
   L.off_ccnt = o;  o = align16(o + 4 * (size_t)(n_levels + G));
   L.off_w = o;     o = align16(o + 4 * (size_t)n_levels * wstride);   // level tables, resident
   L.off_k = o;     o = align16(o + 4 * (size_t)n_levels);
@@ -68,13 +67,39 @@ __device__ __forceinline__ void half_ge(float a, float b, float& lo, float& hi) 
   else if (a < 0.f) hi = fminf(hi, __fdividef(b, a));
   else if (b > 0.f) hi = -1e30f;
 }
+
+template <int G>
+__device__ __forceinline__ int warp_prefix_lookup(const int (&pg)[G], int t, int& base) {
+  int g = 0;
+  base = 0;
+#pragma unroll
+  for (int q = 0; q < G - 1; ++q)
+    if (t >= pg[q]) { g = q + 1; base = pg[q]; }
+  return g;
+}
+
+// inclusive prefix over lanes 0..G-1 of `v`, broadcast to every lane as pg[0..G-1]
+template <int G>
+__device__ __forceinline__ void warp_prefix(int v, int lane, int (&pg)[G]) {
+#pragma unroll
+  for (int o = 1; o < G; o <<= 1) {
+    const int n = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += n;
+  }
+#pragma unroll
+  for (int q = 0; q < G; ++q) pg[q] = __shfl_sync(0xffffffffu, v, q);
+}
 }  // namespace
 
-template <bool kWide, int G>
-__global__ void __launch_bounds__(NT, 1) k_hough(Params P) {
+template <bool kWide, int G, int MINB>
+__global__ void __launch_bounds__(512, MINB) k_hough(Params P) {
   constexpr int NSLOT = G + 2;
+  constexpr int LG = G == 8 ? 3 : G == 4 ? 2 : 1;
+  static_assert((1 << LG) == G, "G must be a power of two");
   extern __shared__ __align__(16) unsigned char smem[];
-  const K2Smem L = k2_layout(G, P.hal, P.entry_cap, P.hot_cap, P.n_levels, P.wstride);
+  const int T = P.k2t;
+  const int RING = T + 2;          // tile + 1 ring side (hotspot registration region)
+  const K2Smem L = k2_layout(G, T, P.hal, P.entry_cap, P.hot_cap, P.n_levels, P.wstride);
   unsigned long long* hS = reinterpret_cast<unsigned long long*>(smem + L.off_hS);  // [NSLOT][hot_cap]
   double2* eD = reinterpret_cast<double2*>(smem + L.off_ed);             // [entry_cap] (s*dx, s*dy)
   uint32_t* raw32 = reinterpret_cast<uint32_t*>(smem + L.off_raw);       // [G] packed uint16 levels
@@ -94,12 +119,14 @@ __global__ void __launch_bounds__(NT, 1) k_hough(Params P) {
   int* s_ecnt = hcnt + P.n_levels + G;
   int* s_flags = s_ecnt + 1;
   int* s_nact = s_ecnt + 2;                                              // [2], by step parity
+  int* s_bin = s_ecnt + 4;                                               // work-stealing bin counter
 
+  const int NT = blockDim.x, NW = NT >> 5;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int f = blockIdx.y;
   const int tile = blockIdx.x;
   const int tyi = tile / P.ntx, txi = tile - tyi * P.ntx;
-  const int X0 = txi * T2, Y0 = tyi * T2;
+  const int X0 = txi * T, Y0 = tyi * T;
   const int W = P.W, H = P.H, hal = P.hal;
   const int RX0 = X0 - hal, RY0 = Y0 - hal;   // raw buffer origin
   const int rawp = L.rawp;
@@ -116,7 +143,7 @@ __global__ void __launch_bounds__(NT, 1) k_hough(Params P) {
     t_acc[i] += (unsigned long long)(t_ - t_last);    \
     t_last = t_;                                      \
   }
-  for (int i = tid; i < nlev + G + 8; i += NT) hcnt[i] = 0;
+  for (int i = tid; i < nlev + G + 16; i += NT) hcnt[i] = 0;
   for (int i = tid; i < nlev + G; i += NT) ccnt[i] = 0;
   for (int i = tid; i < nlev * P.wstride; i += NT) tW[i] = P.lvlW[i];
   for (int i = tid; i < nlev; i += NT) {
@@ -129,20 +156,23 @@ __global__ void __launch_bounds__(NT, 1) k_hough(Params P) {
     for (int i = tid; i < n4; i += NT) r4[i] = make_uint4(0, 0, 0, 0);
     for (int i = n4 * 8 + tid; i < G * lvl_cells; i += NT) raw16[i] = 0;
   }
+  __syncthreads();
 
   // ---------------- phase 0: voting rays that can reach the tile's level boxes
   {
-    const int hmax = hal;  // level boxes are inside tile + hal
-    const int bx0 = max(X0 - hmax, 0), bx1 = min(X0 + T2 - 1 + hmax, W - 1);
-    const int by0 = max(Y0 - hmax, 0), by1 = min(Y0 + T2 - 1 + hmax, H - 1);
+    const int bx0 = max(X0 - hal, 0), bx1 = min(X0 + T - 1 + hal, W - 1);
+    const int by0 = max(Y0 - hal, 0), by1 = min(Y0 + T - 1 + hal, H - 1);
     const int nbx = P.nbx;
     const int cbx0 = max((bx0 - rhi) / T1, 0), cbx1 = min((bx1 + rhi) / T1, P.nbx - 1);
     const int cby0 = max((by0 - rhi) / T1, 0), cby1 = min((by1 + rhi) / T1, P.nby - 1);
     const int nbw = cbx1 - cbx0 + 1, nbins = nbw * (cby1 - cby0 + 1);
     const int64_t fbins = (int64_t)f * P.nbx * P.nby;
     const float m = P.k_slope, c = P.k_icpt;
-    __syncthreads();
-    for (int b = warp; b < nbins; b += NW) {  // warp per ridge bin, lanes over (ridge, sense)
+    for (;;) {  // warps take ridge bins dynamically; lanes over (ridge, sense)
+      int b = 0;
+      if (lane == 0) b = atomicAdd(s_bin, 1);
+      b = __shfl_sync(0xffffffffu, b, 0);
+      if (b >= nbins) break;
       const int by = cby0 + b / nbw, bx = cbx0 + b % nbw;
       const int64_t bin = fbins + by * nbx + bx;
       const int cnt = P.bin_count[bin];
@@ -158,11 +188,11 @@ __global__ void __launch_bounds__(NT, 1) k_hough(Params P) {
         const float fu = (float)u, fv = (float)v, fx = (float)x, fy = (float)y;
         float lo = (float)rlo, hi = (float)rhi;
         half_ge(fu + m, (float)X0 - 1.5f - c - fx, lo, hi);
-        half_ge(m - fu, fx - (float)(X0 + T2) - 0.5f - c, lo, hi);
+        half_ge(m - fu, fx - (float)(X0 + T) - 0.5f - c, lo, hi);
         half_ge(fu, -0.5f - fx, lo, hi);
         half_ge(-fu, fx - (float)W + 0.5f, lo, hi);
         half_ge(fv + m, (float)Y0 - 1.5f - c - fy, lo, hi);
-        half_ge(m - fv, fy - (float)(Y0 + T2) - 0.5f - c, lo, hi);
+        half_ge(m - fv, fy - (float)(Y0 + T) - 0.5f - c, lo, hi);
         half_ge(fv, -0.5f - fy, lo, hi);
         half_ge(-fv, fy - (float)H + 0.5f, lo, hi);
         if (hi < lo - 2.f) continue;
@@ -185,14 +215,14 @@ __global__ void __launch_bounds__(NT, 1) k_hough(Params P) {
   int my_votes = 0, my_hot = 0;
   const uint32_t T_raw = (uint32_t)P.T_raw;
 
-  // per-step setup: weights, level boxes, compacted active rays (into parity buffer)
+  // per-step setup: level boxes and the compacted active rays (into the parity counter)
   auto setup = [&](int L0s) {
     const int Lhs = min(L0s + G - 1, nlev - 1);
     if (tid < G) {
       const int K = (L0s + tid < nlev) ? tK[L0s + tid] : 0;
-      box[tid] = make_int4(max(X0 - K - 1, 0), min(X0 + T2 + K, W - 1), max(Y0 - K - 1, 0), min(Y0 + T2 + K, H - 1));
+      box[tid] = make_int4(max(X0 - K - 1, 0), min(X0 + T + K, W - 1), max(Y0 - K - 1, 0), min(Y0 + T + K, H - 1));
     }
-    int* cnt = s_nact + ((L0s / G) & 1);
+    int* cnt = s_nact + ((L0s >> LG) & 1);
     for (int e0 = 0; e0 < ne; e0 += NT) {
       const int e = e0 + tid;
       bool a = false;
@@ -207,60 +237,57 @@ __global__ void __launch_bounds__(NT, 1) k_hough(Params P) {
       if (a) act[base + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)e;
     }
   };
-  if (tid == 0) { s_nact[0] = 0; s_nact[1] = 0; }
-  __syncthreads();
   setup(0);
   __syncthreads();
   PMARK(1);
 
+  // target cell of pair (ray e, level L0+g) in the raw buffers, or -1 (not in the level box)
+  auto target = [&](int e, int g, int L0s, int& tx, int& ty) -> int {
+    const uint32_t rr = eR[e];
+    const int li = L0s + g;
+    if (li < (int)(rr & 0xFFFFu) || li > (int)(rr >> 16)) return -1;
+    const double2 d = eD[e];
+    const uint32_t xy = eXY[e];
+    const double rd = (double)(rlo + li);
+    tx = (int)(xy & 0xFFFFu) + (int)llround(__dmul_rn(rd, d.x));
+    ty = (int)(xy >> 16) + (int)llround(__dmul_rn(rd, d.y));
+    const int4 bb = box[g];
+    if (tx < bb.x || tx > bb.y || ty < bb.z || ty > bb.w) return -1;
+    return g * lvl_cells + (ty - RY0) * rawp + (tx - RX0);
+  };
+
   // ---------------- level sweep, G levels per step
   for (int L0 = 0; L0 < nlev; L0 += G) {
     const int Lhi = min(L0 + G - 1, nlev - 1);
-    const int par = (L0 / G) & 1;
-    const int nact = s_nact[par];
-    // (a) votes of levels L0..Lhi: per active ray, the G
-    //     targets are computed first and their atomics issued back to back (ILP)
-    for (int i = tid; i < nact; i += NT) {
-      const int e = act[i];
-      const uint32_t rr = eR[e];
-      const int l0 = max((int)(rr & 0xFFFFu), L0), l1 = min((int)(rr >> 16), Lhi);
-      const double2 d = eD[e];
-      const uint32_t xy = eXY[e];
-      const int x = (int)(xy & 0xFFFFu), y = (int)(xy >> 16);
-      const double rd0 = (double)(rlo + L0);
-      int cell[G], txs[G], tys[G];
+    const int par = (L0 >> LG) & 1;
+    const int npair = s_nact[par] << LG;   // (active ray, level) pairs, ray-major
+    // (a) votes of levels L0..Lhi
+    for (int p0 = tid; p0 < npair; p0 += BATCH * NT) {
+      int cell[BATCH], txs[BATCH], tys[BATCH];
+      uint32_t old[BATCH];
 #pragma unroll
-      for (int g = 0; g < G; ++g) {
-        cell[g] = -1;
-        if (L0 + g < l0 || L0 + g > l1) continue;
-        const double rd = rd0 + (double)g;
-        const int tx = x + (int)llround(__dmul_rn(rd, d.x));
-        const int ty = y + (int)llround(__dmul_rn(rd, d.y));
-        const int4 bb = box[g];
-        if (tx < bb.x || tx > bb.y || ty < bb.z || ty > bb.w) continue;
-        cell[g] = g * lvl_cells + (ty - RY0) * rawp + (tx - RX0);
-        txs[g] = tx;
-        tys[g] = ty;
+      for (int k = 0; k < BATCH; ++k) {
+        const int p = p0 + k * NT;
+        cell[k] = p < npair ? target(act[p >> LG], p & (G - 1), L0, txs[k], tys[k]) : -1;
       }
-      uint32_t old[G];
 #pragma unroll
-      for (int g = 0; g < G; ++g)
-        if (cell[g] >= 0) old[g] = atomicAdd(&raw32[cell[g] >> 1], 1u << ((cell[g] & 1) << 4));
+      for (int k = 0; k < BATCH; ++k)
+        if (cell[k] >= 0) old[k] = atomicAdd(&raw32[cell[k] >> 1], 1u << ((cell[k] & 1) << 4));
 #pragma unroll
-      for (int g = 0; g < G; ++g) {
-        if (cell[g] < 0) continue;
-        const int tx = txs[g], ty = tys[g];
-        const uint32_t oc = (old[g] >> ((cell[g] & 1) << 4)) & 0xFFFFu;
+      for (int k = 0; k < BATCH; ++k) {
+        if (cell[k] < 0) continue;
+        const int tx = txs[k], ty = tys[k];
+        const uint32_t oc = (old[k] >> ((cell[k] & 1) << 4)) & 0xFFFFu;
         if (oc == T_raw) {
           const int ix = tx - (X0 - 1), iy = ty - (Y0 - 1);
           if ((unsigned)ix < (unsigned)RING && (unsigned)iy < (unsigned)RING) {
-            const int li = L0 + g;
+            const int li = L0 + ((p0 + k * NT) & (G - 1));
             const int h = atomicAdd(&hcnt[li], 1);
             if (h < hot_cap) hcell[(li % NSLOT) * hot_cap + h] = (uint16_t)(iy * RING + ix);
             else atomicOr(s_flags, OVF_HOTSPOTS);
           }
         }
-        my_votes += ((unsigned)(tx - X0) < (unsigned)T2) & ((unsigned)(ty - Y0) < (unsigned)T2);
+        my_votes += ((unsigned)(tx - X0) < (unsigned)T) & ((unsigned)(ty - Y0) < (unsigned)T);
       }
     }
     if (tid == 0) s_nact[par ^ 1] = 0;   // counter of the next step (last read a barrier ago)
@@ -270,26 +297,16 @@ __global__ void __launch_bounds__(NT, 1) k_hough(Params P) {
     //     a sub-warp of SUB >= 2K+1 lanes per hotspot, lanes over window rows, shuffle sum;
     //     the hotspots of all G levels are processed concurrently
     {
-      int pre = 0;
-      if (lane < G) pre = (L0 + lane < nlev) ? min(hcnt[L0 + lane], hot_cap) : 0;
-#pragma unroll
-      for (int o = 1; o < G; o <<= 1) {
-        const int nn = __shfl_up_sync(0xffffffffu, pre, o);
-        if (lane >= o) pre += nn;
-      }
       int pg[G];
-#pragma unroll
-      for (int q = 0; q < G; ++q) pg[q] = __shfl_sync(0xffffffffu, pre, q);
+      warp_prefix<G>(lane < G && L0 + lane < nlev ? min(hcnt[L0 + lane], hot_cap) : 0, lane, pg);
       const int Rmx = 2 * tK[Lhi] + 1;   // K_r is non-decreasing in r
       const int SUB = Rmx <= 4 ? 4 : Rmx <= 8 ? 8 : Rmx <= 16 ? 16 : 32;
       const int per = 32 / SUB, sub = lane / SUB, sl_ = lane - sub * SUB;
       const int total = pg[G - 1];
       for (int tb = warp * per; tb < total; tb += NW * per) {
         const int t = tb + sub;
-        int g = 0, base = 0;
-#pragma unroll
-        for (int q = 0; q < G - 1; ++q)
-          if (t >= pg[q]) { g = q + 1; base = pg[q]; }
+        int base;
+        const int g = warp_prefix_lookup<G>(pg, t, base);
         const int li = min(L0 + g, nlev - 1), h = t - base;
         const int K = tK[li], R = 2 * K + 1;
         const int sl = li % NSLOT;
@@ -328,25 +345,15 @@ __global__ void __launch_bounds__(NT, 1) k_hough(Params P) {
     // (c0) hotspot bookkeeping: interior count, debug records, candidates S > T_norm(r)
     //       for r in [r_min, r_max]
     {
-      int pre = 0;
-      if (lane < G) pre = (L0 + lane < nlev) ? min(hcnt[L0 + lane], hot_cap) : 0;
-#pragma unroll
-      for (int o = 1; o < G; o <<= 1) {
-        const int n = __shfl_up_sync(0xffffffffu, pre, o);
-        if (lane >= o) pre += n;
-      }
       int pg[G];
-#pragma unroll
-      for (int g = 0; g < G; ++g) pg[g] = __shfl_sync(0xffffffffu, pre, g);
+      warp_prefix<G>(lane < G && L0 + lane < nlev ? min(hcnt[L0 + lane], hot_cap) : 0, lane, pg);
       for (int p = tid; p < pg[G - 1]; p += NT) {
-        int g = 0, base = 0;
-#pragma unroll
-        for (int q = 0; q < G - 1; ++q)
-          if (p >= pg[q]) { g = q + 1; base = pg[q]; }
+        int base;
+        const int g = warp_prefix_lookup<G>(pg, p, base);
         const int li = L0 + g, sl = li % NSLOT, h = p - base;
         const int c16 = hcell[sl * hot_cap + h];
         const int iy = c16 / RING, ix = c16 - iy * RING;
-        if (ix < 1 || ix > T2 || iy < 1 || iy > T2) continue;     // interior cells only
+        if (ix < 1 || ix > T || iy < 1 || iy > T) continue;     // interior cells only
         ++my_hot;
         const unsigned long long S = hS[sl * hot_cap + h];
         if (P.debug) {
@@ -367,24 +374,16 @@ __global__ void __launch_bounds__(NT, 1) k_hough(Params P) {
       }
     }
     // (c1) undo: restore the counters touched in this step to zero
-    for (int i = tid; i < nact; i += NT) {
-      const int e = act[i];
-      const uint32_t rr = eR[e];
-      const int l0 = max((int)(rr & 0xFFFFu), L0), l1 = min((int)(rr >> 16), Lhi);
-      const double2 d = eD[e];
-      const uint32_t xy = eXY[e];
-      const int x = (int)(xy & 0xFFFFu), y = (int)(xy >> 16);
-      const double rd0 = (double)(rlo + L0);
+    for (int p0 = tid; p0 < npair; p0 += BATCH * NT) {
+      int cell[BATCH], tx, ty;
 #pragma unroll
-      for (int g = 0; g < G; ++g) {
-        if (L0 + g < l0 || L0 + g > l1) continue;
-        const double rd = rd0 + (double)g;
-        const int tx = x + (int)llround(__dmul_rn(rd, d.x));
-        const int ty = y + (int)llround(__dmul_rn(rd, d.y));
-        const int4 bb = box[g];
-        if (tx < bb.x || tx > bb.y || ty < bb.z || ty > bb.w) continue;
-        raw16[g * lvl_cells + (ty - RY0) * rawp + (tx - RX0)] = 0;
+      for (int k = 0; k < BATCH; ++k) {
+        const int p = p0 + k * NT;
+        cell[k] = p < npair ? target(act[p >> LG], p & (G - 1), L0, tx, ty) : -1;
       }
+#pragma unroll
+      for (int k = 0; k < BATCH; ++k)
+        if (cell[k] >= 0) raw16[cell[k]] = 0;
     }
     __syncthreads();
     PMARK(4);
@@ -392,21 +391,11 @@ __global__ void __launch_bounds__(NT, 1) k_hough(Params P) {
     //     candidate; meanwhile the next step's setup (reads only static ray data)
     {
       const int lc0 = max(L0 - 1, 1), lc1 = min(Lhi - 1, nlev - 2);
-      int pre = 0;
-      if (lane < G) pre = (lc0 + lane <= lc1) ? ccnt[lc0 + lane] : 0;
-#pragma unroll
-      for (int o = 1; o < G; o <<= 1) {
-        const int n = __shfl_up_sync(0xffffffffu, pre, o);
-        if (lane >= o) pre += n;
-      }
       int pg[G];
-#pragma unroll
-      for (int g = 0; g < G; ++g) pg[g] = __shfl_sync(0xffffffffu, pre, g);
+      warp_prefix<G>(lane < G && lc0 + lane <= lc1 ? ccnt[lc0 + lane] : 0, lane, pg);
       for (int p = warp; p < pg[G - 1]; p += NW) {
-        int q = 0, base = 0;
-#pragma unroll
-        for (int t = 0; t < G - 1; ++t)
-          if (p >= pg[t]) { q = t + 1; base = pg[t]; }
+        int base;
+        const int q = warp_prefix_lookup<G>(pg, p, base);
         const int lc = lc0 + q, sc = lc % NSLOT;
         const int h = cand[sc * hot_cap + (p - base)];
         const int c16 = hcell[sc * hot_cap + h];
@@ -466,36 +455,34 @@ __global__ void __launch_bounds__(NT, 1) k_hough(Params P) {
   if (tid == 0 && *s_flags) atomicOr(&P.flags[f], *s_flags);
 }
 
-// Largest level-group size G whose shared-memory footprint fits the device.
-int k_hough_group(const Params& P, size_t smem_limit) {
-  for (int G : {8, 6, 4, 2})
-    if (k2_layout(G, P.hal, P.entry_cap, P.hot_cap, P.n_levels, P.wstride).total <= smem_limit) return G;
-  return 0;
-}
-
 size_t k_hough_smem(const Params& P, int G) {
-  return k2_layout(G, P.hal, P.entry_cap, P.hot_cap, P.n_levels, P.wstride).total;
+  return k2_layout(G, P.k2t, P.hal, P.entry_cap, P.hot_cap, P.n_levels, P.wstride).total;
 }
 
 int k_hough_max_entries() { return 65535; }
 
-template <bool Wd, int Gv>
-static void launch_one(int n_frames, const Params& P, cudaStream_t st) {
+template <bool Wd, int Gv, int MB>
+static void launch_one(int n_frames, const Params& P, int nt, cudaStream_t st) {
   const size_t sm = k_hough_smem(P, Gv);
-  cudaFuncSetAttribute(k_hough<Wd, Gv>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_hough<Wd, Gv><<<dim3(P.ntx * P.nty, n_frames), NT, sm, st>>>(P);
+  cudaFuncSetAttribute(k_hough<Wd, Gv, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_hough<Wd, Gv, MB><<<dim3(P.ntx * P.nty, n_frames), nt, sm, st>>>(P);
 }
 
-cudaError_t launch_hough(int n_frames, const Params& P, bool wide, int G, cudaStream_t st) {
-  switch (G * 2 + (wide ? 1 : 0)) {
-    case 16: launch_one<false, 8>(n_frames, P, st); break;
-    case 17: launch_one<true, 8>(n_frames, P, st); break;
-    case 12: launch_one<false, 6>(n_frames, P, st); break;
-    case 13: launch_one<true, 6>(n_frames, P, st); break;
-    case 8: launch_one<false, 4>(n_frames, P, st); break;
-    case 9: launch_one<true, 4>(n_frames, P, st); break;
-    case 4: launch_one<false, 2>(n_frames, P, st); break;
-    case 5: launch_one<true, 2>(n_frames, P, st); break;
+cudaError_t launch_hough(int n_frames, const Params& P, bool wide, int G, int nt, int minb, cudaStream_t st) {
+  const int key = (G << 2) | (wide ? 2 : 0) | (minb > 1 ? 1 : 0);
+  switch (key) {
+    case (8 << 2) | 0: launch_one<false, 8, 1>(n_frames, P, nt, st); break;
+    case (8 << 2) | 2: launch_one<true, 8, 1>(n_frames, P, nt, st); break;
+    case (8 << 2) | 1: launch_one<false, 8, 2>(n_frames, P, nt, st); break;
+    case (8 << 2) | 3: launch_one<true, 8, 2>(n_frames, P, nt, st); break;
+    case (4 << 2) | 0: launch_one<false, 4, 1>(n_frames, P, nt, st); break;
+    case (4 << 2) | 2: launch_one<true, 4, 1>(n_frames, P, nt, st); break;
+    case (4 << 2) | 1: launch_one<false, 4, 2>(n_frames, P, nt, st); break;
+    case (4 << 2) | 3: launch_one<true, 4, 2>(n_frames, P, nt, st); break;
+    case (2 << 2) | 0: launch_one<false, 2, 1>(n_frames, P, nt, st); break;
+    case (2 << 2) | 2: launch_one<true, 2, 1>(n_frames, P, nt, st); break;
+    case (2 << 2) | 1: launch_one<false, 2, 2>(n_frames, P, nt, st); break;
+    case (2 << 2) | 3: launch_one<true, 2, 2>(n_frames, P, nt, st); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

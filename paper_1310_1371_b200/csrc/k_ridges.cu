@@ -2,8 +2,8 @@
 // curvature and directed-ridge test, with deterministic compaction into 32x32 bins.
 //
 // Rows A1-A4 of DESIGN.md §2 ("Directed ridge detection"; SI steps 1-2,
-// PAPER.md:919-931).  One CTA per 32x32 output tile; everything stays on chip:
-//   I (tile + 3 + K_s halo, replicate border, int32)
+// PAPER.md:919-931).  Per 32x32 output tile, everything stays on chip:
+//   I (tile + 3 + K_s halo, replicate border) staged by TMA into shared memory
 //   -> R = q (x) I along x                    (int32, exact)
 //   -> G = q (x) R along y                    (fp64, exact integers < 2^53)
 //   -> horizontal Sobel passes d2, s5, d1     (fp64, exact)
@@ -13,6 +13,14 @@
 // direction recipe is order-sensitive and it is written with explicit _rn intrinsics.
 // Every stencil pass is register-blocked: a thread produces a strip of 8 outputs from a
 // sliding window held in registers (one shared-memory load per input, not per tap).
+// The TMA kernel is persistent: while a tile is computed, the TMA engine already fetches
+// the next tile's input into the other buffer (mbarrier double buffering).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdlib>
+
 #include "rd_internal.cuh"
 
 namespace rd {
@@ -21,52 +29,69 @@ namespace {
 constexpr int GRS = T1 + 6;     // G region side (tile + 3)
 constexpr int KRS = T1 + 2;     // kappa region side (tile + 1)
 constexpr int SB = 8;           // strip length of the register-blocked passes
-}  // namespace
 
+struct K1Smem {
+  int irs, ip, bh, co;          // region side, row pitch (elements), TMA box rows, region column offset
+  size_t off_bar, off_in0, off_in1, off_x, off_g, off_k, off_d, off_cnt, total;
+};
+
+__host__ __device__ inline size_t al128(size_t v) { return (v + 127) & ~size_t(127); }
+
+__host__ __device__ inline K1Smem k1_layout(int KS, int pb) {
+  K1Smem L;
+  L.irs = T1 + 6 + 2 * KS;
+  const int vec = 16 / pb;                       // TMA box rows are multiples of 16 bytes
+  // The TMA box must start on a 16-byte boundary in x (measured on B200: other starts trap
+  // with an illegal instruction), so the box starts `co` elements left of the region; tile
+  // origins are multiples of 32 >= 16/pb, hence co is the same for every tile.
+  L.co = ((-(3 + KS)) % vec + vec) % vec;
+  L.ip = (L.co + L.irs + vec - 1) / vec * vec;
+  L.bh = (L.irs + 15) / 16 * 16;                 // TMA box rows (multiple of 16)
+  const size_t in_bytes = (size_t)L.bh * L.ip * pb + SB * 4;    // + strip over-read pad
+  const size_t x_dbl = (size_t)L.irs * GRS > (size_t)3 * GRS * KRS ? (size_t)L.irs * GRS : (size_t)3 * GRS * KRS;
+  size_t o = 0;
+  L.off_bar = o;  o = al128(o + 16);
+  L.off_in0 = o;  o = al128(o + in_bytes);
+  L.off_in1 = o;  o = al128(o + in_bytes);
+  L.off_x = o;    o = al128(o + 8 * x_dbl);            // R, later HA|HB|HC
+  L.off_g = o;    o = al128(o + 8 * (size_t)GRS * GRS);
+  L.off_k = o;    o = al128(o + 8 * (size_t)KRS * KRS);
+  L.off_d = o;    o = al128(o + 16 * (size_t)T1 * T1);
+  L.off_cnt = o;  o = al128(o + 4 * 33);
+  L.total = o;
+  return L;
+}
+
+// Steps 2-6 for one tile whose input region (origin x0-3-KS, y0-3-KS, replicate border
+// already applied) is in sIn with row pitch L.ip.
 template <typename PixT, int KS>
-__global__ void __launch_bounds__(K1_THREADS, 2)
-k_ridges(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, Params P) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  constexpr int IRS = T1 + 6 + 2 * KS;  // input region side
+__device__ __forceinline__ void ridge_tile(const PixT* __restrict__ sIn, unsigned char* smem, const K1Smem& L,
+                                           int x0, int y0, int f, int bx, int by, const Params& P) {
   constexpr int NTAP = 2 * KS + 1;
-  constexpr int RSTR = (GRS + SB - 1) / SB;   // row-pass strips per row
-  double* sR = reinterpret_cast<double*>(smem);              // [IRS][GRS]
-  double* sG = sR + IRS * GRS;                                // [GRS][GRS]
-  double* sHA = sG + GRS * GRS;                               // [GRS][KRS]
+  constexpr int IRS = T1 + 6 + 2 * KS;
+  constexpr int RSTR = (GRS + SB - 1) / SB;
+  const int IP = L.ip;
+  double* sR = reinterpret_cast<double*>(smem + L.off_x);   // [IRS][GRS]
+  double* sHA = sR;                                         // [GRS][KRS] x3 (after R is consumed)
   double* sHB = sHA + GRS * KRS;
   double* sHC = sHB + GRS * KRS;
-  double* sK = sHC + GRS * KRS;                               // [KRS][KRS]
-  double2* sD = reinterpret_cast<double2*>(sK + KRS * KRS);   // [T1][T1]
-  int* sI = reinterpret_cast<int*>(sD + T1 * T1);             // [IRS][IRS + SB] (padded for strips)
-  int* sCnt = sI + IRS * (IRS + SB);                          // [33]
-  constexpr int IP = IRS + SB;                                // sI row pitch
-
+  double* sG = reinterpret_cast<double*>(smem + L.off_g);   // [GRS][GRS]
+  double* sK = reinterpret_cast<double*>(smem + L.off_k);   // [KRS][KRS]
+  double2* sD = reinterpret_cast<double2*>(smem + L.off_d); // [T1][T1]
+  int* sCnt = reinterpret_cast<int*>(smem + L.off_cnt);     // [33]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int f = blockIdx.z;
-  const int x0 = blockIdx.x * T1, y0 = blockIdx.y * T1;
   const int W = P.W, H = P.H;
-  const uint8_t* frame = frames + (int64_t)f * fstride;
   int q[NTAP];
 #pragma unroll
   for (int j = 0; j < NTAP; ++j) q[j] = P.q[j];
 
-  // 1. input region with replicate border (warp per row, lanes along the row)
-  {
-    const int ox = x0 - 3 - KS, oy = y0 - 3 - KS;
-    for (int r = warp; r < IRS; r += K1_THREADS / 32) {
-      const int gy = min(max(oy + r, 0), H - 1);
-      const PixT* row = reinterpret_cast<const PixT*>(frame + (int64_t)gy * pitch);
-      for (int c = lane; c < IRS; c += 32) sI[r * IP + c] = (int)__ldg(row + min(max(ox + c, 0), W - 1));
-    }
-  }
-  __syncthreads();
   // 2. row pass (int32 exact: max_value * sum q < 2^31 checked at rd_create)
   for (int it = tid; it < IRS * RSTR; it += K1_THREADS) {
     const int r = it / RSTR, c0 = (it - r * RSTR) * SB;
-    const int* src = sI + r * IP + c0;
+    const PixT* src = sIn + r * IP + c0;
     int v[SB + NTAP - 1];
 #pragma unroll
-    for (int j = 0; j < SB + NTAP - 1; ++j) v[j] = src[j];
+    for (int j = 0; j < SB + NTAP - 1; ++j) v[j] = (int)src[j];
 #pragma unroll
     for (int o = 0; o < SB; ++o) {
       int acc = 0;
@@ -180,7 +205,7 @@ k_ridges(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, Par
   }
   __syncthreads();
   const int total = sCnt[32];
-  const int bin = blockIdx.y * P.nbx + blockIdx.x;
+  const int bin = by * P.nbx + bx;
   const int64_t base = ((int64_t)f * P.nbx * P.nby + bin) * P.ridge_cap;
   const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
@@ -200,20 +225,138 @@ k_ridges(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, Par
     if (total) atomicAdd(&P.stats[f].ridges, (unsigned long long)total);
   }
 }
+}  // namespace
 
-size_t k_ridges_smem(int Ks) {
-  const int IRS = T1 + 6 + 2 * Ks;
-  size_t dbl = (size_t)IRS * GRS + GRS * GRS + 3 * GRS * KRS + KRS * KRS + 2 * T1 * T1;
-  return dbl * 8 + (size_t)IRS * (IRS + SB) * 4 + 33 * 4;
+// One CTA per tile; input staged with plain loads (any pitch / alignment).
+template <typename PixT, int KS>
+__global__ void __launch_bounds__(K1_THREADS, 2)
+k_ridges(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, Params P) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const K1Smem L = k1_layout(KS, (int)sizeof(PixT));
+  constexpr int IRS = T1 + 6 + 2 * KS;
+  PixT* sIn = reinterpret_cast<PixT*>(smem + L.off_in0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int f = blockIdx.z;
+  const int x0 = blockIdx.x * T1, y0 = blockIdx.y * T1;
+  const int W = P.W, H = P.H;
+  const uint8_t* frame = frames + (int64_t)f * fstride;
+  const int ox = x0 - 3 - KS, oy = y0 - 3 - KS;
+  for (int r = warp; r < IRS; r += K1_THREADS / 32) {  // warp per row, replicate border
+    const int gy = min(max(oy + r, 0), H - 1);
+    const PixT* row = reinterpret_cast<const PixT*>(frame + (int64_t)gy * pitch);
+    for (int c = lane; c < IRS; c += 32) sIn[r * L.ip + c] = __ldg(row + min(max(ox + c, 0), W - 1));
+  }
+  __syncthreads();
+  ridge_tile<PixT, KS>(sIn, smem, L, x0, y0, f, blockIdx.x, blockIdx.y, P);
 }
+
+// Persistent CTAs; the input region of the next tile is fetched by TMA (zero fill out of
+// the frame, then patched to replicate the border) while the current tile is computed.
+template <typename PixT, int KS>
+__global__ void __launch_bounds__(K1_THREADS, 2)
+k_ridges_tma(const __grid_constant__ CUtensorMap tmap, int n_frames, Params P) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const K1Smem L = k1_layout(KS, (int)sizeof(PixT));
+  constexpr int IRS = T1 + 6 + 2 * KS;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.off_bar);
+  PixT* buf[2] = {reinterpret_cast<PixT*>(smem + L.off_in0), reinterpret_cast<PixT*>(smem + L.off_in1)};
+  const uint32_t box_bytes = (uint32_t)(L.bh * L.ip * sizeof(PixT));
+  const int tid = threadIdx.x;
+  const int W = P.W, H = P.H;
+  const int tiles_per_frame = P.nbx * P.nby;
+  const int ntiles = tiles_per_frame * n_frames;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  auto issue = [&](int t, int b) {
+    const int f = t / tiles_per_frame, rem = t - f * tiles_per_frame;
+    const int by = rem / P.nbx, bx = rem - by * P.nbx;
+    fence_proxy_async_smem();
+    mbar_expect_tx(&bar[b], box_bytes);
+    tma_load_3d(buf[b], &tmap, &bar[b], bx * T1 - 3 - KS - L.co, by * T1 - 3 - KS, f);
+  };
+  int t = blockIdx.x;
+  if (tid == 0 && t < ntiles) issue(t, 0);
+  uint32_t phase[2] = {0u, 0u};
+  for (int k = 0; t < ntiles; ++k, t += gridDim.x) {
+    const int b = k & 1;
+    if (tid == 0 && t + (int)gridDim.x < ntiles) issue(t + gridDim.x, b ^ 1);
+    mbar_wait(&bar[b], phase[b]);
+    phase[b] ^= 1u;
+    const int f = t / tiles_per_frame, rem = t - f * tiles_per_frame;
+    const int by = rem / P.nbx, bx = rem - by * P.nbx;
+    const int x0 = bx * T1, y0 = by * T1;
+    const int ox = x0 - 3 - KS, oy = y0 - 3 - KS;
+    PixT* sIn = buf[b] + L.co;   // region origin inside the 16-byte aligned box
+    if (ox < 0 || oy < 0 || ox + IRS > W || oy + IRS > H) {  // replicate-border patch
+      for (int i = tid; i < IRS * IRS; i += K1_THREADS) {
+        const int r = i / IRS, c = i - r * IRS;
+        const int sy = min(max(oy + r, 0), H - 1) - oy, sx = min(max(ox + c, 0), W - 1) - ox;
+        if (sy != r || sx != c) sIn[r * L.ip + c] = sIn[sy * L.ip + sx];
+      }
+      __syncthreads();
+    }
+    ridge_tile<PixT, KS>(sIn, smem, L, x0, y0, f, bx, by, P);
+    __syncthreads();   // all reads of buf[b] done before it is refilled
+  }
+}
+
+size_t k_ridges_smem(int Ks) { return k1_layout(Ks, 2).total; }
+
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+bool make_tmap(CUtensorMap* map, const void* frames, int pb, int W, int H, int n, int64_t pitch, int64_t fstride,
+               int box_w, int box_h) {
+  if (!g_encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return false;
+    g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  if (((uintptr_t)frames & 15) || (pitch & 15) || (fstride & 15) || box_w > 256 || box_h > 256) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)n};
+  cuuint64_t strides[2] = {(cuuint64_t)pitch, (cuuint64_t)(n > 1 ? fstride : pitch * H)};
+  cuuint32_t box[3] = {(cuuint32_t)box_w, (cuuint32_t)box_h, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = g_encode(map, pb == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 3,
+                        const_cast<void*>(frames), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int g_num_sms = 0;
+}  // namespace
 
 template <typename PixT, int KS>
 static cudaError_t launch_t(const void* frames, int64_t pitch, int64_t fstride, int n_frames, const Params& P,
                             cudaStream_t st) {
+  const K1Smem L = k1_layout(KS, (int)sizeof(PixT));
+  CUtensorMap map;
+  static const bool no_tma = getenv("RD_NO_TMA") != nullptr;   // diagnostic switch
+  if (!no_tma && make_tmap(&map, frames, (int)sizeof(PixT), P.W, P.H, n_frames, pitch, fstride, L.ip, L.bh)) {
+    if (!g_num_sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    cudaFuncSetAttribute(k_ridges_tma<PixT, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ridges_tma<PixT, KS>, K1_THREADS, L.total);
+    const int ntiles = P.nbx * P.nby * n_frames;
+    const int grid = std::min(ntiles, std::max(1, per_sm) * g_num_sms);
+    k_ridges_tma<PixT, KS><<<grid, K1_THREADS, L.total, st>>>(map, n_frames, P);
+    return cudaGetLastError();
+  }
   dim3 grid(P.nbx, P.nby, n_frames);
-  size_t sm = k_ridges_smem(KS);
-  cudaFuncSetAttribute(k_ridges<PixT, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_ridges<PixT, KS><<<grid, K1_THREADS, sm, st>>>((const uint8_t*)frames, pitch, fstride, P);
+  cudaFuncSetAttribute(k_ridges<PixT, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+  k_ridges<PixT, KS><<<grid, K1_THREADS, L.total, st>>>((const uint8_t*)frames, pitch, fstride, P);
   return cudaGetLastError();
 }
 

@@ -4,6 +4,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "rd.h"
@@ -15,9 +17,8 @@ cudaError_t launch_ridges(const void* frames, int64_t pitch, int64_t fstride, in
                           cudaStream_t st);
 cudaError_t launch_eigen(const double* abc, int64_t n, double* out, int* deg, cudaStream_t st);
 size_t k_hough_smem(const Params& P, int G);
-int k_hough_group(const Params& P, size_t smem_limit);
 int k_hough_max_entries();
-cudaError_t launch_hough(int n_frames, const Params& P, bool wide, int G, cudaStream_t st);
+cudaError_t launch_hough(int n_frames, const Params& P, bool wide, int G, int nt, int minb, cudaStream_t st);
 size_t k_fit_smem(const Params& P);
 cudaError_t launch_fit(int n_frames, const Params& P, void* rings, int* counts, cudaStream_t st);
 }  // namespace rd
@@ -42,7 +43,7 @@ struct rd_detector {
   int max_batch;
   Params P;
   bool wide;
-  int G;
+  int G, k2_threads, k2_minb;   // Hough kernel launch shape (levels per step, threads, CTAs/SM)
   // device allocations
   void* d_tables = nullptr;
   void* d_bins_count = nullptr;
@@ -214,23 +215,43 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   P.nbx = (c.width + T1 - 1) / T1;
   P.nby = (c.height + T1 - 1) / T1;
   P.ridge_cap = c.max_ridges_per_tile;
-  P.ntx = (c.width + T2 - 1) / T2;
-  P.nty = (c.height + T2 - 1) / T2;
   P.entry_cap = c.max_entries_per_tile;
   P.hot_cap = c.max_hotspots_per_level;
   P.ring_cap = c.max_rings_per_frame;
   P.debug = c.debug;
   P.dbg_cap = c.debug ? (1 << 20) : 0;
 
-  // shared-memory feasibility
+  // Hough launch shape (tile side T, levels per step G, threads, CTAs per SM): the first of
+  // the candidates whose shared memory fits; RD_K2_SHAPE="T,G,threads,ctas" puts a shape first
   cudaDeviceProp prop;
   e = cudaGetDeviceProperties(&prop, device);
   if (e != cudaSuccess) { delete det; return cuda_fail(e, "cudaGetDeviceProperties"); }
-  size_t smax = prop.sharedMemPerBlockOptin;
-  det->G = k_hough_group(P, smax);
+  const size_t smax = prop.sharedMemPerBlockOptin, sm_sm = prop.sharedMemPerMultiprocessor;
+  struct Shape { int T, G, nt, minb; };
+  std::vector<Shape> shapes = {{64, 8, 512, 1}, {64, 4, 512, 1}, {48, 4, 384, 2}, {64, 2, 512, 1}, {32, 2, 256, 1}};
+  if (const char* env = getenv("RD_K2_SHAPE")) {
+    Shape s{};
+    if (sscanf(env, "%d,%d,%d,%d", &s.T, &s.G, &s.nt, &s.minb) == 4 && s.T >= 16 && s.T <= 128 &&
+        (s.G == 2 || s.G == 4 || s.G == 8) && s.nt >= 64 && s.nt <= 512 && (s.nt % 32) == 0 && s.minb >= 1)
+      shapes.insert(shapes.begin(), s);
+  }
+  det->G = 0;
+  for (const Shape& s : shapes) {
+    P.k2t = s.T;
+    const size_t need = k_hough_smem(P, s.G);
+    const size_t limit = s.minb == 1 ? smax : std::min(smax, sm_sm / s.minb - 1024);
+    if (need <= limit) {
+      det->G = s.G;
+      det->k2_threads = s.nt;
+      det->k2_minb = s.minb;
+      break;
+    }
+  }
+  P.ntx = (c.width + P.k2t - 1) / P.k2t;
+  P.nty = (c.height + P.k2t - 1) / P.k2t;
   if (k_ridges_smem(P.Ks) > smax || det->G == 0 || k_fit_smem(P) > smax) {
     delete det;
-    snprintf(g_err, sizeof g_err, "shared memory: K1 %zu K2(G=2) %zu K3 %zu > %zu", k_ridges_smem(P.Ks),
+    snprintf(g_err, sizeof g_err, "shared memory: K1 %zu K2 %zu K3 %zu > %zu", k_ridges_smem(P.Ks),
              k_hough_smem(P, 2), k_fit_smem(P), smax);
     return RD_ERR_CONFIG;
   }
@@ -334,7 +355,7 @@ static rd_status detect_impl(rd_detector* det, const void* d_frames, int64_t pit
   if (ev) CK(cudaEventRecord(ev[0], st));
   CK(launch_ridges(d_frames, pitch, fstride, n, P, st));
   if (ev) CK(cudaEventRecord(ev[1], st));
-  CK(launch_hough(n, P, det->wide, det->G, st));
+  CK(launch_hough(n, P, det->wide, det->G, det->k2_threads, det->k2_minb, st));
   if (ev) CK(cudaEventRecord(ev[2], st));
   CK(launch_fit(n, P, d_rings, d_counts, st));
   if (ev) CK(cudaEventRecord(ev[3], st));

@@ -7,7 +7,6 @@
 namespace rd {
 
 constexpr int T1 = 32;          // K1 (ridge) tile: 32x32 output pixels; also the ridge-bin size
-constexpr int T2 = 64;          // K2 (Hough) tile: 64x64 accumulator cells (2x2 ridge bins)
 constexpr int KS_MAX = 15;      // smoothing half-width limit (sigma_s <= 5)
 constexpr int K1_THREADS = 256;
 constexpr int K2_THREADS = 256;
@@ -54,7 +53,8 @@ struct Params {
   uint32_t* bin_xy;             // [F][bins][ridge_cap] x | y<<16
   double2* bin_d;               // [F][bins][ridge_cap] (dx, dy)
   // Hough tiles (K2)
-  int ntx, nty;                 // 64x64 tiles per frame
+  int k2t;                      // Hough tile side (T x T accumulator cells per CTA)
+  int ntx, nty;                 // Hough tiles per frame
   int entry_cap, hot_cap;
   int ring_cap;
   Peak* peaks;                  // [F][ring_cap]
@@ -94,5 +94,40 @@ __device__ __forceinline__ bool direction_of(double b, double e, double s, doubl
 
 // round half away from zero of an exactly computed double (llround semantics)
 __device__ __forceinline__ int round_half_away(double v) { return (int)llround(v); }
+
+// ---------------------------------------------------------------- TMA / mbarrier (sm_90+)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// 3-D tiled TMA load of box (x, y, z) of the tensor map into shared memory; completes on `bar`
+__device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, uint64_t* bar, int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
+      ::"r"(smem_u32(dst)), "l"(tmap), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
 
 }  // namespace rd

@@ -1,4 +1,6 @@
-"""Per-phase cycle breakdown of the Hough kernel and per-kernel event times on cfg3."""
+"""Per-phase cycle breakdown of the Hough kernel and per-kernel event times.
+
+usage: phase_probe.py [cfg] [batch]   (env: RD_K2_SHAPE=T,G,threads,ctas  PROBE_ENTRY_CAP=n  PROBE_HOT_CAP=n)"""
 import os
 import sys
 
@@ -12,25 +14,30 @@ import synth  # noqa: E402
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 B = int(sys.argv[2]) if len(sys.argv) > 2 else 128
 params = synth.preset(cfg)
+if os.environ.get("PROBE_ENTRY_CAP"):
+    params["max_entries_per_tile"] = int(os.environ["PROBE_ENTRY_CAP"])
+if os.environ.get("PROBE_HOT_CAP"):
+    params["max_hotspots_per_level"] = int(os.environ["PROBE_HOT_CAP"])
 frames = torch.from_numpy(synth.batch(cfg, 0, 0, B)).cuda()
 det = rd.Detector(params, max_batch=B)
 for _ in range(2):
-    det.detect(frames)
-det.sync()
+    rings, counts = det.detect(frames)
+st = det.sync(raise_on_overflow=False)
+ovf = det.overflow(B)
 det.set_timing(True)
 for _ in range(3):
     det.detect(frames)
-det.sync()
+det.sync(raise_on_overflow=False)
 ms, n = det.kernel_times()
-print("kernel us/frame:", [round(1000 * m / n / B, 2) for m in ms])
+print("shape", os.environ.get("RD_K2_SHAPE", "default"), "overflow frames", int((ovf != 0).sum()),
+      "kernel us/frame:", [round(1000 * m / n / B, 2) for m in ms])
 det.set_timing(False)
 phase_cycles(det, True)
 det.detect(frames)
-det.sync()
+det.sync(raise_on_overflow=False)
 c = phase_cycles(det, False)
 names = ["rays", "setup0", "votes", "S", "cand+undo", "nms+setup"]
 ncta = int(c[15])
 tot = sum(int(x) for x in c[:6])
-print("CTAs", ncta, "cycles/CTA", tot / max(ncta, 1))
-for i, nm in enumerate(names):
-    print(f"  {nm:10s} {int(c[i]) / max(ncta, 1):10.0f} cyc/CTA  {100 * int(c[i]) / max(tot, 1):5.1f}%")
+print("  CTAs", ncta, "cycles/CTA", round(tot / max(ncta, 1)), " ".join(
+    f"{nm}={int(c[i]) / max(ncta, 1):.0f}" for i, nm in enumerate(names)))
