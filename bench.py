@@ -225,53 +225,64 @@ def run_gpu(args):
         dt = float(t.item())
     e2e_value = world * B * e2e_steps / dt
 
-    # ---------------- gather ring lists to rank 0 over NCCL (after timing)
+    # ---------------- gather ring lists to rank 0 over NCCL (after timing; PAPER.md:698-705)
     gather_ms = None
     n_rings_total = int(counts.clamp(min=0).sum().item())
     if world > 1:
+        from paper_1310_1371_b200.distributed import gather_rings
         torch.cuda.synchronize(dev)
         g0 = time.perf_counter()
-        cnt_all = [torch.empty_like(counts) for _ in range(world)]
-        dist.all_gather(cnt_all, counts)
-        ring_all = [torch.empty_like(rings) for _ in range(world)]
-        dist.all_gather(ring_all, rings)
+        res = gather_rings(rings, counts)
         torch.cuda.synchronize(dev)
         gather_ms = (time.perf_counter() - g0) * 1e3
-        n_rings_total = int(sum(int(c.clamp(min=0).sum().item()) for c in cnt_all))
+        if res is not None:
+            n_rings_total = int(res[1].clamp(min=0).sum().item())
 
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return 0
 
-    # ---------------- roofline of the dominant kernel (DESIGN.md §5)
-    names = ["k_ridges", "k_hough", "k_fit"]
-    dom = int(np.argmax(kms))
+    # ---------------- roofline of the dominant kernel (DESIGN.md §6)
+    names = ["k_ridges", "k_rays", "k_hough", "k_fit"]
+    kms_all = [k / ncalls for k in kms]
+    kms_step = [kms_all[0], kms_all[2], kms_all[3]]      # K1, K2, K3 (K1.5 reported separately)
+    dom = int(np.argmax(kms_step))
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
-    fp64_peak = 148 * 64 * sm_max * 1e6 / 1e12          # DFMA issue slots / s (T op/s)
+    # K1: fp64 pipe (exact stencil arithmetic); peak = 148 SM x 64 DFMA/clk x sm_max
     Ks = math.ceil(3 * params["smoothing_sigma"])
-    k1_ops_per_px = (2 * Ks + 1) + 9 + 9 + 10          # column pass + Sobel-x + Sobel-y + kappa
+    k1_ops_per_px = (2 * Ks + 1) + 9 + 9 + 10
     px = params["width"] * params["height"]
-    k1_launch_ms = kms[0] / ncalls
-    k1_achieved = B * px * k1_ops_per_px / (k1_launch_ms / 1e3) / 1e12
+    fp64_peak = 148 * 64 * sm_max * 1e6 / 1e12
+    k1_ach = B * px * k1_ops_per_px / (kms_step[0] / 1e3) / 1e12
+    # K2: one shared-memory atomic per in-frame vote is the irreducible work of an
+    # accumulator Hough transform; peak = measured ATOMS throughput 11.0/clk/SM
+    # (tools/microbench, profiles/microbench_r01.log) x 148 SM x sm_max
+    atom_peak = 11.0 * 148 * sm_max * 1e6 / 1e9
+    k2_ach = votes_per_step / (kms_step[1] / 1e3) / 1e9
+    summ = {}
+    sp = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
+    if os.path.exists(sp):
+        for d in json.load(open(sp)):
+            for n in names:
+                if n in d.get("kernel", "") and "dram_bytes_per_frame" in d:
+                    summ[n] = d["dram_bytes_per_frame"] * B
+    roofs = [
+        {"kernel": "k_ridges", "bound": "alu", "achieved": round(k1_ach, 3), "peak": round(fp64_peak, 3),
+         "unit": "TFLOP/s", "frac": round(k1_ach / fp64_peak, 4), "traffic": summ.get("k_ridges"),
+         "peak_note": "fp64 DFMA issue: 148 SM x 64/clk x sm_max (guide unit counts); ops = fp64 instructions of "
+                      "the exact separable Gaussian + Sobel + kappa per pixel (DESIGN.md §6)"},
+        {"kernel": "k_hough", "bound": "alu", "achieved": round(k2_ach, 3), "peak": round(atom_peak, 1),
+         "unit": "Gvote/s", "frac": round(k2_ach / atom_peak, 5), "traffic": summ.get("k_hough"),
+         "peak_note": "shared-memory atomic issue: measured 11.0 ATOMS/clk/SM x 148 SM x sm_max; one atomic per "
+                      "in-frame vote (DESIGN.md §6)"},
+    ]
+    roof = dict(roofs[0] if dom == 0 else roofs[1])
     hbm_peak = float(peaks.get("hbm_gbs", 6549.1))
     alg_bytes_frame = fbytes + 64 * (n_rings_total / max(1, B * world))
     hbm_achieved = alg_bytes_frame * value / world / 1e9
-    trafic = None
-    tr_path = os.path.join(ROOT, "profiles", "traffic_r01.json")
-    if os.path.exists(tr_path):
-        try:
-            trafic = json.load(open(tr_path)).get("k_ridges_bytes_per_launch_per_frame")
-            trafic = trafic * B if trafic else None
-        except Exception:
-            trafic = None
-    roof = {"kernel": names[dom] if dom == 0 else "k_ridges", "bound": "alu", "achieved": round(k1_achieved, 3),
-            "peak": round(fp64_peak, 3), "unit": "TFLOP/s",
-            "peak_note": "fp64 DFMA issue rate 148 SM x 64/clk x sm_max (guide unit counts); ops = fp64 "
-                         "instructions of the exact separable stencil + kappa (DESIGN.md §5)",
-            "frac": round(k1_achieved / fp64_peak, 4), "traffic": trafic}
 
     cpu = None
     if world == 1 and not args.no_cpu:
@@ -287,8 +298,9 @@ def run_gpu(args):
                        "frame": "1024x688 uint16", "parallelism": f"frame-sharded x{world}",
                        "l2": "inputs larger than L2 (360 MB/step/GPU)"},
             "votes_per_s": round(votes_per_step * world / ms_per_step * 1e3, 1),
-            "kernel_ms_per_step": {n: round(k / ncalls, 4) for n, k in zip(names, kms)},
+            "kernel_ms_per_step": {n: round(k, 4) for n, k in zip(names, kms_all)},
             "roofline": roof,
+            "rooflines": roofs,
             "hbm_roofline": {"achieved": round(hbm_achieved, 2), "peak": hbm_peak, "unit": "GB/s",
                              "frac": round(hbm_achieved / hbm_peak, 5),
                              "note": "algorithmic bytes = frame read + 64 B/ring written (SURVEY §8(d))"},
@@ -297,7 +309,7 @@ def run_gpu(args):
                     "h2d_bytes_per_step": B * fbytes * world,
                     "d2h_bytes_per_step": (B * det.ring_cap * 64 + 4 * B) * world,
                     "api": "Detector.detect_host -> rd_detect_host (pinned host buffers)"},
-            "gpu_launches": 3 * args.steps,
+            "gpu_launches": 4 * args.steps,
             "clocks": clocks}
     if gather_ms is not None:
         line["gather_ms"] = round(gather_ms, 3)

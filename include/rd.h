@@ -137,10 +137,10 @@ rd_status rd_dump_ridges(rd_detector* det, int32_t frame, rd_ridge* h_out, int64
 rd_status rd_dump_hotspots(rd_detector* det, int32_t frame, rd_hotspot* h_out, int64_t cap, int64_t* n);
 
 /* Per-kernel timing with CUDA events recorded on the launching stream around each
- * of the detector's kernels (K1 ridges, K2 Hough, K3 fit).  rd_set_timing(det, 1)
- * clears and enables accumulation; rd_kernel_times waits for the recorded events and
- * writes total milliseconds per kernel into h_ms[0..2] and the number of timed
- * rd_detect calls into *n_calls.  Disabled by default (no events recorded). */
+ * of the detector's kernels (K1 ridges, K1.5 ray routing, K2 Hough, K3 fit).
+ * rd_set_timing(det, 1) clears and enables accumulation; rd_kernel_times waits for the
+ * recorded events and writes total milliseconds per kernel into h_ms[0..3] and the
+ * number of timed rd_detect calls into *n_calls.  Disabled by default (no events). */
 rd_status rd_set_timing(rd_detector* det, int32_t on);
 rd_status rd_kernel_times(rd_detector* det, float* h_ms, int32_t* n_calls);
 

@@ -61,13 +61,6 @@ __host__ __device__ inline K2Smem k2_layout(int G, int T, int hal, int entry_cap
   return L;
 }
 
-// a r >= b restricted to [lo, hi]
-__device__ __forceinline__ void half_ge(float a, float b, float& lo, float& hi) {
-  if (a > 0.f) lo = fmaxf(lo, __fdividef(b, a));
-  else if (a < 0.f) hi = fminf(hi, __fdividef(b, a));
-  else if (b > 0.f) hi = -1e30f;
-}
-
 template <int G>
 __device__ __forceinline__ int warp_prefix_lookup(const int (&pg)[G], int t, int& base) {
   int g = 0;
@@ -119,7 +112,6 @@ __global__ void __launch_bounds__(512, MINB) k_hough(Params P) {
   int* s_ecnt = hcnt + P.n_levels + G;
   int* s_flags = s_ecnt + 1;
   int* s_nact = s_ecnt + 2;                                              // [2], by step parity
-  int* s_bin = s_ecnt + 4;                                               // work-stealing bin counter
 
   const int NT = blockDim.x, NW = NT >> 5;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -132,7 +124,7 @@ __global__ void __launch_bounds__(512, MINB) k_hough(Params P) {
   const int rawp = L.rawp;
   const int lvl_cells = L.raws * rawp;       // uint16 cells per raw level
   const int hot_cap = P.hot_cap, nlev = P.n_levels;
-  const int rhi = P.r_hi, rlo = P.r_lo;
+  const int rlo = P.r_lo;
 
   // optional per-phase cycle accounting (thread 0, after each barrier; rd_phase_cycles)
   unsigned long long t_acc[6] = {0, 0, 0, 0, 0, 0};
@@ -158,60 +150,21 @@ __global__ void __launch_bounds__(512, MINB) k_hough(Params P) {
   }
   __syncthreads();
 
-  // ---------------- phase 0: voting rays that can reach the tile's level boxes
+  // ---------------- phase 0: this tile's voting rays, routed by K1.5 (k_rays.cu)
+  const int64_t tl = (int64_t)f * P.ntx * P.nty + tile;
+  const int ne = min(P.ray_count[tl], P.entry_cap);
   {
-    const int bx0 = max(X0 - hal, 0), bx1 = min(X0 + T - 1 + hal, W - 1);
-    const int by0 = max(Y0 - hal, 0), by1 = min(Y0 + T - 1 + hal, H - 1);
-    const int nbx = P.nbx;
-    const int cbx0 = max((bx0 - rhi) / T1, 0), cbx1 = min((bx1 + rhi) / T1, P.nbx - 1);
-    const int cby0 = max((by0 - rhi) / T1, 0), cby1 = min((by1 + rhi) / T1, P.nby - 1);
-    const int nbw = cbx1 - cbx0 + 1, nbins = nbw * (cby1 - cby0 + 1);
-    const int64_t fbins = (int64_t)f * P.nbx * P.nby;
-    const float m = P.k_slope, c = P.k_icpt;
-    for (;;) {  // warps take ridge bins dynamically; lanes over (ridge, sense)
-      int b = 0;
-      if (lane == 0) b = atomicAdd(s_bin, 1);
-      b = __shfl_sync(0xffffffffu, b, 0);
-      if (b >= nbins) break;
-      const int by = cby0 + b / nbw, bx = cbx0 + b % nbw;
-      const int64_t bin = fbins + by * nbx + bx;
-      const int cnt = P.bin_count[bin];
-      for (int j = lane; j < 2 * cnt; j += 32) {
-        const int64_t g = bin * P.ridge_cap + (j >> 1);
-        const uint32_t xy = P.bin_xy[g];
-        const double2 d = P.bin_d[g];
-        const double sgn = (j & 1) ? -1.0 : 1.0;
-        const int x = (int)(xy & 0xFFFFu), y = (int)(xy >> 16);
-        const double u = sgn * d.x, v = sgn * d.y;
-        // necessary conditions for a vote in the level-r box (K_r <= m r + c), linear in r;
-        // conservative by +-1 level, exactness restored per vote
-        const float fu = (float)u, fv = (float)v, fx = (float)x, fy = (float)y;
-        float lo = (float)rlo, hi = (float)rhi;
-        half_ge(fu + m, (float)X0 - 1.5f - c - fx, lo, hi);
-        half_ge(m - fu, fx - (float)(X0 + T) - 0.5f - c, lo, hi);
-        half_ge(fu, -0.5f - fx, lo, hi);
-        half_ge(-fu, fx - (float)W + 0.5f, lo, hi);
-        half_ge(fv + m, (float)Y0 - 1.5f - c - fy, lo, hi);
-        half_ge(m - fv, fy - (float)(Y0 + T) - 0.5f - c, lo, hi);
-        half_ge(fv, -0.5f - fy, lo, hi);
-        half_ge(-fv, fy - (float)H + 0.5f, lo, hi);
-        if (hi < lo - 2.f) continue;
-        const int ra = max((int)floorf(lo) - 1, rlo), rb = min((int)ceilf(hi) + 1, rhi);
-        if (ra > rb) continue;
-        const int e = atomicAdd(s_ecnt, 1);
-        if (e < P.entry_cap) {
-          eD[e] = make_double2(u, v);
-          eXY[e] = xy;
-          eR[e] = (uint32_t)(ra - rlo) | ((uint32_t)(rb - rlo) << 16);
-        } else {
-          atomicOr(s_flags, OVF_ENTRIES);
-        }
-      }
+    const double2* gd = P.ray_d + tl * P.entry_cap;
+    const uint32_t* gxy = P.ray_xy + tl * P.entry_cap;
+    const uint32_t* gr = P.ray_r + tl * P.entry_cap;
+    for (int e = tid; e < ne; e += NT) {
+      eD[e] = gd[e];
+      eXY[e] = gxy[e];
+      eR[e] = gr[e];
     }
   }
   __syncthreads();
   PMARK(0);
-  const int ne = min(*s_ecnt, P.entry_cap);
   int my_votes = 0, my_hot = 0;
   const uint32_t T_raw = (uint32_t)P.T_raw;
 

@@ -21,6 +21,8 @@ int k_hough_max_entries();
 cudaError_t launch_hough(int n_frames, const Params& P, bool wide, int G, int nt, int minb, cudaStream_t st);
 size_t k_fit_smem(const Params& P);
 cudaError_t launch_fit(int n_frames, const Params& P, void* rings, int* counts, cudaStream_t st);
+cudaError_t launch_rays(int n_frames, const Params& P, cudaStream_t st);
+constexpr int RD_NEV = 5;   // timing events per rd_detect: K1 | K1.5 | K2 | K3
 }  // namespace rd
 
 using namespace rd;
@@ -50,6 +52,9 @@ struct rd_detector {
   void* d_bins_xy = nullptr;
   void* d_bins_d = nullptr;
   void* d_peaks = nullptr;
+  void* d_ray_d = nullptr;     // K1.5 -> K2 ray lists per Hough tile
+  void* d_ray_xy = nullptr;
+  void* d_ray_r = nullptr;
   void* d_counters = nullptr;  // stats | peak_count | flags | dbg_count
   size_t counters_bytes = 0;
   void* d_dbg = nullptr;
@@ -268,7 +273,11 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   ALLOC(det->d_bins_xy, sizeof(uint32_t) * B * nbins * P.ridge_cap);
   ALLOC(det->d_bins_d, sizeof(double2) * B * nbins * P.ridge_cap);
   ALLOC(det->d_peaks, sizeof(Peak) * B * P.ring_cap);
-  det->counters_bytes = sizeof(Stats) * B + sizeof(int) * 3 * B;
+  const int64_t ntl = (int64_t)P.ntx * P.nty;
+  ALLOC(det->d_ray_d, sizeof(double2) * B * ntl * P.entry_cap);
+  ALLOC(det->d_ray_xy, sizeof(uint32_t) * B * ntl * P.entry_cap);
+  ALLOC(det->d_ray_r, sizeof(uint32_t) * B * ntl * P.entry_cap);
+  det->counters_bytes = sizeof(Stats) * B + sizeof(int) * 3 * B + sizeof(int) * B * ntl;
   ALLOC(det->d_counters, det->counters_bytes);
   if (c.debug) ALLOC(det->d_dbg, sizeof(HotRec) * B * P.dbg_cap);
   // tables
@@ -297,6 +306,10 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   P.peak_count = (int*)((char*)det->d_counters + sizeof(Stats) * B);
   P.flags = P.peak_count + B;
   P.dbg_count = P.flags + B;
+  P.ray_count = P.dbg_count + B;
+  P.ray_d = (double2*)det->d_ray_d;
+  P.ray_xy = (uint32_t*)det->d_ray_xy;
+  P.ray_r = (uint32_t*)det->d_ray_r;
   P.dbg_hot = (HotRec*)det->d_dbg;
   det->P = P;
   e = cudaEventCreateWithFlags(&det->ev_last, cudaEventDisableTiming);
@@ -313,6 +326,9 @@ rd_status rd_destroy(rd_detector* det) {
   cudaFree(det->d_bins_xy);
   cudaFree(det->d_bins_d);
   cudaFree(det->d_peaks);
+  cudaFree(det->d_ray_d);
+  cudaFree(det->d_ray_xy);
+  cudaFree(det->d_ray_r);
   cudaFree(det->d_counters);
   cudaFree(det->d_dbg);
   cudaFree(det->d_prof);
@@ -342,23 +358,25 @@ static rd_status detect_impl(rd_detector* det, const void* d_frames, int64_t pit
   const Params& P = det->P;
   cudaEvent_t* ev = nullptr;
   if (det->timing) {
-    size_t need = 4 * (size_t)(det->n_timed + 1);
+    size_t need = RD_NEV * (size_t)(det->n_timed + 1);
     while (det->tev.size() < need) {
       cudaEvent_t e;
       CK(cudaEventCreate(&e));
       det->tev.push_back(e);
     }
-    ev = &det->tev[4 * (size_t)det->n_timed];
+    ev = &det->tev[RD_NEV * (size_t)det->n_timed];
     det->n_timed++;
   }
   CK(cudaMemsetAsync(det->d_counters, 0, det->counters_bytes, st));
   if (ev) CK(cudaEventRecord(ev[0], st));
   CK(launch_ridges(d_frames, pitch, fstride, n, P, st));
   if (ev) CK(cudaEventRecord(ev[1], st));
-  CK(launch_hough(n, P, det->wide, det->G, det->k2_threads, det->k2_minb, st));
+  CK(launch_rays(n, P, st));
   if (ev) CK(cudaEventRecord(ev[2], st));
-  CK(launch_fit(n, P, d_rings, d_counts, st));
+  CK(launch_hough(n, P, det->wide, det->G, det->k2_threads, det->k2_minb, st));
   if (ev) CK(cudaEventRecord(ev[3], st));
+  CK(launch_fit(n, P, d_rings, d_counts, st));
+  if (ev) CK(cudaEventRecord(ev[4], st));
   CK(cudaEventRecord(det->ev_last, st));
   det->have_last = true;
   det->last_n = n;
@@ -535,17 +553,17 @@ rd_status rd_set_timing(rd_detector* det, int32_t on) {
 rd_status rd_kernel_times(rd_detector* det, float* h_ms, int32_t* n_calls) {
   if (!det || !h_ms || !n_calls) return RD_ERR_PARAM;
   CK(cudaSetDevice(det->device));
-  float acc[3] = {0, 0, 0};
+  float acc[RD_NEV - 1] = {0, 0, 0, 0};
   for (int c = 0; c < det->n_timed; ++c) {
-    cudaEvent_t* ev = &det->tev[4 * (size_t)c];
-    CK(cudaEventSynchronize(ev[3]));
-    for (int k = 0; k < 3; ++k) {
+    cudaEvent_t* ev = &det->tev[RD_NEV * (size_t)c];
+    CK(cudaEventSynchronize(ev[RD_NEV - 1]));
+    for (int k = 0; k < RD_NEV - 1; ++k) {
       float ms = 0;
       CK(cudaEventElapsedTime(&ms, ev[k], ev[k + 1]));
       acc[k] += ms;
     }
   }
-  for (int k = 0; k < 3; ++k) h_ms[k] = acc[k];
+  for (int k = 0; k < RD_NEV - 1; ++k) h_ms[k] = acc[k];
   *n_calls = det->n_timed;
   return RD_OK;
 }

@@ -56,6 +56,10 @@ struct Params {
   int k2t;                      // Hough tile side (T x T accumulator cells per CTA)
   int ntx, nty;                 // Hough tiles per frame
   int entry_cap, hot_cap;
+  int* ray_count;               // [F][tiles] voting rays routed to each Hough tile (K1.5)
+  double2* ray_d;               // [F][tiles][entry_cap] (s*dx, s*dy)
+  uint32_t* ray_xy;             // [F][tiles][entry_cap] x | y<<16
+  uint32_t* ray_r;              // [F][tiles][entry_cap] ra | rb<<16 (level indices)
   int ring_cap;
   Peak* peaks;                  // [F][ring_cap]
   int* peak_count;              // [F]

@@ -131,11 +131,11 @@ class Detector:
         check(lib().rd_set_timing(self._h, 1 if on else 0), "rd_set_timing")
 
     def kernel_times(self):
-        """(ms per kernel [K1 ridges, K2 hough, K3 fit] summed over timed calls, n_calls)."""
-        ms = (C.c_float * 3)()
+        """(ms per kernel [K1 ridges, K1.5 rays, K2 hough, K3 fit] summed over timed calls, n_calls)."""
+        ms = (C.c_float * 4)()
         n = C.c_int32()
         check(lib().rd_kernel_times(self._h, ms, C.byref(n)), "rd_kernel_times")
-        return [ms[0], ms[1], ms[2]], n.value
+        return [ms[0], ms[1], ms[2], ms[3]], n.value
 
     @staticmethod
     def rings_to_numpy(rings: torch.Tensor, counts: torch.Tensor) -> list[np.ndarray]:
