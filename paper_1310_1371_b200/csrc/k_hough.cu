@@ -24,7 +24,10 @@
 namespace rd {
 
 namespace {
-constexpr int BATCH = 4;          // (ray, level) pairs in flight per thread
+#ifndef RD_K2_BATCH
+#define RD_K2_BATCH 4
+#endif
+constexpr int BATCH = RD_K2_BATCH;   // (ray, level) pairs in flight per thread
 
 struct K2Smem {
   int raws, rawp;                 // raw side and row pitch (uint16 units)
