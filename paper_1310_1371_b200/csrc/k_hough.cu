@@ -31,8 +31,8 @@ constexpr int BATCH = RD_K2_BATCH;   // (ray, level) pairs in flight per thread
 
 struct K2Smem {
   int raws, rawp;                 // raw side and row pitch (uint16 units)
-  size_t off_hS, off_ed, off_raw, off_exy, off_err, off_act, off_hcell, off_hraw, off_cand, off_hcnt, off_ccnt,
-      off_w, off_k, off_tn, off_box, total;
+  size_t off_hS, off_ed, off_raw, off_exy, off_err, off_act, off_hcell, off_hraw, off_task, off_ccur, off_cdef,
+      off_hcnt, off_w, off_k, off_tn, off_box, total;
 };
 
 __host__ __device__ inline size_t align16(size_t v) { return (v + 15) & ~size_t(15); }
@@ -53,9 +53,10 @@ __host__ __device__ inline K2Smem k2_layout(int G, int T, int hal, int entry_cap
   L.off_act = o;   o = align16(o + 2 * (size_t)entry_cap);
   L.off_hcell = o; o = align16(o + 2 * (size_t)NSLOT * hot_cap);
   L.off_hraw = o;  o = align16(o + 2 * (size_t)NSLOT * hot_cap);
-  L.off_cand = o;  o = align16(o + 2 * (size_t)NSLOT * hot_cap);
+  L.off_task = o;  o = align16(o + 2 * (size_t)G * hot_cap);         // step's hotspots (g << 12 | h)
+  L.off_ccur = o;  o = align16(o + 2 * (size_t)G * hot_cap);         // step's candidates below Lhi
+  L.off_cdef = o;  o = align16(o + 2 * (size_t)2 * hot_cap);         // candidates of Lhi, by parity
   L.off_hcnt = o;  o = align16(o + 4 * (size_t)(n_levels + G + 16));
-  L.off_ccnt = o;  o = align16(o + 4 * (size_t)(n_levels + G));
   L.off_w = o;     o = align16(o + 4 * (size_t)n_levels * wstride);   // level tables, resident
   L.off_k = o;     o = align16(o + 4 * (size_t)n_levels);
   L.off_tn = o;    o = align16(o + 8 * (size_t)n_levels);
@@ -64,27 +65,6 @@ __host__ __device__ inline K2Smem k2_layout(int G, int T, int hal, int entry_cap
   return L;
 }
 
-template <int G>
-__device__ __forceinline__ int warp_prefix_lookup(const int (&pg)[G], int t, int& base) {
-  int g = 0;
-  base = 0;
-#pragma unroll
-  for (int q = 0; q < G - 1; ++q)
-    if (t >= pg[q]) { g = q + 1; base = pg[q]; }
-  return g;
-}
-
-// inclusive prefix over lanes 0..G-1 of `v`, broadcast to every lane as pg[0..G-1]
-template <int G>
-__device__ __forceinline__ void warp_prefix(int v, int lane, int (&pg)[G]) {
-#pragma unroll
-  for (int o = 1; o < G; o <<= 1) {
-    const int n = __shfl_up_sync(0xffffffffu, v, o);
-    if (lane >= o) v += n;
-  }
-#pragma unroll
-  for (int q = 0; q < G; ++q) pg[q] = __shfl_sync(0xffffffffu, v, q);
-}
 }  // namespace
 
 template <bool kWide, int G, int MINB>
@@ -105,9 +85,10 @@ __global__ void __launch_bounds__(512, MINB) k_hough(Params P) {
   uint16_t* act = reinterpret_cast<uint16_t*>(smem + L.off_act);         // active entries of the step
   uint16_t* hcell = reinterpret_cast<uint16_t*>(smem + L.off_hcell);     // [NSLOT][hot_cap] ring-local cell
   uint16_t* hraw = reinterpret_cast<uint16_t*>(smem + L.off_hraw);       // [NSLOT][hot_cap]
-  uint16_t* cand = reinterpret_cast<uint16_t*>(smem + L.off_cand);       // [NSLOT][hot_cap] candidate hotspots
+  uint16_t* tasks = reinterpret_cast<uint16_t*>(smem + L.off_task);     // [G*hot_cap] step hotspots
+  uint16_t* ccur = reinterpret_cast<uint16_t*>(smem + L.off_ccur);       // [G*hot_cap] step candidates
+  uint16_t* cdef = reinterpret_cast<uint16_t*>(smem + L.off_cdef);       // [2][hot_cap] deferred candidates
   int* hcnt = reinterpret_cast<int*>(smem + L.off_hcnt);                 // [n_levels + G] + misc
-  int* ccnt = reinterpret_cast<int*>(smem + L.off_ccnt);                 // [n_levels + G]
   int* tW = reinterpret_cast<int*>(smem + L.off_w);                      // [n_levels][wstride] w_r(d)
   int* tK = reinterpret_cast<int*>(smem + L.off_k);                      // [n_levels] K_r
   double* tTn = reinterpret_cast<double*>(smem + L.off_tn);              // [n_levels] T_norm(r)
@@ -115,6 +96,9 @@ __global__ void __launch_bounds__(512, MINB) k_hough(Params P) {
   int* s_ecnt = hcnt + P.n_levels + G;
   int* s_flags = s_ecnt + 1;
   int* s_nact = s_ecnt + 2;                                              // [2], by step parity
+  int* s_ntask = s_ecnt + 4;                                             // [2], by step parity
+  int* s_ndef = s_ecnt + 6;                                              // [2], by step parity
+  int* s_ncur = s_ecnt + 8;                                              // [1]
 
   const int NT = blockDim.x, NW = NT >> 5;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -139,7 +123,6 @@ __global__ void __launch_bounds__(512, MINB) k_hough(Params P) {
     t_last = t_;                                      \
   }
   for (int i = tid; i < nlev + G + 16; i += NT) hcnt[i] = 0;
-  for (int i = tid; i < nlev + G; i += NT) ccnt[i] = 0;
   for (int i = tid; i < nlev * P.wstride; i += NT) tW[i] = P.lvlW[i];
   for (int i = tid; i < nlev; i += NT) {
     tK[i] = P.lvlK[i];
@@ -217,6 +200,10 @@ __global__ void __launch_bounds__(512, MINB) k_hough(Params P) {
     const int Lhi = min(L0 + G - 1, nlev - 1);
     const int par = (L0 >> LG) & 1;
     const int npair = s_nact[par] << LG;   // (active ray, level) pairs, ray-major
+    if (tid == 0) {   // counters first written in (c0) of this step (last read a barrier ago)
+      s_ncur[0] = 0;
+      s_ndef[par] = 0;
+    }
     // (a) votes of levels L0..Lhi
     for (int p0 = tid; p0 < npair; p0 += BATCH * NT) {
       int cell[BATCH], txs[BATCH], tys[BATCH];
@@ -237,10 +224,14 @@ __global__ void __launch_bounds__(512, MINB) k_hough(Params P) {
         if (oc == T_raw) {
           const int ix = tx - (X0 - 1), iy = ty - (Y0 - 1);
           if ((unsigned)ix < (unsigned)RING && (unsigned)iy < (unsigned)RING) {
-            const int li = L0 + ((p0 + k * NT) & (G - 1));
+            const int g = (p0 + k * NT) & (G - 1), li = L0 + g;
             const int h = atomicAdd(&hcnt[li], 1);
-            if (h < hot_cap) hcell[(li % NSLOT) * hot_cap + h] = (uint16_t)(iy * RING + ix);
-            else atomicOr(s_flags, OVF_HOTSPOTS);
+            if (h < hot_cap) {
+              hcell[(li % NSLOT) * hot_cap + h] = (uint16_t)(iy * RING + ix);
+              tasks[atomicAdd(&s_ntask[par], 1)] = (uint16_t)((g << 12) | h);
+            } else {
+              atomicOr(s_flags, OVF_HOTSPOTS);
+            }
           }
         }
         my_votes += ((unsigned)(tx - X0) < (unsigned)T) & ((unsigned)(ty - Y0) < (unsigned)T);
@@ -249,84 +240,74 @@ __global__ void __launch_bounds__(512, MINB) k_hough(Params P) {
     if (tid == 0) s_nact[par ^ 1] = 0;   // counter of the next step (last read a barrier ago)
     __syncthreads();
     PMARK(2);
+    const int ntask = s_ntask[par];
     // (b) S = sum_i w(i) sum_j w(j) raw(y+i, x+j) at each hotspot:
-    //     a sub-warp of SUB >= 2K+1 lanes per hotspot, lanes over window rows, shuffle sum;
-    //     the hotspots of all G levels are processed concurrently
-    {
-      int pg[G];
-      warp_prefix<G>(lane < G && L0 + lane < nlev ? min(hcnt[L0 + lane], hot_cap) : 0, lane, pg);
-      const int Rmx = 2 * tK[Lhi] + 1;   // K_r is non-decreasing in r
-      const int SUB = Rmx <= 4 ? 4 : Rmx <= 8 ? 8 : Rmx <= 16 ? 16 : 32;
-      const int per = 32 / SUB, sub = lane / SUB, sl_ = lane - sub * SUB;
-      const int total = pg[G - 1];
-      for (int tb = warp * per; tb < total; tb += NW * per) {
-        const int t = tb + sub;
-        int base;
-        const int g = warp_prefix_lookup<G>(pg, t, base);
-        const int li = min(L0 + g, nlev - 1), h = t - base;
-        const int K = tK[li], R = 2 * K + 1;
-        const int sl = li % NSLOT;
-        const int* w = tW + li * P.wstride;
-        const uint16_t* lvl = raw16 + g * lvl_cells;
-        unsigned long long acc = 0;
-        int ly = 0, lx = 0;
-        if (t < total) {
-          const int c16 = hcell[sl * hot_cap + h];
-          const int iy = c16 / RING, ix = c16 - iy * RING;
-          ly = iy - 1 + hal;
-          lx = ix - 1 + hal;
-          for (int row = sl_; row < R; row += SUB) {
-            const uint16_t* rowp = lvl + (ly + row - K) * rawp + lx;
-            if (kWide) {
-              unsigned long long rs = (unsigned long long)w[0] * rowp[0];
-              for (int j = 1; j <= K; ++j) rs += (unsigned long long)w[j] * (uint32_t)(rowp[-j] + rowp[j]);
-              acc += rs * (unsigned long long)w[abs(row - K)];
-            } else {
-              uint32_t rs = (uint32_t)w[0] * rowp[0];
+    //     one warp per hotspot, lanes over window rows; integer sums, reduced in-warp
+    for (int t = warp; t < ntask; t += NW) {
+      const int tk = tasks[t], g = tk >> 12, h = tk & 0xFFF;
+      const int li = L0 + g, sl = li % NSLOT;
+      const int K = tK[li], R = 2 * K + 1;
+      const int* w = tW + li * P.wstride;
+      const uint16_t* lvl = raw16 + g * lvl_cells;
+      const int c16 = hcell[sl * hot_cap + h];
+      const int iy = c16 / RING, ix = c16 - iy * RING;
+      const int ly = iy - 1 + hal, lx = ix - 1 + hal;   // raw-local coordinates of the hotspot
+      unsigned long long acc = 0;
+      for (int row = lane; row < R; row += 32) {
+        const uint16_t* rowp = lvl + (ly + row - K) * rawp + lx;
+        if (kWide) {
+          unsigned long long rs = (unsigned long long)w[0] * rowp[0];
+          for (int j = 1; j <= K; ++j) rs += (unsigned long long)w[j] * (uint32_t)(rowp[-j] + rowp[j]);
+          acc += rs * (unsigned long long)w[abs(row - K)];
+        } else {
+          uint32_t rs = (uint32_t)w[0] * rowp[0];
 #pragma unroll 4
-              for (int j = 1; j <= K; ++j) rs += (uint32_t)w[j] * (uint32_t)(rowp[-j] + rowp[j]);
-              acc += (unsigned long long)rs * (unsigned long long)w[abs(row - K)];
-            }
-          }
+          for (int j = 1; j <= K; ++j) rs += (uint32_t)w[j] * (uint32_t)(rowp[-j] + rowp[j]);
+          acc += (unsigned long long)rs * (unsigned long long)w[abs(row - K)];
         }
-        for (int o = SUB >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (t < total && sl_ == 0) {
-          hS[sl * hot_cap + h] = acc;
-          hraw[sl * hot_cap + h] = lvl[ly * rawp + lx];
-        }
+      }
+      unsigned long long S;
+      if (kWide) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        S = acc;
+      } else {   // every lane term < 2^45: split in 24-bit halves, two single-instruction reductions
+        const unsigned lo = __reduce_add_sync(0xffffffffu, (unsigned)(acc & 0xFFFFFFull));
+        const unsigned hi = __reduce_add_sync(0xffffffffu, (unsigned)(acc >> 24));
+        S = ((unsigned long long)hi << 24) + lo;
+      }
+      if (lane == 0) {
+        hS[sl * hot_cap + h] = S;
+        hraw[sl * hot_cap + h] = lvl[ly * rawp + lx];
       }
     }
     __syncthreads();
     PMARK(3);
     // (c0) hotspot bookkeeping: interior count, debug records, candidates S > T_norm(r)
-    //       for r in [r_min, r_max]
-    {
-      int pg[G];
-      warp_prefix<G>(lane < G && L0 + lane < nlev ? min(hcnt[L0 + lane], hot_cap) : 0, lane, pg);
-      for (int p = tid; p < pg[G - 1]; p += NT) {
-        int base;
-        const int g = warp_prefix_lookup<G>(pg, p, base);
-        const int li = L0 + g, sl = li % NSLOT, h = p - base;
-        const int c16 = hcell[sl * hot_cap + h];
-        const int iy = c16 / RING, ix = c16 - iy * RING;
-        if (ix < 1 || ix > T || iy < 1 || iy > T) continue;     // interior cells only
-        ++my_hot;
-        const unsigned long long S = hS[sl * hot_cap + h];
-        if (P.debug) {
-          int kd = atomicAdd(&P.dbg_count[f], 1);
-          if (kd < P.dbg_cap) {
-            HotRec rec;
-            rec.r = rlo + li; rec.y = Y0 - 1 + iy; rec.x = X0 - 1 + ix; rec.raw = hraw[sl * hot_cap + h];
-            rec.S = (long long)S;
-            P.dbg_hot[(int64_t)f * P.dbg_cap + kd] = rec;
-          } else {
-            atomicOr(&P.flags[f], OVF_DEBUG);
-          }
+    //       for r in [r_min, r_max]; candidates of the top level
+    //      of the step wait for the next step (its upper neighbour level is not done yet)
+    for (int t = tid; t < ntask; t += NT) {
+      const int tk = tasks[t], g = tk >> 12, h = tk & 0xFFF;
+      const int li = L0 + g, sl = li % NSLOT;
+      const int c16 = hcell[sl * hot_cap + h];
+      const int iy = c16 / RING, ix = c16 - iy * RING;
+      if (ix < 1 || ix > T || iy < 1 || iy > T) continue;     // interior cells only
+      ++my_hot;
+      const unsigned long long S = hS[sl * hot_cap + h];
+      if (P.debug) {
+        int kd = atomicAdd(&P.dbg_count[f], 1);
+        if (kd < P.dbg_cap) {
+          HotRec rec;
+          rec.r = rlo + li; rec.y = Y0 - 1 + iy; rec.x = X0 - 1 + ix; rec.raw = hraw[sl * hot_cap + h];
+          rec.S = (long long)S;
+          P.dbg_hot[(int64_t)f * P.dbg_cap + kd] = rec;
+        } else {
+          atomicOr(&P.flags[f], OVF_DEBUG);
         }
-        if (li >= 1 && li <= nlev - 2 && (double)(long long)S > tTn[li]) {
-          const int k = atomicAdd(&ccnt[li], 1);
-          cand[sl * hot_cap + k] = (uint16_t)h;   // k < hot_cap: candidates are hotspots
-        }
+      }
+      if (li >= 1 && li <= nlev - 2 && (double)(long long)S > tTn[li]) {
+        if (li == Lhi) cdef[par * hot_cap + atomicAdd(&s_ndef[par], 1)] = (uint16_t)h;
+        else ccur[atomicAdd(&s_ncur[0], 1)] = (uint16_t)tk;
       }
     }
     // (c1) undo: restore the counters touched in this step to zero
@@ -343,17 +324,21 @@ __global__ void __launch_bounds__(512, MINB) k_hough(Params P) {
     }
     __syncthreads();
     PMARK(4);
-    // (d) peaks of levels lc in [L0-1, Lhi-1]: 3x3x3 maxima of N = S/r (R14), one warp per
-    //     candidate; meanwhile the next step's setup (reads only static ray data)
+    // (d) peaks among the candidates of levels L0-1 (deferred) .. Lhi-1: 3x3x3 maxima of
+    //     N = S/r (R14), one warp per candidate; meanwhile the next step's setup
     {
-      const int lc0 = max(L0 - 1, 1), lc1 = min(Lhi - 1, nlev - 2);
-      int pg[G];
-      warp_prefix<G>(lane < G && lc0 + lane <= lc1 ? ccnt[lc0 + lane] : 0, lane, pg);
-      for (int p = warp; p < pg[G - 1]; p += NW) {
-        int base;
-        const int q = warp_prefix_lookup<G>(pg, p, base);
-        const int lc = lc0 + q, sc = lc % NSLOT;
-        const int h = cand[sc * hot_cap + (p - base)];
+      const int nd = L0 > 0 ? s_ndef[par ^ 1] : 0, nc = s_ncur[0];
+      for (int p = warp; p < nd + nc; p += NW) {
+        int lc, h;
+        if (p < nd) {
+          lc = L0 - 1;
+          h = cdef[(par ^ 1) * hot_cap + p];
+        } else {
+          const int tk = ccur[p - nd];
+          lc = L0 + (tk >> 12);
+          h = tk & 0xFFF;
+        }
+        const int sc = lc % NSLOT;
         const int c16 = hcell[sc * hot_cap + h];
         const int iy = c16 / RING, ix = c16 - iy * RING;
         const long long S = (long long)hS[sc * hot_cap + h];
@@ -389,6 +374,7 @@ __global__ void __launch_bounds__(512, MINB) k_hough(Params P) {
       }
     }
     if (L0 + G < nlev) setup(L0 + G);
+    if (tid == 0) s_ntask[par ^ 1] = 0;   // hotspot-task counter of the next step
     __syncthreads();
     PMARK(5);
   }

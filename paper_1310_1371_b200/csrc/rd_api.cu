@@ -146,7 +146,7 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   if (!c.max_entries_per_tile) c.max_entries_per_tile = 2048;
   if (!c.max_hotspots_per_level) c.max_hotspots_per_level = 256;
   if (c.max_ridges_per_tile > T1 * T1) c.max_ridges_per_tile = T1 * T1;
-  if (c.max_hotspots_per_level > 65535) return RD_ERR_PARAM;
+  if (c.max_hotspots_per_level > 4095) return RD_ERR_PARAM;   // 12-bit hotspot index in K2 task lists
   if (c.max_entries_per_tile > k_hough_max_entries()) c.max_entries_per_tile = k_hough_max_entries();
 
   // ---- host tables (DESIGN.md §2 A1, A5, A7, A8, A9)
