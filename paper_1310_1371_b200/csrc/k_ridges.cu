@@ -32,7 +32,7 @@ constexpr int SB = 8;           // strip length of the register-blocked passes
 
 struct K1Smem {
   int irs, ip, bh, co;          // region side, row pitch (elements), TMA box rows, region column offset
-  size_t off_bar, off_in0, off_in1, off_x, off_g, off_k, off_d, off_cnt, total;
+  size_t off_bar, off_in0, off_in1, off_x, off_g, off_k, off_d, off_s, off_list, off_cnt, total;
 };
 
 __host__ __device__ inline size_t al128(size_t v) { return (v + 127) & ~size_t(127); }
@@ -57,6 +57,8 @@ __host__ __device__ inline K1Smem k1_layout(int KS, int pb) {
   L.off_g = o;    o = al128(o + 8 * (size_t)GRS * GRS);
   L.off_k = o;    o = al128(o + 8 * (size_t)KRS * KRS);
   L.off_d = o;    o = al128(o + 16 * (size_t)T1 * T1);
+  L.off_s = o;    o = al128(o + 8 * (size_t)T1 * T1);   // s of candidates, -1 otherwise
+  L.off_list = o; o = al128(o + 2 * (size_t)T1 * T1);   // candidate pixel list
   L.off_cnt = o;  o = al128(o + 4 * 33);
   L.total = o;
   return L;
@@ -77,7 +79,9 @@ __device__ __forceinline__ void ridge_tile(const PixT* __restrict__ sIn, unsigne
   double* sHC = sHB + GRS * KRS;
   double* sG = reinterpret_cast<double*>(smem + L.off_g);   // [GRS][GRS]
   double* sK = reinterpret_cast<double*>(smem + L.off_k);   // [KRS][KRS]
-  double2* sD = reinterpret_cast<double2*>(smem + L.off_d); // [T1][T1]
+  double2* sD = reinterpret_cast<double2*>(smem + L.off_d); // [T1][T1] (e, Ixy), then rho
+  double* sS = reinterpret_cast<double*>(smem + L.off_s);   // [T1][T1] s if candidate, else -1
+  uint16_t* sList = reinterpret_cast<uint16_t*>(smem + L.off_list);
   int* sCnt = reinterpret_cast<int*>(smem + L.off_cnt);     // [33]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int W = P.W, H = P.H;
@@ -132,13 +136,15 @@ __device__ __forceinline__ void ridge_tile(const PixT* __restrict__ sIn, unsigne
     }
   }
   __syncthreads();
-  // 5. vertical passes -> Ixx = s5_y (x) d2_x, Iyy = d2_y (x) s5_x, Ixy = d1_y (x) d1_x; kappa
+  // 5. vertical passes -> Ixx = s5_y (x) d2_x, Iyy = d2_y (x) s5_x, Ixy = d1_y (x) d1_x; kappa.
+  //    Tile pixels with kappa < t keep (e, b, s) for step 5b; the others get s = -1.
+  constexpr int SB5 = 6;   // 34 columns x 6 strips = 204 work items <= 256 threads
   const double t_int = P.t_int;
-  for (int it = tid; it < KRS * ((KRS + SB - 1) / SB); it += K1_THREADS) {
-    const int c = it % KRS, r0 = (it / KRS) * SB;
-    double a[SB + 4], b[SB + 4], d[SB + 4];
+  for (int it = tid; it < KRS * ((KRS + SB5 - 1) / SB5); it += K1_THREADS) {
+    const int c = it % KRS, r0 = (it / KRS) * SB5;
+    double a[SB5 + 4], b[SB5 + 4], d[SB5 + 4];
 #pragma unroll
-    for (int j = 0; j < SB + 4; ++j) {
+    for (int j = 0; j < SB5 + 4; ++j) {
       const bool ok = r0 + j < GRS;
       a[j] = ok ? sHA[(r0 + j) * KRS + c] : 0.0;
       b[j] = ok ? sHB[(r0 + j) * KRS + c] : 0.0;
@@ -146,25 +152,61 @@ __device__ __forceinline__ void ridge_tile(const PixT* __restrict__ sIn, unsigne
     }
     const int x = x0 - 1 + c;
 #pragma unroll
-    for (int o = 0; o < SB; ++o) {
+    for (int o = 0; o < SB5; ++o) {
       const int r = r0 + o;
       if (r >= KRS) break;
       const int y = y0 - 1 + r;
-      double kap = HUGE_VAL;
-      double2 dir = make_double2(2.0, 2.0);  // 2.0 = "not a candidate"
+      const bool in_tile = r >= 1 && r <= T1 && c >= 1 && c <= T1;
+      double kap = HUGE_VAL, s = -1.0, e = 0.0, Ixy = 0.0;
       if (x >= 2 && x <= W - 3 && y >= 2 && y <= H - 3) {
         const double Ixx = (a[o] + a[o + 4]) + 4.0 * (a[o + 1] + a[o + 3]) + 6.0 * a[o + 2];
         const double Iyy = (b[o] + b[o + 4]) - 2.0 * b[o + 2];
-        const double Ixy = (d[o + 4] - d[o]) + 2.0 * (d[o + 3] - d[o + 1]);
-        double s, e;
+        Ixy = (d[o + 4] - d[o]) + 2.0 * (d[o + 3] - d[o + 1]);
         kap = kappa_of(Ixx, Ixy, Iyy, &s, &e);
-        if (r >= 1 && r <= T1 && c >= 1 && c <= T1 && kap < t_int) {
-          double dx, dy;
-          if (direction_of(Ixy, e, s, &dx, &dy)) dir = make_double2(dx, dy);
-        }
+        if (!(kap < t_int)) s = -1.0;
       }
       sK[r * KRS + c] = kap;
-      if (r >= 1 && r <= T1 && c >= 1 && c <= T1) sD[(r - 1) * T1 + (c - 1)] = dir;
+      if (in_tile) {
+        const int k = (r - 1) * T1 + (c - 1);
+        sS[k] = s;
+        sD[k] = make_double2(e, Ixy);
+      }
+    }
+  }
+  __syncthreads();
+  // 5b. directions rho of the candidate pixels (kappa < t), dealt evenly to all threads
+  {
+    unsigned cb[T1 * T1 / K1_THREADS];
+#pragma unroll
+    for (int it = 0; it < T1 * T1 / K1_THREADS; ++it) {
+      cb[it] = __ballot_sync(0xffffffffu, sS[tid + it * K1_THREADS] >= 0.0);
+      if (lane == 0) sCnt[it * (K1_THREADS / 32) + warp] = __popc(cb[it]);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      int v = sCnt[lane], incl = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int n = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += n;
+      }
+      sCnt[lane] = incl - v;
+      if (lane == 31) sCnt[32] = incl;
+    }
+    __syncthreads();
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int it = 0; it < T1 * T1 / K1_THREADS; ++it)
+      if ((cb[it] >> lane) & 1u)
+        sList[sCnt[it * (K1_THREADS / 32) + warp] + __popc(cb[it] & lt)] = (uint16_t)(tid + it * K1_THREADS);
+    const int ncand = sCnt[32];
+    __syncthreads();
+    for (int i = tid; i < ncand; i += K1_THREADS) {
+      const int k = sList[i];
+      const double2 eb = sD[k];
+      double dx, dy;
+      if (direction_of(eb.y, eb.x, sS[k], &dx, &dy)) sD[k] = make_double2(dx, dy);
+      else sS[k] = -1.0;   // isotropic: never a ridge (R3)
     }
   }
   __syncthreads();
@@ -177,8 +219,9 @@ __device__ __forceinline__ void ridge_tile(const PixT* __restrict__ sIn, unsigne
     int ty = k / T1, tx = k - ty * T1;
     int x = x0 + tx, y = y0 + ty;
     bool ok = false;
+    const bool cand = sS[k] >= 0.0;
     double2 dir = sD[k];
-    if (x >= 3 && x <= W - 4 && y >= 3 && y <= H - 4 && dir.x != 2.0) {
+    if (x >= 3 && x <= W - 4 && y >= 3 && y <= H - 4 && cand) {
       double kp = sK[(ty + 1) * KRS + tx + 1];
       int ox = (int)llround(dir.x), oy = (int)llround(dir.y);
       bool after_plus = (oy > 0) || (oy == 0 && ox > 0);
