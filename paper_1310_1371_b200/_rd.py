@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librd.so")
+LIB_PATH = os.environ.get("RD_LIB_PATH") or os.path.join(_HERE, "librd.so")   # override: tuning builds
 
 RD_OK, RD_ERR_PARAM, RD_ERR_DIM, RD_ERR_CONFIG, RD_ERR_CAPACITY, RD_ERR_CUDA, RD_ERR_STATE = range(7)
 RD_U8, RD_U16 = 0, 1

@@ -30,7 +30,7 @@ namespace {
 constexpr int BATCH = RD_K2_BATCH;   // (ray, level) pairs in flight per thread
 
 struct K2Smem {
-  int raws, rawp;                 // raw side and row pitch (uint16 units)
+  int raws, rawp, lvlc;           // raw side, row pitch, cells per level (multiple of 8; uint16 units)
   size_t off_hS, off_ed, off_raw, off_exy, off_err, off_act, off_hcell, off_hraw, off_task, off_ccur, off_cdef,
       off_hcnt, off_w, off_k, off_tn, off_box, total;
 };
@@ -47,7 +47,8 @@ __host__ __device__ inline K2Smem k2_layout(int G, int T, int hal, int entry_cap
   size_t o = 0;
   L.off_hS = o;    o = align16(o + sizeof(unsigned long long) * NSLOT * hot_cap);
   L.off_ed = o;    o = align16(o + sizeof(double2) * entry_cap);
-  L.off_raw = o;   o = align16(o + 2 * (size_t)G * L.raws * L.rawp);
+  L.lvlc = (L.raws * L.rawp + 7) & ~7;   // 16-byte aligned level buffers (bulk clears)
+  L.off_raw = o;   o = align16(o + 2 * (size_t)G * L.lvlc);
   L.off_exy = o;   o = align16(o + 4 * (size_t)entry_cap);
   L.off_err = o;   o = align16(o + 4 * (size_t)entry_cap);
   L.off_act = o;   o = align16(o + 2 * (size_t)entry_cap);
@@ -109,7 +110,7 @@ __global__ void __launch_bounds__(512, MINB) k_hough(Params P) {
   const int W = P.W, H = P.H, hal = P.hal;
   const int RX0 = X0 - hal, RY0 = Y0 - hal;   // raw buffer origin
   const int rawp = L.rawp;
-  const int lvl_cells = L.raws * rawp;       // uint16 cells per raw level
+  const int lvl_cells = L.lvlc;              // uint16 cells per raw level (16-byte multiple)
   const int hot_cap = P.hot_cap, nlev = P.n_levels;
   const int rlo = P.r_lo;
 
@@ -215,7 +216,11 @@ __global__ void __launch_bounds__(512, MINB) k_hough(Params P) {
       }
 #pragma unroll
       for (int k = 0; k < BATCH; ++k)
+#ifdef RD_K2_EXPERIMENT_NORET   // timing experiment only: wrong hotspot registration
+        if (cell[k] >= 0) { atomicAdd(&raw32[cell[k] >> 1], 1u << ((cell[k] & 1) << 4)); old[k] = 0; }
+#else
         if (cell[k] >= 0) old[k] = atomicAdd(&raw32[cell[k] >> 1], 1u << ((cell[k] & 1) << 4));
+#endif
 #pragma unroll
       for (int k = 0; k < BATCH; ++k) {
         if (cell[k] < 0) continue;
@@ -310,17 +315,17 @@ __global__ void __launch_bounds__(512, MINB) k_hough(Params P) {
         else ccur[atomicAdd(&s_ncur[0], 1)] = (uint16_t)tk;
       }
     }
-    // (c1) undo: restore the counters touched in this step to zero
-    for (int p0 = tid; p0 < npair; p0 += BATCH * NT) {
-      int cell[BATCH], tx, ty;
-#pragma unroll
-      for (int k = 0; k < BATCH; ++k) {
-        const int p = p0 + k * NT;
-        cell[k] = p < npair ? target(act[p >> LG], p & (G - 1), L0, tx, ty) : -1;
-      }
-#pragma unroll
-      for (int k = 0; k < BATCH; ++k)
-        if (cell[k] >= 0) raw16[cell[k]] = 0;
+    // (c1) restore the step's counters to zero.  The paper undoes the registered cells
+    //     (PAPER.md:426-434); here the rows of each level box are cleared with 16-byte
+    //     stores, which costs far fewer instructions than re-walking the votes.
+#pragma unroll 1
+    for (int g = 0; g < G; ++g) {
+      if (L0 + g >= nlev) break;
+      const int4 bb = box[g];
+      const int s8 = (g * lvl_cells + (bb.z - RY0) * rawp) >> 3;               // align down
+      const int e8 = (g * lvl_cells + (bb.w - RY0 + 1) * rawp + 7) >> 3;       // align up
+      uint4* r4 = reinterpret_cast<uint4*>(raw16);
+      for (int i = s8 + tid; i < e8; i += NT) r4[i] = make_uint4(0u, 0u, 0u, 0u);
     }
     __syncthreads();
     PMARK(4);
