@@ -80,7 +80,8 @@ class Detector:
             es = frames.element_size()
             pitch, fstride = frames.stride(1) * es, frames.stride(0) * es
         else:
-            frames = np.ascontiguousarray(frames)
+            if frames.ndim != 3 or frames.strides[2] != frames.itemsize:
+                frames = np.ascontiguousarray(frames)
             ptr, n = frames.ctypes.data, frames.shape[0]
             pitch, fstride = frames.strides[1], frames.strides[0]
         if rings is None:

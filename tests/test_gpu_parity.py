@@ -245,3 +245,44 @@ def test_detect_host_matches_device(rdmod):
     for i in range(70):
         assert hc[i] == len(dev_out[i])
         assert hr[i, : hc[i]].tobytes() == dev_out[i].tobytes()
+
+
+def test_full_batch_cfg4_dense(rdmod):
+    """cfg4 at BASELINE size (512 frames of 1024x1024, 200 rings): sampled frames vs the
+    oracle; every frame valid (no capacity overflow with the dense-config capacities)."""
+    params = dict(synth.preset(4), max_entries_per_tile=4096, max_hotspots_per_level=512)
+    frames = synth.batch(4, 0, 0, 512)
+    det = _det(rdmod, params, max_batch=512)
+    rings, counts = det.detect(torch.from_numpy(frames).cuda())
+    det.sync()
+    out = det.rings_to_numpy(rings, counts)
+    assert all(g is not None and len(g) > 100 for g in out)
+    for i in (0, 511):
+        _check_frame(rdmod, det, i, params, frames[i], out[i], full=False)
+
+
+def test_cfg5_high_frame_indices(rdmod):
+    """cfg5 (8192 frames = cfg3 seeds, sharded by frame): the last 256 frames as one rank's
+    batch; frame content is independent of the sharding (synth keys by frame index)."""
+    params = synth.preset(5)
+    frames = synth.batch(5, 0, 8192 - 256, 256)
+    assert np.array_equal(frames[-1], synth.frame(3, 0, 8191)[0])
+    det = _det(rdmod, params, max_batch=256)
+    rings, counts = det.detect(torch.from_numpy(frames).cuda())
+    det.sync()
+    out = det.rings_to_numpy(rings, counts)
+    for i in (0, 255):
+        _check_frame(rdmod, det, i, params, frames[i], out[i], full=False)
+
+
+def test_detect_host_pitched_frames(rdmod):
+    """rd_detect_host with a row pitch wider than the frame (non-contiguous rows)."""
+    params = synth.preset(2)
+    frames = synth.batch(2, 0, 20, 5)
+    padded = np.zeros((5, 480, 704), np.uint8)
+    padded[:, :, :640] = frames
+    det = _det(rdmod, params, max_batch=3)
+    hr, hc = det.detect_host(padded[:, :, :640])
+    p = oracle.params(**params)
+    for i in range(5):
+        _compare_rings(hr[i, : hc[i]], oracle.detect(p, frames[i])[0])
