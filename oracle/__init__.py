@@ -73,6 +73,9 @@ def lib():
         L.orc_detect_batch.restype = C.c_int
         L.orc_peaks.argtypes = [P, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]
         L.orc_peaks.restype = C.c_int64
+        L.orc_stream_peaks.argtypes = [P, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                                       C.POINTER(C.c_int64)]
+        L.orc_stream_peaks.restype = C.c_int64
         L.orc_fit.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32] + [C.POINTER(C.c_double)] * 4
         L.orc_fit.restype = C.c_int
         _LIB = L
@@ -183,6 +186,19 @@ def peaks(p, raw):
     if n < 0:
         raise RuntimeError("orc_peaks failed")
     return pk[:n].copy(), hot[: nh.value].copy()
+
+
+def stream_peaks(p, ridge_arr, hot_cap: int = 1 << 21):
+    """The paper's streamed steps 5-8 (SI steps 2-4) on a ridge list -> (peaks, hotspots)."""
+    ridge_arr = np.ascontiguousarray(ridge_arr, dtype=RIDGE_DTYPE)
+    pk = np.zeros(4096, dtype=HOT_DTYPE)
+    hot = np.zeros(hot_cap, dtype=HOT_DTYPE)
+    nh = C.c_int64()
+    n = lib().orc_stream_peaks(C.byref(p), ridge_arr.ctypes.data, len(ridge_arr), pk.ctypes.data, len(pk),
+                               hot.ctypes.data, hot_cap, C.byref(nh))
+    if n < 0:
+        raise RuntimeError("orc_stream_peaks failed")
+    return pk[: min(n, len(pk))].copy(), hot[: min(nh.value, hot_cap)].copy()
 
 
 def detect(p, img, want_debug=False):

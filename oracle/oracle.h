@@ -70,6 +70,13 @@ int64_t orc_window_sum(const orc_params* p, const int32_t* raw, int32_t r, int32
 int64_t orc_peaks(const orc_params* p, const int32_t* raw, orc_hotspot* peaks, int64_t peak_cap,
                   orc_hotspot* hot_out, int64_t hot_cap, int64_t* n_hot);
 
+/* streamed.c: the paper's own streamed form of steps 5-8 (SI steps 2-4):
+ * sorted vote stack, 3-level raw and normalised sub-spaces indexed by r mod 3, registration
+ * and undo.  Same outputs and order as orc_peaks on the full accumulator of the same ridges.
+ * Returns #peaks or -1 on allocation failure. */
+int64_t orc_stream_peaks(const orc_params* p, const orc_ridge* ridges, int64_t n_ridges, orc_hotspot* peaks,
+                         int64_t peak_cap, orc_hotspot* hot_out, int64_t hot_cap, int64_t* n_hot);
+
 /* Whole pipeline, steps 1-10, for one frame.  rings: canonical (r, cy, cx) order.
  * Optional debug outputs may be NULL.  Returns the number of rings (all are
  * written only if <= ring_cap), or -1 on allocation failure / bad parameters. */

@@ -40,10 +40,10 @@ def build_synth(force=False):
 
 def build_oracle(force=False):
     out = os.path.join(ROOT, "oracle", "liboracle.so")
-    srcs = [os.path.join(ROOT, "oracle", f) for f in ("oracle.c", "oracle.h")]
+    srcs = [os.path.join(ROOT, "oracle", f) for f in ("oracle.c", "streamed.c", "oracle.h")]
     if force or _stale(out, srcs):
         _run(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-Wall", "-o", out, srcs[0],
-              "-lm", "-lpthread"])
+              srcs[1], "-lm", "-lpthread"])
     return out
 
 
