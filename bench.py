@@ -99,8 +99,9 @@ def make_frames(first: int, n: int):
 
 
 # ------------------------------------------------------------------------ CPU oracle arm
-def cpu_oracle_rate(n_frames: int, first: int = 0, frames=None):
-    """Time the oracle (as it stands) on all host cores over a bounded sample."""
+def cpu_oracle_rate(n_frames: int, first: int = 0, frames=None, streamed: bool = False):
+    """Time the oracle (as it stands) on all host cores over a bounded sample.  streamed=True
+    times the paper's own streamed CPU method (oracle/streamed.c, NEXT-1) instead."""
     import oracle
     import synth
     p = oracle.params(**synth.preset(CFG))
@@ -108,7 +109,7 @@ def cpu_oracle_rate(n_frames: int, first: int = 0, frames=None):
         frames = make_frames(first, n_frames)
     cores = os.cpu_count() or 1
     t0 = time.perf_counter()
-    oracle.detect_batch(p, frames, nthreads=cores)
+    oracle.detect_batch(p, frames, nthreads=cores, streamed=streamed)
     dt = time.perf_counter() - t0
     return n_frames / dt, cores, dt
 
@@ -290,6 +291,10 @@ def run_gpu(args):
         rate, cores, dt = cpu_oracle_rate(n_cpu, frames=frames_h[:n_cpu])
         cpu = {"value": round(rate, 3), "unit": "frames/s", "cores": cores, "kind": "oracle",
                "sample": f"first {n_cpu} frames of this batch (cfg3, full frames), {dt:.1f} s wall"}
+        srate, _, sdt = cpu_oracle_rate(n_cpu, frames=frames_h[:n_cpu], streamed=True)
+        cpu["paper_streamed"] = {"value": round(srate, 3), "unit": "frames/s", "cores": cores,
+                                 "note": "the paper's streamed CPU method (sorted vote stack, r mod 3 "
+                                         f"sub-spaces; oracle/streamed.c), same sample, {sdt:.1f} s wall"}
 
     line = {"metric": METRIC, "value": round(value, 1), "unit": "frames/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,

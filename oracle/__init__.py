@@ -71,6 +71,8 @@ def lib():
         L.orc_detect_batch.argtypes = [P, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p,
                                        C.c_void_p, C.c_int32]
         L.orc_detect_batch.restype = C.c_int
+        L.orc_detect_batch_streamed.argtypes = L.orc_detect_batch.argtypes
+        L.orc_detect_batch_streamed.restype = C.c_int
         L.orc_peaks.argtypes = [P, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]
         L.orc_peaks.restype = C.c_int64
         L.orc_stream_peaks.argtypes = [P, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
@@ -226,13 +228,16 @@ def detect(p, img, want_debug=False):
     return res
 
 
-def detect_batch(p, frames: np.ndarray, nthreads: int = 0, ring_stride: int = 1024):
+def detect_batch(p, frames: np.ndarray, nthreads: int = 0, ring_stride: int = 1024, streamed: bool = False):
+    """Steps 1-10 on many frames with a host thread pool.  streamed=True does steps 5-8 the
+    paper's streamed way (oracle/streamed.c); the outputs are identical."""
     frames = np.ascontiguousarray(frames)
     n = frames.shape[0]
     rings = np.zeros((n, ring_stride), dtype=RING_DTYPE)
     counts = np.zeros(n, dtype=np.int32)
     stats = np.zeros(n, dtype=STATS_DTYPE)
-    rc = lib().orc_detect_batch(C.byref(p), frames.ctypes.data, frames.strides[0], n, rings.ctypes.data,
+    fn = lib().orc_detect_batch_streamed if streamed else lib().orc_detect_batch
+    rc = fn(C.byref(p), frames.ctypes.data, frames.strides[0], n, rings.ctypes.data,
                                 ring_stride, counts.ctypes.data, stats.ctypes.data, nthreads)
     if rc:
         raise RuntimeError("orc_detect_batch failed")

@@ -418,24 +418,32 @@ typedef struct detect_ws {
   int64_t hot_cap;
   orc_hotspot* peaks;
   int64_t peak_cap;
+  orc_stream_ws* sws;   /* non-NULL: steps 5-8 the streamed way (streamed.c) */
 } detect_ws;
 
-static int dws_init(detect_ws* d, const orc_params* p) {
+static int dws_init(detect_ws* d, const orc_params* p, int streamed) {
   memset(d, 0, sizeof *d);
   if (ws_alloc(&d->img, p->width, p->height)) return -1;
-  int nr = p->r_max - p->r_min + 3;
-  d->raw_cells = (size_t)nr * p->width * p->height;
-  d->raw = (int32_t*)malloc(d->raw_cells * sizeof(int32_t));
+  if (streamed) {
+    d->sws = orc_stream_ws_create(p);
+    if (!d->sws) return -1;
+  } else {
+    int nr = p->r_max - p->r_min + 3;
+    d->raw_cells = (size_t)nr * p->width * p->height;
+    d->raw = (int32_t*)malloc(d->raw_cells * sizeof(int32_t));
+    if (!d->raw) return -1;
+  }
   d->ridge_cap = (int64_t)p->width * p->height;
   d->ridges = (orc_ridge*)malloc(sizeof(orc_ridge) * (size_t)d->ridge_cap);
   d->hot_cap = 1 << 16;
   d->hot = (orc_hotspot*)malloc(sizeof(orc_hotspot) * (size_t)d->hot_cap);
   d->peak_cap = 4096;
   d->peaks = (orc_hotspot*)malloc(sizeof(orc_hotspot) * (size_t)d->peak_cap);
-  return d->raw && d->ridges && d->hot && d->peaks ? 0 : -1;
+  return d->ridges && d->hot && d->peaks ? 0 : -1;
 }
 static void dws_free(detect_ws* d) {
   ws_free(&d->img);
+  orc_stream_ws_free(d->sws);
   free(d->raw);
   free(d->ridges);
   free(d->hot);
@@ -578,18 +586,32 @@ static int64_t detect_ws_run(const orc_params* p, detect_ws* d, const void* fram
   int64_t nr = ridges_ws(p, &d->img, frame, pitch, d->ridges, d->ridge_cap);
   if (ridges_out)
     memcpy(ridges_out, d->ridges, sizeof(orc_ridge) * (size_t)(nr < ridge_cap ? nr : ridge_cap));
-  /* step 5: full accumulator, zeroed per frame */
-  memset(d->raw, 0, d->raw_cells * sizeof(int32_t));
-  int64_t votes = orc_votes(p, d->ridges, nr, d->raw);
-  /* steps 6-8 */
-  int64_t nh = 0;
-  int64_t npk = hot_and_peaks(p, d->raw, &d->hot, &d->hot_cap, &nh, d->peaks, d->peak_cap);
-  if (npk < 0) return -1;
-  if (npk > d->peak_cap) { /* grow and redo the (cheap) peak pass */
-    d->peak_cap = npk;
-    d->peaks = (orc_hotspot*)realloc(d->peaks, sizeof(orc_hotspot) * (size_t)d->peak_cap);
-    if (!d->peaks) return -1;
+  int64_t votes, nh = 0, npk;
+  if (d->sws) {
+    /* steps 5-8 streamed (SI steps 2-4); hotspots are not collected */
+    npk = orc_stream_peaks_ws(p, d->sws, d->ridges, nr, d->peaks, d->peak_cap, NULL, 0, &nh);
+    if (npk > d->peak_cap) {
+      d->peak_cap = npk;
+      d->peaks = (orc_hotspot*)realloc(d->peaks, sizeof(orc_hotspot) * (size_t)d->peak_cap);
+      if (!d->peaks) return -1;
+      npk = orc_stream_peaks_ws(p, d->sws, d->ridges, nr, d->peaks, d->peak_cap, NULL, 0, &nh);
+    }
+    if (npk < 0) return -1;
+    votes = orc_stream_votes(d->sws);
+    hot_out = NULL;
+  } else {
+    /* step 5: full accumulator, zeroed per frame */
+    memset(d->raw, 0, d->raw_cells * sizeof(int32_t));
+    votes = orc_votes(p, d->ridges, nr, d->raw);
+    /* steps 6-8 */
     npk = hot_and_peaks(p, d->raw, &d->hot, &d->hot_cap, &nh, d->peaks, d->peak_cap);
+    if (npk < 0) return -1;
+    if (npk > d->peak_cap) { /* grow and redo the (cheap) peak pass */
+      d->peak_cap = npk;
+      d->peaks = (orc_hotspot*)realloc(d->peaks, sizeof(orc_hotspot) * (size_t)d->peak_cap);
+      if (!d->peaks) return -1;
+      npk = hot_and_peaks(p, d->raw, &d->hot, &d->hot_cap, &nh, d->peaks, d->peak_cap);
+    }
   }
   if (hot_out) memcpy(hot_out, d->hot, sizeof(orc_hotspot) * (size_t)(nh < hot_cap ? nh : hot_cap));
   /* steps 9-10, rings in canonical (r, cy, cx) order (the hotspot scan order) */
@@ -608,7 +630,7 @@ int64_t orc_detect(const orc_params* p, const void* frame, int64_t pitch, orc_ri
                    int64_t hot_cap) {
   if (!params_ok(p)) return -1;
   detect_ws d;
-  if (dws_init(&d, p)) { dws_free(&d); return -1; }
+  if (dws_init(&d, p, 0)) { dws_free(&d); return -1; }
   int64_t n = detect_ws_run(p, &d, frame, pitch, rings, ring_cap, stats, ridges_out, ridge_cap, hot_out, hot_cap);
   dws_free(&d);
   return n;
@@ -625,13 +647,14 @@ typedef struct {
   orc_stats* stats;
   int next;
   int err;
+  int streamed;
   pthread_mutex_t mu;
 } batch_t;
 
 static void* batch_worker(void* arg) {
   batch_t* b = (batch_t*)arg;
   detect_ws d;
-  if (dws_init(&d, b->p)) { dws_free(&d); b->err = 1; return NULL; }
+  if (dws_init(&d, b->p, b->streamed)) { dws_free(&d); b->err = 1; return NULL; }
   for (;;) {
     pthread_mutex_lock(&b->mu);
     int i = b->next++;
@@ -648,15 +671,26 @@ static void* batch_worker(void* arg) {
   return NULL;
 }
 
-int orc_detect_batch(const orc_params* p, const void* frames, int64_t stride, int32_t n, orc_ring* rings,
-                     int32_t ring_stride, int32_t* counts, orc_stats* stats, int32_t nthreads) {
+static int detect_batch(const orc_params* p, const void* frames, int64_t stride, int32_t n, orc_ring* rings,
+                        int32_t ring_stride, int32_t* counts, orc_stats* stats, int32_t nthreads, int streamed) {
   if (!params_ok(p)) return -1;
   if (nthreads <= 0) nthreads = (int32_t)sysconf(_SC_NPROCESSORS_ONLN);
   if (nthreads > n) nthreads = n > 0 ? n : 1;
   if (nthreads > 512) nthreads = 512;
-  batch_t b = {p, (const uint8_t*)frames, stride, n, rings, ring_stride, counts, stats, 0, 0, PTHREAD_MUTEX_INITIALIZER};
+  batch_t b = {p, (const uint8_t*)frames, stride, n, rings, ring_stride, counts, stats, 0, 0, streamed,
+               PTHREAD_MUTEX_INITIALIZER};
   pthread_t th[512];
   for (int t = 0; t < nthreads; ++t) pthread_create(&th[t], NULL, batch_worker, &b);
   for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
   return b.err ? -1 : 0;
+}
+
+int orc_detect_batch(const orc_params* p, const void* frames, int64_t stride, int32_t n, orc_ring* rings,
+                     int32_t ring_stride, int32_t* counts, orc_stats* stats, int32_t nthreads) {
+  return detect_batch(p, frames, stride, n, rings, ring_stride, counts, stats, nthreads, 0);
+}
+
+int orc_detect_batch_streamed(const orc_params* p, const void* frames, int64_t stride, int32_t n, orc_ring* rings,
+                              int32_t ring_stride, int32_t* counts, orc_stats* stats, int32_t nthreads) {
+  return detect_batch(p, frames, stride, n, rings, ring_stride, counts, stats, nthreads, 1);
 }

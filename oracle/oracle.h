@@ -76,6 +76,19 @@ int64_t orc_peaks(const orc_params* p, const int32_t* raw, orc_hotspot* peaks, i
  * Returns #peaks or -1 on allocation failure. */
 int64_t orc_stream_peaks(const orc_params* p, const orc_ridge* ridges, int64_t n_ridges, orc_hotspot* peaks,
                          int64_t peak_cap, orc_hotspot* hot_out, int64_t hot_cap, int64_t* n_hot);
+/* the same with a per-thread workspace reused across frames (zero between calls) */
+typedef struct orc_stream_ws orc_stream_ws;
+orc_stream_ws* orc_stream_ws_create(const orc_params* p);
+void orc_stream_ws_free(orc_stream_ws* w);
+int64_t orc_stream_peaks_ws(const orc_params* p, orc_stream_ws* w, const orc_ridge* ridges, int64_t n_ridges,
+                            orc_hotspot* peaks, int64_t peak_cap, orc_hotspot* hot_out, int64_t hot_cap,
+                            int64_t* n_hot);
+int64_t orc_stream_votes(const orc_stream_ws* w);   /* votes of the last call */
+
+/* orc_detect_batch with steps 5-8 done the streamed way (NEXT-1): identical outputs. */
+int orc_detect_batch_streamed(const orc_params* p, const void* frames, int64_t frame_stride_bytes, int32_t n_frames,
+                              orc_ring* rings, int32_t ring_stride, int32_t* counts, orc_stats* stats,
+                              int32_t nthreads);
 
 /* Whole pipeline, steps 1-10, for one frame.  rings: canonical (r, cy, cx) order.
  * Optional debug outputs may be NULL.  Returns the number of rings (all are

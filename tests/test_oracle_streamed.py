@@ -82,3 +82,16 @@ def test_streamed_empty_and_single_level():
     pk_f, hot_f = _full(p, rid)
     _same(hot_s, hot_f)
     _same(pk_s, pk_f)
+
+
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_streamed_batch_rings_identical(cfg):
+    """Whole pipeline with the streamed stage: byte-identical rings and stats, threads reusing
+    their workspace across frames (the undo must leave it zero)."""
+    p = oracle.params(**synth.preset(cfg))
+    frames = synth.batch(cfg, 0, 0, 4 if cfg == 3 else 6)
+    r_full, st_full = oracle.detect_batch(p, frames, nthreads=2)
+    r_str, st_str = oracle.detect_batch(p, frames, nthreads=2, streamed=True)
+    for a, b in zip(r_full, r_str):
+        assert a.tobytes() == b.tobytes()
+    assert st_full.tobytes() == st_str.tobytes()
