@@ -1,0 +1,513 @@
+// k_hough2.cu — K2 (persistent form): directed voting, hotspot registration, radius-
+// dependent smoothing with 1/r normalisation and 3x3x3 peak extraction.
+//
+// Rows A5-A8 of DESIGN.md §1 (SI steps 2-4, PAPER.md:931-978;
+// range extension PAPER.md:998-1001).  Persistent CTAs (MINB per SM) take (frame, T x T
+// tile) work items from a global counter.  For its tile a CTA sweeps r upward G levels
+// per step, keeping on chip G levels of packed uint16 counters over the tile + (K_max+1)
+// halo and the hotspot lists of the last G + 2 levels (the paper's rolling level window,
+// PAPER.md:407-424).  A step has three phases separated by CTA barriers:
+//   (1) votes: one thread per active ray (ridge pixel x sense of rho, routed to this tile
+//       by K1.5, staged in shared memory by the previous step) casts its votes for the G
+//       levels of the step; the atomic that lifts a counter past T_raw registers the
+//       hotspot; the atomic that finds a zero 32-bit word appends the
+//       word to its warp's undo segment;
+//   (2) S at each hotspot — one warp (K > 7) or half-warp (K <= 7) per
+//       hotspot, lanes over window rows — and the candidate test S > T_norm(r)
+//        in the same pass; meanwhile the next step's active rays
+//       are selected and staged;
+//   (3) undo: each warp resets the words of its undo segment (the paper's register-and-
+//       undo; a bulk clear of the level buffers if a segment overflowed),
+//       and 3x3x3 peak extraction of the levels whose upper neighbour is complete
+//       (PAPER.md:967-972), one warp per candidate.
+// The shared-memory layout is computed on the host (Params::k2o, constant bank).  Only
+// peak records (and optional debug hotspots) leave the SM.
+#include <algorithm>
+
+#include "rd_internal.cuh"
+
+namespace rd {
+
+namespace {
+
+inline size_t al16(size_t v) { return (v + 15) & ~size_t(15); }
+
+constexpr int SMALL_K = 7;   // window rows 2K+1 <= 15: a half-warp per hotspot
+
+// llround of an exactly computed product (|v| < 2^31): copysign(0.5) added toward zero,
+// then truncated — the same two roundings as the oracle's llround (R9)
+__device__ __forceinline__ int round_half_away_i(double v) {
+  return __double2int_rz(__dadd_rz(v, copysign(0.5, v)));
+}
+
+// predicated shared-memory atomic add (no branch): returns the old word, or 1 if !pred
+__device__ __forceinline__ uint32_t atom_add_shared_if(uint32_t saddr, uint32_t v, uint32_t pred) {
+  uint32_t old = 1u;
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.u32 q, %3, 0;\n @q atom.shared.add.u32 %0, [%1], %2;\n}"
+      : "+r"(old)
+      : "r"(saddr), "r"(v), "r"(pred)
+      : "memory");
+  return old;
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+}  // namespace
+
+// Host: the K2 shared-memory layout for (G, threads) with the capacities in P; returns bytes.
+size_t k_hough2_layout(Params& P, int G, int nt) {
+  K2Layout& L = P.k2o;
+  const int NSLOT = G + 2, NW = nt / 32;
+  const int T = P.k2t, hot_cap = P.hot_cap, nlev = P.n_levels;
+  L.raws = T + 2 * P.hal;
+  // row pitch with an odd number of 32-bit words: the rows of a window fall in distinct banks
+  L.rawp = ((L.raws / 2) & 1) ? L.raws : L.raws + 2;
+  L.lvlc = (L.raws * L.rawp + 7) & ~7;   // 16-byte aligned level buffers (bulk clears)
+  L.tseg = std::max(P.k2_tcap / NW, 32) & ~7;
+  size_t o = 0;
+  L.raw = o;   o = al16(o + 2 * (size_t)G * L.lvlc);
+  L.hS = o;    o = al16(o + 8 * (size_t)NSLOT * hot_cap);
+  L.sd = o;    o = al16(o + 16 * (size_t)P.k2_scap);
+  L.hcell = o; o = al16(o + 2 * (size_t)NSLOT * hot_cap);
+  L.hraw = o;  o = al16(o + 2 * (size_t)NSLOT * hot_cap);
+  L.task = o;  o = al16(o + 2 * (size_t)G * hot_cap);
+  L.cand = o;  o = al16(o + 2 * (size_t)G * hot_cap);
+  L.cdef = o;  o = al16(o + 2 * 2 * (size_t)hot_cap);
+  L.touch = o; o = al16(o + 2 * (size_t)L.tseg * NW);
+  L.act = o;   o = al16(o + 2 * (size_t)P.entry_cap);
+  L.sxy = o;   o = al16(o + 4 * (size_t)P.k2_scap);
+  L.srr = o;   o = al16(o + 4 * (size_t)P.k2_scap);
+  L.hcnt = o;  o = al16(o + 4 * (size_t)(nlev + 32));
+  L.w = o;     o = al16(o + 2 * (size_t)nlev * P.wstride);
+  L.k = o;     o = al16(o + 4 * (size_t)nlev);
+  L.tn = o;    o = al16(o + 8 * (size_t)nlev);
+  L.total = (int)o;
+  return o;
+}
+
+template <bool kWide, int G, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Params P, int n_frames) {
+  constexpr int NSLOT = G + 2;
+  constexpr int NW = NT / 32;
+  constexpr unsigned FULL = 0xffffffffu;
+  extern __shared__ __align__(16) unsigned char smem[];
+#define SM(type, field) reinterpret_cast<type*>(smem + P.k2o.field)
+  uint32_t* raw32 = SM(uint32_t, raw);          // [G] levels of packed uint16 counters
+  uint16_t* raw16 = SM(uint16_t, raw);
+  unsigned long long* hS = SM(unsigned long long, hS);   // [NSLOT][hot_cap] S
+  uint16_t* hcell = SM(uint16_t, hcell);        // [NSLOT][hot_cap] iy<<8 | ix (ring coordinates)
+  uint16_t* hraw = SM(uint16_t, hraw);          // [NSLOT][hot_cap] raw count
+  uint16_t* tasks = SM(uint16_t, task);         // [G*hot_cap] g<<12 | h (small K front, large K back)
+  uint16_t* cand = SM(uint16_t, cand);          // [G*hot_cap] g<<12 | h
+  uint16_t* cdef = SM(uint16_t, cdef);          // [2][hot_cap] h, top level of a step
+  uint16_t* touch = SM(uint16_t, touch);        // [NW][tseg] raw32 word indices
+  uint16_t* act = SM(uint16_t, act);            // [entry_cap] active rays beyond the staging
+  double2* sd = SM(double2, sd);                // [scap] staged (s*dx, s*dy)
+  uint32_t* sxy = SM(uint32_t, sxy);            // [scap] staged raw-local x | y<<16 (int16 each)
+  uint32_t* srr = SM(uint32_t, srr);            // [scap] staged level interval ra | rb<<16
+  int* hcnt = SM(int, hcnt);                    // [nlev] hotspots per level + counters
+  uint16_t* tW = SM(uint16_t, w);               // [nlev][wstride] w_r(d)
+  int* tK = SM(int, k);                         // [nlev] K_r
+  double* tTn = SM(double, tn);                 // [nlev] T_norm(r)
+#undef SM
+  const int nlev = P.n_levels;
+  int* cnt = hcnt + nlev;
+  int* s_flags = cnt + 0;
+  int* s_nact = cnt + 2;    // [2] by step parity
+  int* s_ntask = cnt + 4;   // [2] small-K tasks from the front, large-K from the back
+  int* s_ncand = cnt + 6;
+  int* s_ndef = cnt + 8;    // [2] by step parity
+  int* s_bulk = cnt + 10;   // [2] by step parity: an undo segment overflowed
+  int* s_item = cnt + 12;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int T = P.k2t, hal = P.hal, hot_cap = P.hot_cap;
+  const int rawp = P.k2o.rawp, lvlc = P.k2o.lvlc, tseg = P.k2o.tseg, scap = P.k2_scap;
+  const int ntiles = P.ntx * P.nty;
+  const uint32_t T_raw = (uint32_t)P.T_raw;
+
+  unsigned long long t_acc[6] = {0, 0, 0, 0, 0, 0};
+  long long t_last = clock64();
+#define PMARK(i)                                      \
+  if (P.prof && tid == 0) {                           \
+    const long long t_ = clock64();                   \
+    t_acc[i] += (unsigned long long)(t_ - t_last);    \
+    t_last = t_;                                      \
+  }
+
+  // once per CTA: level tables, zeroed counters and raw levels (the undo keeps them zero)
+  for (int i = tid; i < nlev * P.wstride; i += NT) tW[i] = (uint16_t)P.lvlW[i];
+  for (int i = tid; i < nlev; i += NT) {
+    tK[i] = P.lvlK[i];
+    tTn[i] = P.lvlTn[i];
+  }
+  {
+    uint4* r4 = reinterpret_cast<uint4*>(raw32);
+    for (int i = tid; i < (G * lvlc) / 8; i += NT) r4[i] = make_uint4(0, 0, 0, 0);
+  }
+  for (int i = tid; i < 32; i += NT) cnt[i] = 0;
+  __syncthreads();
+
+  for (;;) {
+    if (tid == 0) *s_item = atomicAdd(P.k2_work, 1);
+    for (int i = tid; i < nlev; i += NT) hcnt[i] = 0;
+    __syncthreads();
+    const int item = *s_item;
+    if (item >= n_frames * ntiles) break;
+    const int f = item / ntiles, tile = item - f * ntiles;
+    const int tyi = tile / P.ntx, txi = tile - tyi * P.ntx;
+    const int X0 = txi * T, Y0 = tyi * T;
+    const int RX0 = X0 - hal, RY0 = Y0 - hal;   // raw buffer origin (frame coordinates)
+    const int64_t tl = (int64_t)f * ntiles + tile;
+    const int ne = min(P.ray_count[tl], P.entry_cap);
+    const int64_t gbase = tl * P.entry_cap;
+    int my_votes = 0, my_hot = 0;
+
+    // select the rays active in the step starting at level L0s and stage them (count: s_nact[p])
+    auto setup = [&](int L0s, int p) {
+      const int Lhs = min(L0s + G - 1, nlev - 1);
+      for (int e0 = warp * 32; e0 < ne; e0 += NT) {
+        const int e = e0 + lane;
+        uint32_t rr = 0xFFFFu;
+        if (e < ne) rr = __ldg(P.ray_r + gbase + e);
+        const bool a = (int)(rr & 0xFFFFu) <= Lhs && (int)(rr >> 16) >= L0s;
+        const unsigned bal = __ballot_sync(FULL, a);
+        if (!bal) continue;
+        int base = 0;
+        if (lane == 0) base = atomicAdd(&s_nact[p], __popc(bal));
+        base = __shfl_sync(FULL, base, 0);
+        if (!a) continue;
+        const int k = base + __popc(bal & lanemask_lt());
+        if (k < scap) {
+          const uint32_t xy = __ldg(P.ray_xy + gbase + e);
+          sd[k] = __ldg(P.ray_d + gbase + e);
+          sxy[k] = (uint32_t)(uint16_t)((int)(xy & 0xFFFFu) - RX0) | ((uint32_t)((int)(xy >> 16) - RY0) << 16);
+          srr[k] = rr;
+        } else {
+          act[k] = (uint16_t)e;
+        }
+      }
+    };
+    setup(0, 0);
+    PMARK(0);
+
+    for (int L0 = 0, step = 0; L0 < nlev; L0 += G, ++step) {
+      const int Lhi = min(L0 + G - 1, nlev - 1);
+      const int par = step & 1;
+      __syncthreads();
+      PMARK(1);
+      if (tid == 0) {   // counters whose last reader is behind the barrier above; first used after the next
+        s_nact[par ^ 1] = 0;
+        s_ncand[0] = 0;
+        s_ndef[par] = 0;
+        s_bulk[par ^ 1] = 0;
+      }
+      // ---------------- (1) votes of levels L0..Lhi
+      int tw = 0;   // words in this warp's undo segment (warp-uniform)
+      {
+        const int nact = s_nact[par];
+        const double rb0 = (double)(P.r_lo + L0);
+        uint16_t* seg = touch + warp * tseg;
+        const uint32_t raw_base = (uint32_t)__cvta_generic_to_shared(raw32);
+        const int bx0 = max(0, -RX0), bxs = min(P.k2o.raws - 1, P.W - 1 - RX0) - bx0;
+        const int by0 = max(0, -RY0), bys = min(P.k2o.raws - 1, P.H - 1 - RY0) - by0;
+        for (int i0 = warp * 32; i0 < nact; i0 += NT) {
+          const int i = i0 + lane;
+          int ga = G, gb = -1, xr = 0, yr = 0;
+          double dx = 0.0, dy = 0.0;
+          if (i < nact) {
+            uint32_t rr, xyr;
+            double2 d;
+            if (i < scap) {
+              d = sd[i];
+              xyr = sxy[i];
+              rr = srr[i];
+            } else {
+              const int e = act[i];
+              const uint32_t xy = __ldg(P.ray_xy + gbase + e);
+              d = __ldg(P.ray_d + gbase + e);
+              rr = __ldg(P.ray_r + gbase + e);
+              xyr = (uint32_t)(uint16_t)((int)(xy & 0xFFFFu) - RX0) | ((uint32_t)((int)(xy >> 16) - RY0) << 16);
+            }
+            ga = max((int)(rr & 0xFFFFu) - L0, 0);
+            gb = min((int)(rr >> 16) - L0, G - 1);
+            dx = d.x;
+            dy = d.y;
+            xr = (int)(int16_t)(xyr & 0xFFFFu);
+            yr = (int)(int16_t)(xyr >> 16);
+          }
+          // targets of the G levels, branch-free: a vote counts if its level is in the ray's
+          // interval and its cell lies in the raw buffer and in the frame (cells outside a
+          // level's box (tile + K_r + 1) are never read by that level's windows; undo clears them)
+          int cell[G], hc[G];
+          uint32_t old[G];
+          unsigned okm = 0, ringm = 0;
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const double rd = rb0 + (double)g;
+            const int cx = xr + round_half_away_i(__dmul_rn(rd, dx));
+            const int cy = yr + round_half_away_i(__dmul_rn(rd, dy));
+            const bool ok = (g >= ga) & (g <= gb) & ((unsigned)(cx - bx0) <= (unsigned)bxs) &
+                            ((unsigned)(cy - by0) <= (unsigned)bys);
+            cell[g] = g * lvlc + cy * rawp + cx;
+            const int ix = cx - (hal - 1), iy = cy - (hal - 1);
+            hc[g] = (iy << 8) | ix;
+            okm |= (unsigned)ok << g;
+            ringm |= (unsigned)(ok & ((unsigned)ix < (unsigned)(T + 2)) & ((unsigned)iy < (unsigned)(T + 2))) << g;
+            my_votes += ok & ((unsigned)(ix - 1) < (unsigned)T) & ((unsigned)(iy - 1) < (unsigned)T);
+          }
+#pragma unroll
+          for (int g = 0; g < G; ++g)
+            old[g] = atom_add_shared_if(raw_base + 4u * (uint32_t)(cell[g] >> 1), 1u << ((cell[g] & 1) << 4),
+                                        (okm >> g) & 1u);
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const bool first = old[g] == 0u;   // this vote found its 32-bit word zero: undo entry
+            const unsigned bal = __ballot_sync(FULL, first);
+            const int k = tw + __popc(bal & lanemask_lt());
+            if (first && k < tseg) seg[k] = (uint16_t)(cell[g] >> 1);
+            tw += __popc(bal);
+          }
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const uint32_t oc = (old[g] >> ((cell[g] & 1) << 4)) & 0xFFFFu;
+            if (((ringm >> g) & 1u) && oc == T_raw) {   // rare: this vote lifted the counter past T_raw
+              const int li = L0 + g;
+              const int h = atomicAdd(&hcnt[li], 1);
+              if (h < hot_cap) {
+                hcell[(li % NSLOT) * hot_cap + h] = (uint16_t)hc[g];
+                const int slot = tK[li] <= SMALL_K ? atomicAdd(&s_ntask[0], 1)
+                                                   : G * hot_cap - 1 - atomicAdd(&s_ntask[1], 1);
+                tasks[slot] = (uint16_t)((g << 12) | h);
+              } else {
+                atomicOr(s_flags, OVF_HOTSPOTS);
+              }
+            }
+          }
+        }
+        if (tw > tseg && lane == 0) s_bulk[par] = 1;
+      }
+      __syncthreads();
+      PMARK(2);
+      // ---------------- (2) S = sum_i w(i) sum_j w(j) raw(y+i, x+j) at each hotspot
+      //     (PAPER.md:962-966), the candidate test, and the next step's active rays
+      {
+        const int nsmall = s_ntask[0], nlarge = s_ntask[1];
+        const int half = lane >> 4;
+        // small-K hotspots: a half-warp each; large-K: a warp each (lanes over window rows)
+        const int nsp = (nsmall + 1) >> 1;
+        for (int t = warp; t < nsp + nlarge; t += NW) {
+          const bool small = t < nsp;
+          int tk;
+          bool valid = true;
+          if (small) {
+            const int ts = 2 * t + half;
+            valid = ts < nsmall;
+            tk = tasks[valid ? ts : 2 * t];
+          } else {
+            tk = tasks[G * hot_cap - 1 - (t - nsp)];
+          }
+          const int g = tk >> 12, h = tk & 0xFFF;
+          const int li = L0 + g, sl = li % NSLOT;
+          const int K = tK[li];
+          const uint16_t* w = tW + li * P.wstride;
+          const int c = hcell[sl * hot_cap + h];
+          const int iy = c >> 8, ix = c & 0xFF;
+          const uint16_t* ctr = raw16 + g * lvlc + (iy - 1 + hal) * rawp + (ix - 1 + hal);   // the hotspot's cell
+          const int sub = small ? (lane & 15) : lane;
+          unsigned long long acc = 0;
+          if (valid && sub <= 2 * K) {
+            const int row = sub;   // 2K+1 <= 31 rows (K <= 15), one per lane
+            const uint16_t* rowp = ctr + (row - K) * rawp;
+            if (kWide) {
+              unsigned long long rs = (unsigned long long)w[0] * rowp[0];
+              for (int j = 1; j <= K; ++j) rs += (unsigned long long)w[j] * (uint32_t)(rowp[-j] + rowp[j]);
+              acc = rs * (unsigned long long)w[abs(row - K)];
+            } else {
+              uint32_t rs = (uint32_t)w[0] * rowp[0];
+#pragma unroll 4
+              for (int j = 1; j <= K; ++j) rs += (uint32_t)w[j] * (uint32_t)(rowp[-j] + rowp[j]);
+              acc = (unsigned long long)rs * (unsigned long long)w[abs(row - K)];
+            }
+          }
+          unsigned long long S;
+          if (kWide) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              const unsigned long long v = __shfl_xor_sync(FULL, acc, o);
+              if (!(small && o == 16)) acc += v;
+            }
+            S = acc;
+          } else {   // lane terms < 2^45: 24-bit halves reduced with single-instruction reductions
+            const unsigned lo = (unsigned)(acc & 0xFFFFFFull), hi = (unsigned)(acc >> 24);
+            unsigned slo, shi;
+            if (small) {   // (warp-uniform branch) the two halves reduce separately
+              const unsigned lo0 = __reduce_add_sync(FULL, half ? 0u : lo);
+              const unsigned hi0 = __reduce_add_sync(FULL, half ? 0u : hi);
+              const unsigned lo1 = __reduce_add_sync(FULL, half ? lo : 0u);
+              const unsigned hi1 = __reduce_add_sync(FULL, half ? hi : 0u);
+              slo = half ? lo1 : lo0;
+              shi = half ? hi1 : hi0;
+            } else {
+              slo = __reduce_add_sync(FULL, lo);
+              shi = __reduce_add_sync(FULL, hi);
+            }
+            S = ((unsigned long long)shi << 24) + slo;
+          }
+          if (valid && sub == 0) {
+            hS[sl * hot_cap + h] = S;
+            const uint16_t rv = *ctr;
+            hraw[sl * hot_cap + h] = rv;
+            if (ix >= 1 && ix <= T && iy >= 1 && iy <= T) {   // interior hotspot
+              ++my_hot;
+              if (P.debug) {
+                const int kd = atomicAdd(&P.dbg_count[f], 1);
+                if (kd < P.dbg_cap) {
+                  HotRec rec;
+                  rec.r = P.r_lo + li; rec.y = Y0 - 1 + iy; rec.x = X0 - 1 + ix; rec.raw = rv;
+                  rec.S = (long long)S;
+                  P.dbg_hot[(int64_t)f * P.dbg_cap + kd] = rec;
+                } else {
+                  atomicOr(&P.flags[f], OVF_DEBUG);
+                }
+              }
+              // candidate: r in [r_min, r_max] and S > T_norm(r);
+              // the top level of the step waits for the next step's S of its upper neighbour
+              if (li >= 1 && li <= nlev - 2 && (double)(long long)S > tTn[li]) {
+                if (li == Lhi) cdef[par * hot_cap + atomicAdd(&s_ndef[par], 1)] = (uint16_t)h;
+                else cand[atomicAdd(s_ncand, 1)] = (uint16_t)tk;
+              }
+            }
+          }
+        }
+        if (L0 + G < nlev) setup(L0 + G, par ^ 1);
+      }
+      __syncthreads();
+      PMARK(3);
+      // ---------------- (3) undo the step's counters, then peaks of levels L0-1 .. Lhi-1
+      {
+        if (!s_bulk[par]) {
+          const uint16_t* seg = touch + warp * tseg;
+          for (int k = lane; k < tw; k += 32) raw32[seg[k]] = 0u;
+        } else {   // an undo segment overflowed: clear the step's level buffers
+          uint4* r4 = reinterpret_cast<uint4*>(raw16);
+          for (int i = tid; i < (G * lvlc) / 8; i += NT) r4[i] = make_uint4(0u, 0u, 0u, 0u);
+        }
+        if (tid == 0) {
+          s_ntask[0] = 0;
+          s_ntask[1] = 0;
+        }
+        const int nd = L0 > 0 ? s_ndef[par ^ 1] : 0, nc = s_ncand[0];
+        for (int p = warp; p < nd + nc; p += NW) {
+          int lc, h;
+          if (p < nd) {
+            lc = L0 - 1;
+            h = cdef[(par ^ 1) * hot_cap + p];
+          } else {
+            const int tk = cand[p - nd];
+            lc = L0 + (tk >> 12);
+            h = tk & 0xFFF;
+          }
+          const int sc = lc % NSLOT;
+          const int c = hcell[sc * hot_cap + h];
+          const int iy = c >> 8, ix = c & 0xFF;
+          const long long S = (long long)hS[sc * hot_cap + h];
+          const long long rc = P.r_lo + lc;
+          bool beaten = false;
+#pragma unroll
+          for (int dl = -1; dl <= 1; ++dl) {
+            const int l = lc + dl, sl = l % NSLOT;
+            const int n = min(hcnt[l], hot_cap);
+            const long long ru = P.r_lo + l;
+            for (int j = lane; j < n; j += 32) {
+              const int u = hcell[sl * hot_cap + j];
+              const int dy = (u >> 8) - iy, dx = (u & 0xFF) - ix;
+              if (dy < -1 || dy > 1 || dx < -1 || dx > 1 || (dl == 0 && dy == 0 && dx == 0)) continue;
+              const long long Su = (long long)hS[sl * hot_cap + j];
+              const long long lhs = S * ru, rhs = Su * rc;
+              const bool v_first = dl > 0 || (dl == 0 && (dy > 0 || (dy == 0 && dx > 0)));
+              if (!(lhs > rhs || (lhs == rhs && v_first))) beaten = true;
+            }
+          }
+          if (__any_sync(FULL, beaten)) continue;
+          if (lane == 0) {
+            const int kk = atomicAdd(&P.peak_count[f], 1);
+            if (kk < P.ring_cap) {
+              Peak pk;
+              pk.x = X0 - 1 + ix; pk.y = Y0 - 1 + iy; pk.r = (int)rc; pk.raw = hraw[sc * hot_cap + h]; pk.S = S;
+              P.peaks[(int64_t)f * P.ring_cap + kk] = pk;
+            } else {
+              atomicOr(&P.flags[f], OVF_RINGS);
+            }
+          }
+        }
+      }
+      PMARK(4);
+    }
+    // ---------------- per-frame counters of this tile
+    my_votes = __reduce_add_sync(FULL, my_votes);
+    my_hot = __reduce_add_sync(FULL, my_hot);
+    if (lane == 0) {
+      if (my_votes) atomicAdd(&P.stats[f].votes, (unsigned long long)my_votes);
+      if (my_hot) atomicAdd(&P.stats[f].hotspots, (unsigned long long)my_hot);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      if (*s_flags) atomicOr(&P.flags[f], *s_flags);
+      for (int i = 0; i < 12; ++i) cnt[i] = 0;   // flags and all step counters, for the next tile
+      if (P.prof) atomicAdd(&P.prof[15], 1ull);
+    }
+  }
+  if (P.prof && tid == 0) {
+#pragma unroll
+    for (int i = 0; i < 6; ++i) atomicAdd(&P.prof[i], t_acc[i]);
+  }
+#undef PMARK
+}
+
+template <bool Wd, int Gv, int NT, int MB>
+static cudaError_t launch2_one(int n_frames, const Params& P, int n_sm, cudaStream_t st) {
+  const size_t sm = (size_t)P.k2o.total;
+  cudaError_t e =
+      cudaFuncSetAttribute(k_hough2<Wd, Gv, NT, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hough2<Wd, Gv, NT, MB>, NT, sm);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  const int items = n_frames * P.ntx * P.nty;
+  const int grid = std::min(items, per_sm * n_sm);
+  k_hough2<Wd, Gv, NT, MB><<<grid, NT, sm, st>>>(P, n_frames);
+  return cudaGetLastError();
+}
+
+bool k_hough2_has_shape(int G, int nt, int minb) {
+  return (G == 4 && nt == 512 && minb == 2) || (G == 8 && nt == 512 && minb == 1) ||
+         (G == 4 && nt == 384 && minb == 2) || (G == 8 && nt == 384 && minb == 2) ||
+         (G == 4 && nt == 256 && minb == 3);
+}
+
+// shapes (G, threads, CTAs/SM) as listed in k_hough2_has_shape
+cudaError_t launch_hough2(int n_frames, const Params& P, bool wide, int G, int nt, int minb, int n_sm,
+                          cudaStream_t st) {
+  const int key = (G << 12) | (nt << 2) | (minb << 1) | (wide ? 1 : 0);
+#define CASE(Gv, NTv, MBv)                                                                    \
+  case (Gv << 12) | (NTv << 2) | (MBv << 1) | 0: return launch2_one<false, Gv, NTv, MBv>(n_frames, P, n_sm, st); \
+  case (Gv << 12) | (NTv << 2) | (MBv << 1) | 1: return launch2_one<true, Gv, NTv, MBv>(n_frames, P, n_sm, st);
+  switch (key) {
+    CASE(4, 512, 2)
+    CASE(8, 512, 1)
+    CASE(4, 384, 2)
+    CASE(8, 384, 2)
+    CASE(4, 256, 3)
+    default: return cudaErrorInvalidValue;
+  }
+#undef CASE
+}
+
+}  // namespace rd

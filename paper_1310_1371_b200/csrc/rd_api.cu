@@ -19,6 +19,10 @@ cudaError_t launch_eigen(const double* abc, int64_t n, double* out, int* deg, cu
 size_t k_hough_smem(const Params& P, int G);
 int k_hough_max_entries();
 cudaError_t launch_hough(int n_frames, const Params& P, bool wide, int G, int nt, int minb, cudaStream_t st);
+size_t k_hough2_layout(Params& P, int G, int nt);
+bool k_hough2_has_shape(int G, int nt, int minb);
+cudaError_t launch_hough2(int n_frames, const Params& P, bool wide, int G, int nt, int minb, int n_sm,
+                          cudaStream_t st);
 size_t k_fit_smem(const Params& P);
 cudaError_t launch_fit(int n_frames, const Params& P, void* rings, int* counts, cudaStream_t st);
 cudaError_t launch_rays(int n_frames, const Params& P, cudaStream_t st);
@@ -46,6 +50,8 @@ struct rd_detector {
   Params P;
   bool wide;
   int G, k2_threads, k2_minb;   // Hough kernel launch shape (levels per step, threads, CTAs/SM)
+  int k2_impl;                  // 2: persistent K2 (k_hough2.cu), 1: one CTA per tile (k_hough.cu)
+  int n_sm;
   // device allocations
   void* d_tables = nullptr;
   void* d_bins_count = nullptr;
@@ -241,17 +247,58 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
       shapes.insert(shapes.begin(), s);
   }
   det->G = 0;
-  for (const Shape& s : shapes) {
-    P.k2t = s.T;
-    const size_t need = k_hough_smem(P, s.G);
-    const size_t limit = s.minb == 1 ? smax : std::min(smax, sm_sm / s.minb - 1024);
-    if (need <= limit) {
+  det->n_sm = prop.multiProcessorCount;
+  det->k2_impl = 2;
+  if (const char* env = getenv("RD_K2_IMPL")) det->k2_impl = atoi(env) == 1 ? 1 : 2;
+  if (det->k2_impl == 2) {
+    // persistent K2: (G, threads, CTAs/SM) candidates, T = 64; RD_K2_SHAPE2="G,threads,ctas" first.
+    // Capacities: undo segments of 64*G words per warp, then as many staged rays (>= 256) as fit.
+    std::vector<Shape> sh2 = {{64, 4, 384, 2}, {64, 4, 512, 2}, {64, 8, 512, 1}};
+    if (const char* env = getenv("RD_K2_SHAPE2")) {
+      Shape s{64, 0, 0, 0};
+      if (sscanf(env, "%d,%d,%d", &s.G, &s.nt, &s.minb) == 3 && k_hough2_has_shape(s.G, s.nt, s.minb))
+        sh2.insert(sh2.begin(), s);
+    }
+    for (const Shape& s : sh2) {
+      P.k2t = s.T;
+      const size_t limit = s.minb == 1 ? smax : std::min(smax, sm_sm / s.minb - 1024);
+      const int raws = s.T + 2 * P.hal;
+      if ((int64_t)s.G * raws * (raws + 2) / 2 > 65535) continue;   // undo entries are 16-bit word indices
+      P.k2_tcap = 64 * s.G * (s.nt / 32);   // two full vote iterations per warp and step
+      P.k2_scap = 256;
+      if (k_hough2_layout(P, s.G, s.nt) > limit) continue;
+      while (P.k2_scap < P.entry_cap) {
+        P.k2_scap += 64;
+        if (k_hough2_layout(P, s.G, s.nt) > limit) {
+          P.k2_scap -= 64;
+          break;
+        }
+      }
+      k_hough2_layout(P, s.G, s.nt);
       det->G = s.G;
       det->k2_threads = s.nt;
       det->k2_minb = s.minb;
       break;
     }
   }
+  if (det->G == 0) {   // no persistent shape fits (large halo or capacities): one CTA per tile
+    det->k2_impl = 1;
+    for (const Shape& s : shapes) {
+      P.k2t = s.T;
+      const size_t need = k_hough_smem(P, s.G);
+      const size_t limit = s.minb == 1 ? smax : std::min(smax, sm_sm / s.minb - 1024);
+      if (need <= limit) {
+        det->G = s.G;
+        det->k2_threads = s.nt;
+        det->k2_minb = s.minb;
+        break;
+      }
+    }
+  }
+  if (getenv("RD_K2_VERBOSE"))
+    fprintf(stderr, "rd: K2 impl %d G %d threads %d ctas/SM %d smem %d scap %d tcap %d\n", det->k2_impl, det->G,
+            det->k2_threads, det->k2_minb, det->k2_impl == 2 ? P.k2o.total : (int)k_hough_smem(P, det->G),
+            P.k2_scap, P.k2_tcap);
   P.ntx = (c.width + P.k2t - 1) / P.k2t;
   P.nty = (c.height + P.k2t - 1) / P.k2t;
   if (k_ridges_smem(P.Ks) > smax || det->G == 0 || k_fit_smem(P) > smax) {
@@ -277,7 +324,7 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   ALLOC(det->d_ray_d, sizeof(double2) * B * ntl * P.entry_cap);
   ALLOC(det->d_ray_xy, sizeof(uint32_t) * B * ntl * P.entry_cap);
   ALLOC(det->d_ray_r, sizeof(uint32_t) * B * ntl * P.entry_cap);
-  det->counters_bytes = sizeof(Stats) * B + sizeof(int) * 3 * B + sizeof(int) * B * ntl;
+  det->counters_bytes = sizeof(Stats) * B + sizeof(int) * 3 * B + sizeof(int) * B * ntl + 16;
   ALLOC(det->d_counters, det->counters_bytes);
   if (c.debug) ALLOC(det->d_dbg, sizeof(HotRec) * B * P.dbg_cap);
   // tables
@@ -307,6 +354,7 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   P.flags = P.peak_count + B;
   P.dbg_count = P.flags + B;
   P.ray_count = P.dbg_count + B;
+  P.k2_work = P.ray_count + B * ntl;
   P.ray_d = (double2*)det->d_ray_d;
   P.ray_xy = (uint32_t*)det->d_ray_xy;
   P.ray_r = (uint32_t*)det->d_ray_r;
@@ -373,7 +421,10 @@ static rd_status detect_impl(rd_detector* det, const void* d_frames, int64_t pit
   if (ev) CK(cudaEventRecord(ev[1], st));
   CK(launch_rays(n, P, st));
   if (ev) CK(cudaEventRecord(ev[2], st));
-  CK(launch_hough(n, P, det->wide, det->G, det->k2_threads, det->k2_minb, st));
+  if (det->k2_impl == 2)
+    CK(launch_hough2(n, P, det->wide, det->G, det->k2_threads, det->k2_minb, det->n_sm, st));
+  else
+    CK(launch_hough(n, P, det->wide, det->G, det->k2_threads, det->k2_minb, st));
   if (ev) CK(cudaEventRecord(ev[3], st));
   CK(launch_fit(n, P, d_rings, d_counts, st));
   if (ev) CK(cudaEventRecord(ev[4], st));

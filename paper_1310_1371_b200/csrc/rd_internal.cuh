@@ -29,6 +29,12 @@ struct Stats {         // per-frame counters (same layout as rd_frame_stats)
   unsigned long long ridges, votes, hotspots, peaks;
 };
 
+// Shared-memory layout of the persistent Hough kernel (byte offsets; host-computed)
+struct K2Layout {
+  int raws, rawp, lvlc, tseg;
+  int raw, hS, sd, hcell, hraw, task, cand, cdef, touch, act, sxy, srr, hcnt, w, k, tn, total;
+};
+
 // Everything the kernels need, passed by value (< 4 KB).
 struct Params {
   int W, H, pixel_bytes;
@@ -60,6 +66,10 @@ struct Params {
   double2* ray_d;               // [F][tiles][entry_cap] (s*dx, s*dy)
   uint32_t* ray_xy;             // [F][tiles][entry_cap] x | y<<16
   uint32_t* ray_r;              // [F][tiles][entry_cap] ra | rb<<16 (level indices)
+  int* k2_work;                 // persistent K2: next (frame, tile) work item (zeroed per call)
+  int k2_tcap;                  // K2 undo-list capacity (32-bit words per step, all warps)
+  int k2_scap;                  // K2 staged active rays per step
+  K2Layout k2o;
   int ring_cap;
   Peak* peaks;                  // [F][ring_cap]
   int* peak_count;              // [F]
