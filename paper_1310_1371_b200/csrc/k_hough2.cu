@@ -4,25 +4,29 @@
 // Rows A5-A8 of DESIGN.md §1 (SI steps 2-4, PAPER.md:931-978;
 // range extension PAPER.md:998-1001).  Persistent CTAs (MINB per SM) take (frame, T x T
 // tile) work items from a global counter.  For its tile a CTA sweeps r upward G levels
-// per step, keeping on chip G levels of packed uint16 counters over the tile + (K_max+1)
-// halo and the hotspot lists of the last G + 2 levels (the paper's rolling level window,
-// PAPER.md:407-424).  A step has three phases separated by CTA barriers:
+// per step, keeping on chip G levels of packed counters (CB = 1 or 2 bytes) over the tile
+// + (K_max+1) halo and the hotspot lists of the last G + 2 levels (the paper's rolling
+// level window).  A step has three phases separated by CTA barriers:
 //   (1) votes: one thread per active ray (ridge pixel x sense of rho, routed to this tile
-//       by K1.5, staged in shared memory by the previous step) casts its votes for the G
-//       levels of the step; the atomic that lifts a counter past T_raw registers the
+//       by K1.5, staged in shared memory during the previous step) casts its votes for the
+//       G levels of the step; the atomic that lifts a counter past T_raw registers the
 //       hotspot; the atomic that finds a zero 32-bit word appends the
 //       word to its warp's undo segment;
-//   (2) S at each hotspot — one warp (K > 7) or half-warp (K <= 7) per
-//       hotspot, lanes over window rows — and the candidate test S > T_norm(r)
-//        in the same pass; meanwhile the next step's active rays
-//       are selected and staged;
+//   (2) the rays of the next step are selected and their staging copies issued
+//       (cp.async); S at each hotspot — one warp (K > 7) or half-warp
+//       (K <= 7) per hotspot, lanes over window rows — and the candidate test
+//       S > T_norm(r) in the same pass;
 //   (3) undo: each warp resets the words of its undo segment (the paper's register-and-
 //       undo; a bulk clear of the level buffers if a segment overflowed),
 //       and 3x3x3 peak extraction of the levels whose upper neighbour is complete
 //       (PAPER.md:967-972), one warp per candidate.
+// Byte counters (CB = 1) are exact while no counter passes 255: the atomic that finds 255
+// marks the frame, whose K2 results are then discarded and recomputed by the CB = 2
+// instance (k_redo_reset + the redo list), so results never depend on the counter width.
 // The shared-memory layout is computed on the host (Params::k2o, constant bank).  Only
 // peak records (and optional debug hotspots) leave the SM.
 #include <algorithm>
+#include <type_traits>
 
 #include "rd_internal.cuh"
 
@@ -40,7 +44,7 @@ __device__ __forceinline__ int round_half_away_i(double v) {
   return __double2int_rz(__dadd_rz(v, copysign(0.5, v)));
 }
 
-// predicated shared-memory atomic add (no branch): returns the old word, or 1 if !pred
+// predicated shared-memory atomic add: returns the old word, or 1 if !pred
 __device__ __forceinline__ uint32_t atom_add_shared_if(uint32_t saddr, uint32_t v, uint32_t pred) {
   uint32_t old = 1u;
   asm volatile(
@@ -51,6 +55,14 @@ __device__ __forceinline__ uint32_t atom_add_shared_if(uint32_t saddr, uint32_t 
   return old;
 }
 
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -59,20 +71,27 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 
 }  // namespace
 
-// Host: the K2 shared-memory layout for (G, threads) with the capacities in P; returns bytes.
-size_t k_hough2_layout(Params& P, int G, int nt) {
+// Host: the K2 shared-memory layout for (G, threads, counter bytes) with the capacities in
+// P (hot_cap, entry_cap, k2_tcap, k2_scap); returns the bytes.
+size_t k_hough2_layout(Params& P, int G, int nt, int cb) {
   K2Layout& L = P.k2o;
   const int NSLOT = G + 2, NW = nt / 32;
   const int T = P.k2t, hot_cap = P.hot_cap, nlev = P.n_levels;
+  L.cb = cb;
   L.raws = T + 2 * P.hal;
-  // row pitch with an odd number of 32-bit words: the rows of a window fall in distinct banks
-  L.rawp = ((L.raws / 2) & 1) ? L.raws : L.raws + 2;
-  L.lvlc = (L.raws * L.rawp + 7) & ~7;   // 16-byte aligned level buffers (bulk clears)
+  // row pitch of an odd number of 32-bit words: the rows of a window fall in distinct banks
+  const int cpw = 4 / cb;   // cells per word
+  L.rawp = ((L.raws + cpw - 1) / cpw) | 1;
+  L.rawp *= cpw;
+  L.lvlc = (L.raws * L.rawp + 15) & ~15;   // 16-byte aligned level buffers (bulk clears)
   L.tseg = std::max(P.k2_tcap / NW, 32) & ~7;
   size_t o = 0;
-  L.raw = o;   o = al16(o + 2 * (size_t)G * L.lvlc);
+  L.raw = o;   o = al16(o + (size_t)cb * G * L.lvlc);
   L.hS = o;    o = al16(o + 8 * (size_t)NSLOT * hot_cap);
   L.sd = o;    o = al16(o + 16 * (size_t)P.k2_scap);
+  L.rr = o;    o = al16(o + 4 * (size_t)P.entry_cap);
+  L.sxy = o;   o = al16(o + 4 * (size_t)P.k2_scap);
+  L.srr = o;   o = al16(o + 4 * (size_t)P.k2_scap);
   L.hcell = o; o = al16(o + 2 * (size_t)NSLOT * hot_cap);
   L.hraw = o;  o = al16(o + 2 * (size_t)NSLOT * hot_cap);
   L.task = o;  o = al16(o + 2 * (size_t)G * hot_cap);
@@ -80,8 +99,6 @@ size_t k_hough2_layout(Params& P, int G, int nt) {
   L.cdef = o;  o = al16(o + 2 * 2 * (size_t)hot_cap);
   L.touch = o; o = al16(o + 2 * (size_t)L.tseg * NW);
   L.act = o;   o = al16(o + 2 * (size_t)P.entry_cap);
-  L.sxy = o;   o = al16(o + 4 * (size_t)P.k2_scap);
-  L.srr = o;   o = al16(o + 4 * (size_t)P.k2_scap);
   L.hcnt = o;  o = al16(o + 4 * (size_t)(nlev + 32));
   L.w = o;     o = al16(o + 2 * (size_t)nlev * P.wstride);
   L.k = o;     o = al16(o + 4 * (size_t)nlev);
@@ -90,16 +107,24 @@ size_t k_hough2_layout(Params& P, int G, int nt) {
   return o;
 }
 
-template <bool kWide, int G, int NT, int MINB>
+template <bool kWide, int G, int NT, int MINB, int CB>
 __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Params P, int n_frames) {
   constexpr int NSLOT = G + 2;
   constexpr int NW = NT / 32;
+  constexpr int CSH = CB == 1 ? 2 : 1;          // log2(cells per 32-bit word)
+  constexpr int BITS = 8 * CB;
+  constexpr uint32_t CMASK = CB == 1 ? 0xFFu : 0xFFFFu;
   constexpr unsigned FULL = 0xffffffffu;
+  typedef typename std::conditional<CB == 1, uint8_t, uint16_t>::type cell_t;
   extern __shared__ __align__(16) unsigned char smem[];
 #define SM(type, field) reinterpret_cast<type*>(smem + P.k2o.field)
-  uint32_t* raw32 = SM(uint32_t, raw);          // [G] levels of packed uint16 counters
-  uint16_t* raw16 = SM(uint16_t, raw);
+  uint32_t* raw32 = SM(uint32_t, raw);          // [G] levels of packed counters
+  cell_t* rawc = SM(cell_t, raw);
   unsigned long long* hS = SM(unsigned long long, hS);   // [NSLOT][hot_cap] S
+  double2* sd = SM(double2, sd);                // [scap] staged (s*dx, s*dy)
+  uint32_t* rr_s = SM(uint32_t, rr);            // [entry_cap] level interval ra | rb<<16 of every ray
+  uint32_t* sxy = SM(uint32_t, sxy);            // [scap] staged x | y<<16 (frame coordinates)
+  uint32_t* srr = SM(uint32_t, srr);            // [scap] staged level interval
   uint16_t* hcell = SM(uint16_t, hcell);        // [NSLOT][hot_cap] iy<<8 | ix (ring coordinates)
   uint16_t* hraw = SM(uint16_t, hraw);          // [NSLOT][hot_cap] raw count
   uint16_t* tasks = SM(uint16_t, task);         // [G*hot_cap] g<<12 | h (small K front, large K back)
@@ -107,9 +132,6 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
   uint16_t* cdef = SM(uint16_t, cdef);          // [2][hot_cap] h, top level of a step
   uint16_t* touch = SM(uint16_t, touch);        // [NW][tseg] raw32 word indices
   uint16_t* act = SM(uint16_t, act);            // [entry_cap] active rays beyond the staging
-  double2* sd = SM(double2, sd);                // [scap] staged (s*dx, s*dy)
-  uint32_t* sxy = SM(uint32_t, sxy);            // [scap] staged raw-local x | y<<16 (int16 each)
-  uint32_t* srr = SM(uint32_t, srr);            // [scap] staged level interval ra | rb<<16
   int* hcnt = SM(int, hcnt);                    // [nlev] hotspots per level + counters
   uint16_t* tW = SM(uint16_t, w);               // [nlev][wstride] w_r(d)
   int* tK = SM(int, k);                         // [nlev] K_r
@@ -124,12 +146,16 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
   int* s_ndef = cnt + 8;    // [2] by step parity
   int* s_bulk = cnt + 10;   // [2] by step parity: an undo segment overflowed
   int* s_item = cnt + 12;
+  int* s_ovf = cnt + 13;    // a byte counter passed 255
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int T = P.k2t, hal = P.hal, hot_cap = P.hot_cap;
   const int rawp = P.k2o.rawp, lvlc = P.k2o.lvlc, tseg = P.k2o.tseg, scap = P.k2_scap;
   const int ntiles = P.ntx * P.nty;
   const uint32_t T_raw = (uint32_t)P.T_raw;
+  // CB = 2 is also the redo pass: work items are then the tiles of the frames in the redo list
+  const bool redo_pass = CB == 2 && P.redo_list != nullptr;
+  const int n_work_frames = redo_pass ? P.redo_list[0] : n_frames;
 
   unsigned long long t_acc[6] = {0, 0, 0, 0, 0, 0};
   long long t_last = clock64();
@@ -148,18 +174,19 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
   }
   {
     uint4* r4 = reinterpret_cast<uint4*>(raw32);
-    for (int i = tid; i < (G * lvlc) / 8; i += NT) r4[i] = make_uint4(0, 0, 0, 0);
+    for (int i = tid; i < (CB * G * lvlc) / 16; i += NT) r4[i] = make_uint4(0, 0, 0, 0);
   }
   for (int i = tid; i < 32; i += NT) cnt[i] = 0;
   __syncthreads();
 
   for (;;) {
-    if (tid == 0) *s_item = atomicAdd(P.k2_work, 1);
+    if (tid == 0) *s_item = atomicAdd(redo_pass ? P.k2_work + 1 : P.k2_work, 1);
     for (int i = tid; i < nlev; i += NT) hcnt[i] = 0;
     __syncthreads();
     const int item = *s_item;
-    if (item >= n_frames * ntiles) break;
-    const int f = item / ntiles, tile = item - f * ntiles;
+    if (item >= n_work_frames * ntiles) break;
+    const int fw = item / ntiles, tile = item - fw * ntiles;
+    const int f = redo_pass ? P.redo_list[1 + fw] : fw;
     const int tyi = tile / P.ntx, txi = tile - tyi * P.ntx;
     const int X0 = txi * T, Y0 = tyi * T;
     const int RX0 = X0 - hal, RY0 = Y0 - hal;   // raw buffer origin (frame coordinates)
@@ -168,13 +195,13 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
     const int64_t gbase = tl * P.entry_cap;
     int my_votes = 0, my_hot = 0;
 
-    // select the rays active in the step starting at level L0s and stage them (count: s_nact[p])
+    // select the rays active in the step starting at level L0s (count: s_nact[p]) and issue
+    // the asynchronous copies that stage them; the caller waits (cp.async.wait_all)
     auto setup = [&](int L0s, int p) {
       const int Lhs = min(L0s + G - 1, nlev - 1);
       for (int e0 = warp * 32; e0 < ne; e0 += NT) {
         const int e = e0 + lane;
-        uint32_t rr = 0xFFFFu;
-        if (e < ne) rr = __ldg(P.ray_r + gbase + e);
+        const uint32_t rr = e < ne ? rr_s[e] : 0xFFFFu;
         const bool a = (int)(rr & 0xFFFFu) <= Lhs && (int)(rr >> 16) >= L0s;
         const unsigned bal = __ballot_sync(FULL, a);
         if (!bal) continue;
@@ -184,16 +211,18 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
         if (!a) continue;
         const int k = base + __popc(bal & lanemask_lt());
         if (k < scap) {
-          const uint32_t xy = __ldg(P.ray_xy + gbase + e);
-          sd[k] = __ldg(P.ray_d + gbase + e);
-          sxy[k] = (uint32_t)(uint16_t)((int)(xy & 0xFFFFu) - RX0) | ((uint32_t)((int)(xy >> 16) - RY0) << 16);
+          cp_async16(&sd[k], P.ray_d + gbase + e);
+          cp_async4(&sxy[k], P.ray_xy + gbase + e);
           srr[k] = rr;
         } else {
           act[k] = (uint16_t)e;
         }
       }
     };
+    for (int e = tid; e < ne; e += NT) rr_s[e] = __ldg(P.ray_r + gbase + e);
+    __syncthreads();
     setup(0, 0);
+    cp_async_wait_all();
     PMARK(0);
 
     for (int L0 = 0, step = 0; L0 < nlev; L0 += G, ++step) {
@@ -213,37 +242,37 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
         const int nact = s_nact[par];
         const double rb0 = (double)(P.r_lo + L0);
         uint16_t* seg = touch + warp * tseg;
-        const uint32_t raw_base = (uint32_t)__cvta_generic_to_shared(raw32);
+        const uint32_t raw_base = smem_u32(raw32);
         const int bx0 = max(0, -RX0), bxs = min(P.k2o.raws - 1, P.W - 1 - RX0) - bx0;
         const int by0 = max(0, -RY0), bys = min(P.k2o.raws - 1, P.H - 1 - RY0) - by0;
+        bool ovf = false;
         for (int i0 = warp * 32; i0 < nact; i0 += NT) {
           const int i = i0 + lane;
           int ga = G, gb = -1, xr = 0, yr = 0;
           double dx = 0.0, dy = 0.0;
           if (i < nact) {
-            uint32_t rr, xyr;
+            uint32_t rr, xy;
             double2 d;
             if (i < scap) {
               d = sd[i];
-              xyr = sxy[i];
+              xy = sxy[i];
               rr = srr[i];
             } else {
               const int e = act[i];
-              const uint32_t xy = __ldg(P.ray_xy + gbase + e);
+              xy = __ldg(P.ray_xy + gbase + e);
               d = __ldg(P.ray_d + gbase + e);
-              rr = __ldg(P.ray_r + gbase + e);
-              xyr = (uint32_t)(uint16_t)((int)(xy & 0xFFFFu) - RX0) | ((uint32_t)((int)(xy >> 16) - RY0) << 16);
+              rr = rr_s[e];
             }
             ga = max((int)(rr & 0xFFFFu) - L0, 0);
             gb = min((int)(rr >> 16) - L0, G - 1);
             dx = d.x;
             dy = d.y;
-            xr = (int)(int16_t)(xyr & 0xFFFFu);
-            yr = (int)(int16_t)(xyr >> 16);
+            xr = (int)(xy & 0xFFFFu) - RX0;
+            yr = (int)(xy >> 16) - RY0;
           }
           // targets of the G levels, branch-free: a vote counts if its level is in the ray's
           // interval and its cell lies in the raw buffer and in the frame (cells outside a
-          // level's box (tile + K_r + 1) are never read by that level's windows; undo clears them)
+          // level's box, tile + K_r + 1, are never read by that level's windows; undo clears them)
           int cell[G], hc[G];
           uint32_t old[G];
           unsigned okm = 0, ringm = 0;
@@ -263,19 +292,20 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
           }
 #pragma unroll
           for (int g = 0; g < G; ++g)
-            old[g] = atom_add_shared_if(raw_base + 4u * (uint32_t)(cell[g] >> 1), 1u << ((cell[g] & 1) << 4),
-                                        (okm >> g) & 1u);
+            old[g] = atom_add_shared_if(raw_base + 4u * (uint32_t)(cell[g] >> CSH),
+                                        1u << ((cell[g] & ((1 << CSH) - 1)) * BITS), (okm >> g) & 1u);
 #pragma unroll
           for (int g = 0; g < G; ++g) {
             const bool first = old[g] == 0u;   // this vote found its 32-bit word zero: undo entry
             const unsigned bal = __ballot_sync(FULL, first);
             const int k = tw + __popc(bal & lanemask_lt());
-            if (first && k < tseg) seg[k] = (uint16_t)(cell[g] >> 1);
+            if (first && k < tseg) seg[k] = (uint16_t)(cell[g] >> CSH);
             tw += __popc(bal);
           }
 #pragma unroll
           for (int g = 0; g < G; ++g) {
-            const uint32_t oc = (old[g] >> ((cell[g] & 1) << 4)) & 0xFFFFu;
+            const uint32_t oc = (old[g] >> ((cell[g] & ((1 << CSH) - 1)) * BITS)) & CMASK;
+            if (CB == 1) ovf |= ((okm >> g) & 1u) && oc == CMASK;
             if (((ringm >> g) & 1u) && oc == T_raw) {   // rare: this vote lifted the counter past T_raw
               const int li = L0 + g;
               const int h = atomicAdd(&hcnt[li], 1);
@@ -291,12 +321,14 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
           }
         }
         if (tw > tseg && lane == 0) s_bulk[par] = 1;
+        if (CB == 1 && __any_sync(FULL, ovf) && lane == 0) *s_ovf = 1;
       }
       __syncthreads();
       PMARK(2);
-      // ---------------- (2) S = sum_i w(i) sum_j w(j) raw(y+i, x+j) at each hotspot
-      //     (PAPER.md:962-966), the candidate test, and the next step's active rays
+      // ---------------- (2) the next step's rays; S = sum_i w(i) sum_j w(j) raw(y+i, x+j) at
+      //     each hotspot and the candidate test
       {
+        if (L0 + G < nlev) setup(L0 + G, par ^ 1);
         const int nsmall = s_ntask[0], nlarge = s_ntask[1];
         const int half = lane >> 4;
         // small-K hotspots: a half-warp each; large-K: a warp each (lanes over window rows)
@@ -318,12 +350,12 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
           const uint16_t* w = tW + li * P.wstride;
           const int c = hcell[sl * hot_cap + h];
           const int iy = c >> 8, ix = c & 0xFF;
-          const uint16_t* ctr = raw16 + g * lvlc + (iy - 1 + hal) * rawp + (ix - 1 + hal);   // the hotspot's cell
+          const cell_t* ctr = rawc + g * lvlc + (iy - 1 + hal) * rawp + (ix - 1 + hal);   // the hotspot's cell
           const int sub = small ? (lane & 15) : lane;
           unsigned long long acc = 0;
           if (valid && sub <= 2 * K) {
             const int row = sub;   // 2K+1 <= 31 rows (K <= 15), one per lane
-            const uint16_t* rowp = ctr + (row - K) * rawp;
+            const cell_t* rowp = ctr + (row - K) * rawp;
             if (kWide) {
               unsigned long long rs = (unsigned long long)w[0] * rowp[0];
               for (int j = 1; j <= K; ++j) rs += (unsigned long long)w[j] * (uint32_t)(rowp[-j] + rowp[j]);
@@ -385,7 +417,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
             }
           }
         }
-        if (L0 + G < nlev) setup(L0 + G, par ^ 1);
+        cp_async_wait_all();
       }
       __syncthreads();
       PMARK(3);
@@ -395,8 +427,8 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
           const uint16_t* seg = touch + warp * tseg;
           for (int k = lane; k < tw; k += 32) raw32[seg[k]] = 0u;
         } else {   // an undo segment overflowed: clear the step's level buffers
-          uint4* r4 = reinterpret_cast<uint4*>(raw16);
-          for (int i = tid; i < (G * lvlc) / 8; i += NT) r4[i] = make_uint4(0u, 0u, 0u, 0u);
+          uint4* r4 = reinterpret_cast<uint4*>(raw32);
+          for (int i = tid; i < (CB * G * lvlc) / 16; i += NT) r4[i] = make_uint4(0u, 0u, 0u, 0u);
         }
         if (tid == 0) {
           s_ntask[0] = 0;
@@ -459,7 +491,9 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
     __syncthreads();
     if (tid == 0) {
       if (*s_flags) atomicOr(&P.flags[f], *s_flags);
-      for (int i = 0; i < 12; ++i) cnt[i] = 0;   // flags and all step counters, for the next tile
+      if (CB == 1 && *s_ovf) atomicExch(&P.redo[f], 1);
+      for (int i = 0; i < 14; ++i)
+        if (i != 12) cnt[i] = 0;   // flags and all step counters, for the next tile
       if (P.prof) atomicAdd(&P.prof[15], 1ull);
     }
   }
@@ -470,44 +504,81 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
 #undef PMARK
 }
 
-template <bool Wd, int Gv, int NT, int MB>
+// Frames marked by the byte-counter pass: discard their K2 results (peaks, K2 counters and
+// flag bits) and list them for the 16-bit pass.  One CTA.
+__global__ void k_redo_reset(Params P, int n_frames) {
+  __shared__ int n;
+  if (threadIdx.x == 0) n = 0;
+  __syncthreads();
+  for (int f = threadIdx.x; f < n_frames; f += blockDim.x) {
+    if (!P.redo[f] && !P.force_redo) continue;
+    P.peak_count[f] = 0;
+    P.stats[f].votes = 0;
+    P.stats[f].hotspots = 0;
+    P.dbg_count[f] = 0;
+    P.flags[f] &= ~(OVF_HOTSPOTS | OVF_RINGS | OVF_DEBUG);
+    P.redo_list[1 + atomicAdd(&n, 1)] = f;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) P.redo_list[0] = n;
+}
+
+template <bool Wd, int Gv, int NT, int MB, int CB>
 static cudaError_t launch2_one(int n_frames, const Params& P, int n_sm, cudaStream_t st) {
   const size_t sm = (size_t)P.k2o.total;
   cudaError_t e =
-      cudaFuncSetAttribute(k_hough2<Wd, Gv, NT, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      cudaFuncSetAttribute(k_hough2<Wd, Gv, NT, MB, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hough2<Wd, Gv, NT, MB>, NT, sm);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hough2<Wd, Gv, NT, MB, CB>, NT, sm);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   const int items = n_frames * P.ntx * P.nty;
   const int grid = std::min(items, per_sm * n_sm);
-  k_hough2<Wd, Gv, NT, MB><<<grid, NT, sm, st>>>(P, n_frames);
+  k_hough2<Wd, Gv, NT, MB, CB><<<grid, NT, sm, st>>>(P, n_frames);
   return cudaGetLastError();
 }
 
-bool k_hough2_has_shape(int G, int nt, int minb) {
-  return (G == 4 && nt == 512 && minb == 2) || (G == 8 && nt == 512 && minb == 1) ||
-         (G == 4 && nt == 384 && minb == 2) || (G == 8 && nt == 384 && minb == 2) ||
-         (G == 4 && nt == 256 && minb == 3);
+bool k_hough2_has_shape(int cb, int G, int nt, int minb) {
+  if (cb == 1)
+    return (G == 4 && nt == 384 && minb == 2) || (G == 4 && nt == 512 && minb == 2) ||
+           (G == 8 && nt == 384 && minb == 2) || (G == 8 && nt == 512 && minb == 1) ||
+           (G == 4 && nt == 256 && minb == 3) || (G == 8 && nt == 256 && minb == 2) ||
+           (G == 2 && nt == 256 && minb == 4) || (G == 2 && nt == 256 && minb == 3);
+  return (G == 4 && nt == 384 && minb == 2) || (G == 4 && nt == 512 && minb == 2) ||
+         (G == 8 && nt == 512 && minb == 1) || (G == 4 && nt == 512 && minb == 1);
 }
 
-// shapes (G, threads, CTAs/SM) as listed in k_hough2_has_shape
-cudaError_t launch_hough2(int n_frames, const Params& P, bool wide, int G, int nt, int minb, int n_sm,
+// one launch of the persistent K2 in shape (G, threads, CTAs/SM) with counter width cb
+cudaError_t launch_hough2(int n_frames, const Params& P, bool wide, int G, int nt, int minb, int cb, int n_sm,
                           cudaStream_t st) {
-  const int key = (G << 12) | (nt << 2) | (minb << 1) | (wide ? 1 : 0);
-#define CASE(Gv, NTv, MBv)                                                                    \
-  case (Gv << 12) | (NTv << 2) | (MBv << 1) | 0: return launch2_one<false, Gv, NTv, MBv>(n_frames, P, n_sm, st); \
-  case (Gv << 12) | (NTv << 2) | (MBv << 1) | 1: return launch2_one<true, Gv, NTv, MBv>(n_frames, P, n_sm, st);
+  const int key = (cb << 20) | (G << 12) | (nt << 2) | (minb << 1) | (wide ? 1 : 0);
+#define CASE(CBv, Gv, NTv, MBv)                                                                       \
+  case (CBv << 20) | (Gv << 12) | (NTv << 2) | (MBv << 1) | 0:                                       \
+    return launch2_one<false, Gv, NTv, MBv, CBv>(n_frames, P, n_sm, st);                          \
+  case (CBv << 20) | (Gv << 12) | (NTv << 2) | (MBv << 1) | 1:                                       \
+    return launch2_one<true, Gv, NTv, MBv, CBv>(n_frames, P, n_sm, st);
   switch (key) {
-    CASE(4, 512, 2)
-    CASE(8, 512, 1)
-    CASE(4, 384, 2)
-    CASE(8, 384, 2)
-    CASE(4, 256, 3)
+    CASE(1, 4, 384, 2)
+    CASE(1, 4, 512, 2)
+    CASE(1, 8, 384, 2)
+    CASE(1, 8, 512, 1)
+    CASE(1, 4, 256, 3)
+    CASE(1, 8, 256, 2)
+    CASE(1, 2, 256, 4)
+    CASE(1, 2, 256, 3)
+    CASE(2, 4, 384, 2)
+    CASE(2, 4, 512, 2)
+    CASE(2, 8, 512, 1)
+    CASE(2, 4, 512, 1)
     default: return cudaErrorInvalidValue;
   }
 #undef CASE
+}
+
+cudaError_t launch_redo_reset(int n_frames, const Params& P, cudaStream_t st) {
+  k_redo_reset<<<1, 256, 0, st>>>(P, n_frames);
+  return cudaGetLastError();
 }
 
 }  // namespace rd

@@ -19,9 +19,10 @@ cudaError_t launch_eigen(const double* abc, int64_t n, double* out, int* deg, cu
 size_t k_hough_smem(const Params& P, int G);
 int k_hough_max_entries();
 cudaError_t launch_hough(int n_frames, const Params& P, bool wide, int G, int nt, int minb, cudaStream_t st);
-size_t k_hough2_layout(Params& P, int G, int nt);
-bool k_hough2_has_shape(int G, int nt, int minb);
-cudaError_t launch_hough2(int n_frames, const Params& P, bool wide, int G, int nt, int minb, int n_sm,
+size_t k_hough2_layout(Params& P, int G, int nt, int cb);
+bool k_hough2_has_shape(int cb, int G, int nt, int minb);
+cudaError_t launch_redo_reset(int n_frames, const Params& P, cudaStream_t st);
+cudaError_t launch_hough2(int n_frames, const Params& P, bool wide, int G, int nt, int minb, int cb, int n_sm,
                           cudaStream_t st);
 size_t k_fit_smem(const Params& P);
 cudaError_t launch_fit(int n_frames, const Params& P, void* rings, int* counts, cudaStream_t st);
@@ -51,6 +52,9 @@ struct rd_detector {
   bool wide;
   int G, k2_threads, k2_minb;   // Hough kernel launch shape (levels per step, threads, CTAs/SM)
   int k2_impl;                  // 2: persistent K2 (k_hough2.cu), 1: one CTA per tile (k_hough.cu)
+  int k2_cb;                    // counter bytes of the main persistent pass (1: + 16-bit redo pass)
+  Params P16;                   // redo pass (16-bit counters): its own layout and shape
+  int G16, k2_threads16, k2_minb16;
   int n_sm;
   // device allocations
   void* d_tables = nullptr;
@@ -64,6 +68,7 @@ struct rd_detector {
   void* d_counters = nullptr;  // stats | peak_count | flags | dbg_count
   size_t counters_bytes = 0;
   void* d_dbg = nullptr;
+  void* d_redo_list = nullptr;
   // host-path staging
   int chunk = 0;
   void* d_stage[2] = {nullptr, nullptr};
@@ -119,7 +124,7 @@ rd_status rd_config_init(rd_config* c, int32_t width, int32_t height, int32_t pi
   c->max_rings_per_frame = 1024;
   c->max_ridges_per_tile = 512;
   c->max_entries_per_tile = 2048;
-  c->max_hotspots_per_level = 256;
+  c->max_hotspots_per_level = 160;
   c->debug = 0;
   return RD_OK;
 }
@@ -150,7 +155,7 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   if (!c.max_rings_per_frame) c.max_rings_per_frame = 1024;
   if (!c.max_ridges_per_tile) c.max_ridges_per_tile = 512;
   if (!c.max_entries_per_tile) c.max_entries_per_tile = 2048;
-  if (!c.max_hotspots_per_level) c.max_hotspots_per_level = 256;
+  if (!c.max_hotspots_per_level) c.max_hotspots_per_level = 160;
   if (c.max_ridges_per_tile > T1 * T1) c.max_ridges_per_tile = T1 * T1;
   if (c.max_hotspots_per_level > 4095) return RD_ERR_PARAM;   // 12-bit hotspot index in K2 task lists
   if (c.max_entries_per_tile > k_hough_max_entries()) c.max_entries_per_tile = k_hough_max_entries();
@@ -251,35 +256,59 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   det->k2_impl = 2;
   if (const char* env = getenv("RD_K2_IMPL")) det->k2_impl = atoi(env) == 1 ? 1 : 2;
   if (det->k2_impl == 2) {
-    // persistent K2: (G, threads, CTAs/SM) candidates, T = 64; RD_K2_SHAPE2="G,threads,ctas" first.
-    // Capacities: undo segments of 64*G words per warp, then as many staged rays (>= 256) as fit.
-    std::vector<Shape> sh2 = {{64, 4, 384, 2}, {64, 4, 512, 2}, {64, 8, 512, 1}};
-    if (const char* env = getenv("RD_K2_SHAPE2")) {
-      Shape s{64, 0, 0, 0};
-      if (sscanf(env, "%d,%d,%d", &s.G, &s.nt, &s.minb) == 3 && k_hough2_has_shape(s.G, s.nt, s.minb))
-        sh2.insert(sh2.begin(), s);
-    }
-    for (const Shape& s : sh2) {
-      P.k2t = s.T;
-      const size_t limit = s.minb == 1 ? smax : std::min(smax, sm_sm / s.minb - 1024);
-      const int raws = s.T + 2 * P.hal;
-      if ((int64_t)s.G * raws * (raws + 2) / 2 > 65535) continue;   // undo entries are 16-bit word indices
-      P.k2_tcap = 64 * s.G * (s.nt / 32);   // two full vote iterations per warp and step
-      P.k2_scap = 256;
-      if (k_hough2_layout(P, s.G, s.nt) > limit) continue;
-      while (P.k2_scap < P.entry_cap) {
-        P.k2_scap += 64;
-        if (k_hough2_layout(P, s.G, s.nt) > limit) {
-          P.k2_scap -= 64;
-          break;
-        }
+    // persistent K2, T = 64: the first (G, threads, CTAs/SM) candidate whose layout fits, with
+    // undo segments of 64*G words per warp and as many staged rays (>= 256) as fit.
+    // RD_K2_SHAPE2="G,threads,ctas" puts a shape first; RD_K2_CB=2 forces 16-bit counters.
+    auto pick = [&](Params& Q, int cb, int& G, int& nt, int& minb) {
+      std::vector<Shape> sh = cb == 1 ? std::vector<Shape>{{64, 4, 256, 3}, {64, 4, 384, 2}, {64, 8, 512, 1}}
+                                      : std::vector<Shape>{{64, 4, 384, 2}, {64, 4, 512, 2}, {64, 8, 512, 1},
+                                                           {64, 4, 512, 1}};
+      if (const char* env = getenv("RD_K2_SHAPE2")) {
+        Shape s{64, 0, 0, 0};
+        if (sscanf(env, "%d,%d,%d", &s.G, &s.nt, &s.minb) == 3 && k_hough2_has_shape(cb, s.G, s.nt, s.minb))
+          sh.insert(sh.begin(), s);
       }
-      k_hough2_layout(P, s.G, s.nt);
-      det->G = s.G;
-      det->k2_threads = s.nt;
-      det->k2_minb = s.minb;
-      break;
+      G = 0;
+      for (const Shape& s : sh) {
+        if (!k_hough2_has_shape(cb, s.G, s.nt, s.minb)) continue;
+        Q.k2t = s.T;
+        const size_t limit = s.minb == 1 ? smax : std::min(smax, sm_sm / s.minb - 1024);
+        const int raws = s.T + 2 * Q.hal;
+        if ((int64_t)s.G * raws * (raws + 4) * cb / 4 > 65535) continue;   // undo entries: 16-bit word indices
+        Q.k2_tcap = 64 * s.G * (s.nt / 32);   // two full vote iterations per warp and step
+        Q.k2_scap = 256;
+        if (k_hough2_layout(Q, s.G, s.nt, cb) > limit) continue;
+        while (Q.k2_scap < Q.entry_cap) {
+          Q.k2_scap += 64;
+          if (k_hough2_layout(Q, s.G, s.nt, cb) > limit) {
+            Q.k2_scap -= 64;
+            break;
+          }
+        }
+        Q.k2_scap = std::min(Q.k2_scap, Q.entry_cap);
+        k_hough2_layout(Q, s.G, s.nt, cb);
+        G = s.G;
+        nt = s.nt;
+        minb = s.minb;
+        return;
+      }
+    };
+    det->k2_cb = 1;
+    if (const char* env = getenv("RD_K2_CB")) det->k2_cb = atoi(env) == 2 ? 2 : 1;
+    det->P16 = P;
+    pick(det->P16, 2, det->G16, det->k2_threads16, det->k2_minb16);
+    if (det->k2_cb == 1) pick(P, 1, det->G, det->k2_threads, det->k2_minb);
+    if (det->G == 0 && det->G16 != 0) {   // 16-bit counters as the only pass
+      det->k2_cb = 2;
+      P.k2t = det->P16.k2t;
+      P.k2_tcap = det->P16.k2_tcap;
+      P.k2_scap = det->P16.k2_scap;
+      P.k2o = det->P16.k2o;
+      det->G = det->G16;
+      det->k2_threads = det->k2_threads16;
+      det->k2_minb = det->k2_minb16;
     }
+    if (det->k2_cb == 1 && det->G16 == 0) det->G = 0;   // no 16-bit redo shape: not exact, do not use
   }
   if (det->G == 0) {   // no persistent shape fits (large halo or capacities): one CTA per tile
     det->k2_impl = 1;
@@ -296,9 +325,10 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
     }
   }
   if (getenv("RD_K2_VERBOSE"))
-    fprintf(stderr, "rd: K2 impl %d G %d threads %d ctas/SM %d smem %d scap %d tcap %d\n", det->k2_impl, det->G,
-            det->k2_threads, det->k2_minb, det->k2_impl == 2 ? P.k2o.total : (int)k_hough_smem(P, det->G),
-            P.k2_scap, P.k2_tcap);
+    fprintf(stderr, "rd: K2 impl %d cb %d G %d threads %d ctas/SM %d smem %d scap %d tcap %d | redo G %d threads %d "
+            "ctas/SM %d smem %d scap %d\n", det->k2_impl, det->k2_cb, det->G, det->k2_threads, det->k2_minb,
+            det->k2_impl == 2 ? P.k2o.total : (int)k_hough_smem(P, det->G), P.k2_scap, P.k2_tcap, det->G16,
+            det->k2_threads16, det->k2_minb16, det->P16.k2o.total, det->P16.k2_scap);
   P.ntx = (c.width + P.k2t - 1) / P.k2t;
   P.nty = (c.height + P.k2t - 1) / P.k2t;
   if (k_ridges_smem(P.Ks) > smax || det->G == 0 || k_fit_smem(P) > smax) {
@@ -324,7 +354,7 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   ALLOC(det->d_ray_d, sizeof(double2) * B * ntl * P.entry_cap);
   ALLOC(det->d_ray_xy, sizeof(uint32_t) * B * ntl * P.entry_cap);
   ALLOC(det->d_ray_r, sizeof(uint32_t) * B * ntl * P.entry_cap);
-  det->counters_bytes = sizeof(Stats) * B + sizeof(int) * 3 * B + sizeof(int) * B * ntl + 16;
+  det->counters_bytes = sizeof(Stats) * B + sizeof(int) * 3 * B + sizeof(int) * B * ntl + 16 + sizeof(int) * B;
   ALLOC(det->d_counters, det->counters_bytes);
   if (c.debug) ALLOC(det->d_dbg, sizeof(HotRec) * B * P.dbg_cap);
   // tables
@@ -355,11 +385,25 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   P.dbg_count = P.flags + B;
   P.ray_count = P.dbg_count + B;
   P.k2_work = P.ray_count + B * ntl;
+  P.redo = P.k2_work + 4;
+  P.redo_list = nullptr;
+  P.force_redo = getenv("RD_K2_FORCE_REDO") ? 1 : 0;
   P.ray_d = (double2*)det->d_ray_d;
   P.ray_xy = (uint32_t*)det->d_ray_xy;
   P.ray_r = (uint32_t*)det->d_ray_r;
   P.dbg_hot = (HotRec*)det->d_dbg;
   det->P = P;
+  {   // the redo pass: same buffers, its own layout, shape and the redo list
+    Params Q = P;
+    Q.k2t = det->P16.k2t;
+    Q.k2_tcap = det->P16.k2_tcap;
+    Q.k2_scap = det->P16.k2_scap;
+    Q.k2o = det->P16.k2o;
+    e = cudaMalloc(&det->d_redo_list, sizeof(int) * (B + 1));
+    if (e != cudaSuccess) { rd_destroy(det); return cuda_fail(e, "cudaMalloc redo_list"); }
+    Q.redo_list = (int*)det->d_redo_list;
+    det->P16 = Q;
+  }
   e = cudaEventCreateWithFlags(&det->ev_last, cudaEventDisableTiming);
   if (e != cudaSuccess) { rd_destroy(det); return cuda_fail(e, "cudaEventCreate"); }
   *out = det;
@@ -379,6 +423,7 @@ rd_status rd_destroy(rd_detector* det) {
   cudaFree(det->d_ray_r);
   cudaFree(det->d_counters);
   cudaFree(det->d_dbg);
+  cudaFree(det->d_redo_list);
   cudaFree(det->d_prof);
   for (int i = 0; i < 2; ++i) {
     cudaFree(det->d_stage[i]);
@@ -421,9 +466,13 @@ static rd_status detect_impl(rd_detector* det, const void* d_frames, int64_t pit
   if (ev) CK(cudaEventRecord(ev[1], st));
   CK(launch_rays(n, P, st));
   if (ev) CK(cudaEventRecord(ev[2], st));
-  if (det->k2_impl == 2)
-    CK(launch_hough2(n, P, det->wide, det->G, det->k2_threads, det->k2_minb, det->n_sm, st));
-  else
+  if (det->k2_impl == 2) {
+    CK(launch_hough2(n, P, det->wide, det->G, det->k2_threads, det->k2_minb, det->k2_cb, det->n_sm, st));
+    if (det->k2_cb == 1) {   // frames whose byte counters overflowed: recomputed with 16-bit counters
+      CK(launch_redo_reset(n, det->P16, st));
+      CK(launch_hough2(n, det->P16, det->wide, det->G16, det->k2_threads16, det->k2_minb16, 2, det->n_sm, st));
+    }
+  } else
     CK(launch_hough(n, P, det->wide, det->G, det->k2_threads, det->k2_minb, st));
   if (ev) CK(cudaEventRecord(ev[3], st));
   CK(launch_fit(n, P, d_rings, d_counts, st));

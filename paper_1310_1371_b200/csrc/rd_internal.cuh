@@ -31,8 +31,8 @@ struct Stats {         // per-frame counters (same layout as rd_frame_stats)
 
 // Shared-memory layout of the persistent Hough kernel (byte offsets; host-computed)
 struct K2Layout {
-  int raws, rawp, lvlc, tseg;
-  int raw, hS, sd, hcell, hraw, task, cand, cdef, touch, act, sxy, srr, hcnt, w, k, tn, total;
+  int cb, raws, rawp, lvlc, tseg;   // counter bytes, raw side, row pitch (cells), cells per level, undo words/warp
+  int raw, hS, sd, rr, hcell, hraw, task, cand, cdef, touch, act, sxy, srr, hcnt, w, k, tn, total;
 };
 
 // Everything the kernels need, passed by value (< 4 KB).
@@ -66,7 +66,10 @@ struct Params {
   double2* ray_d;               // [F][tiles][entry_cap] (s*dx, s*dy)
   uint32_t* ray_xy;             // [F][tiles][entry_cap] x | y<<16
   uint32_t* ray_r;              // [F][tiles][entry_cap] ra | rb<<16 (level indices)
-  int* k2_work;                 // persistent K2: next (frame, tile) work item (zeroed per call)
+  int* k2_work;                 // persistent K2: next work item [0] main pass, [1] redo pass (zeroed per call)
+  int* redo;                    // [F] frames whose byte counters overflowed (zeroed per call)
+  int* redo_list;               // redo pass only: [0] count, [1..] frames; null in the main pass
+  int force_redo;               // test knob (RD_K2_FORCE_REDO): every frame takes the 16-bit redo pass
   int k2_tcap;                  // K2 undo-list capacity (32-bit words per step, all warps)
   int k2_scap;                  // K2 staged active rays per step
   K2Layout k2o;
