@@ -8,20 +8,18 @@
 // + (K_max+1) halo and the hotspot lists of the last G + 2 levels (the paper's rolling
 // level window).  A step has three phases separated by CTA barriers:
 //   (1) votes: one thread per active ray (ridge pixel x sense of rho, routed to this tile
-//       by K1.5, staged in shared memory during the previous step) casts its votes for the
-//       G levels of the step; the atomic that lifts a counter past T_raw registers the
-//       hotspot; the atomic that finds a zero 32-bit word appends the
-//       word to its warp's undo segment;
-//   (2) the rays of the next step are selected and their staging copies issued
-//       (cp.async); S at each hotspot — one warp (K > 7) or half-warp
-//       (K <= 7) per hotspot, lanes over window rows — and the candidate test
-//       S > T_norm(r) in the same pass;
-//   (3) undo: each warp resets the words of its undo segment (the paper's register-and-
-//       undo; a bulk clear of the level buffers if a segment overflowed),
-//       and 3x3x3 peak extraction of the levels whose upper neighbour is complete
-//       (PAPER.md:967-972), one warp per candidate.
+//       by K1.5; the tile's rays are resident in shared memory) casts its votes for the G
+//       levels of the step; the atomic that lifts a counter past T_raw registers the
+//       hotspot;
+//   (2) the rays active in the next step are listed; S at each hotspot
+//       — one warp (K > 7) or half-warp (K <= 7) per hotspot, lanes over window rows — and
+//       the candidate test S > T_norm(r) in the same pass;
+//   (3) the step's level buffers are cleared (16-byte stores; the paper resets the cells it
+//       registered, PAPER.md:426-434 — with byte counters a whole-buffer clear costs fewer
+//       instructions than tracking the touched words), and 3x3x3 peak extraction of the
+//       levels whose upper neighbour is complete, one warp per candidate.
 // Byte counters (CB = 1) are exact while no counter passes 255: the atomic that finds 255
-// marks the frame, whose K2 results are then discarded and recomputed by the CB = 2
+// (P.u8_limit; lower only in tests) marks the frame, whose K2 results are then discarded and recomputed by the CB = 2
 // instance (k_redo_reset + the redo list), so results never depend on the counter width.
 // The shared-memory layout is computed on the host (Params::k2o, constant bank).  Only
 // peak records (and optional debug hotspots) leave the SM.
@@ -44,14 +42,10 @@ __device__ __forceinline__ int round_half_away_i(double v) {
   return __double2int_rz(__dadd_rz(v, copysign(0.5, v)));
 }
 
-// predicated shared-memory atomic add: returns the old word, or 1 if !pred
-__device__ __forceinline__ uint32_t atom_add_shared_if(uint32_t saddr, uint32_t v, uint32_t pred) {
-  uint32_t old = 1u;
-  asm volatile(
-      "{\n .reg .pred q;\n setp.ne.u32 q, %3, 0;\n @q atom.shared.add.u32 %0, [%1], %2;\n}"
-      : "+r"(old)
-      : "r"(saddr), "r"(v), "r"(pred)
-      : "memory");
+// shared-memory atomic add on a 32-bit shared address: returns the old word
+__device__ __forceinline__ uint32_t atom_add_shared(uint32_t saddr, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(saddr), "r"(v) : "memory");
   return old;
 }
 
@@ -72,10 +66,11 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 }  // namespace
 
 // Host: the K2 shared-memory layout for (G, threads, counter bytes) with the capacities in
-// P (hot_cap, entry_cap, k2_tcap, k2_scap); returns the bytes.
+// P (hot_cap, entry_cap, k2_rcap); returns the bytes.
 size_t k_hough2_layout(Params& P, int G, int nt, int cb) {
   K2Layout& L = P.k2o;
-  const int NSLOT = G + 2, NW = nt / 32;
+  const int NSLOT = G + 2;
+  (void)nt;
   const int T = P.k2t, hot_cap = P.hot_cap, nlev = P.n_levels;
   L.cb = cb;
   L.raws = T + 2 * P.hal;
@@ -84,26 +79,25 @@ size_t k_hough2_layout(Params& P, int G, int nt, int cb) {
   L.rawp = ((L.raws + cpw - 1) / cpw) | 1;
   L.rawp *= cpw;
   L.lvlc = (L.raws * L.rawp + 15) & ~15;   // 16-byte aligned level buffers (bulk clears)
-  L.tseg = std::max(P.k2_tcap / NW, 32) & ~7;
   size_t o = 0;
   L.raw = o;   o = al16(o + (size_t)cb * G * L.lvlc);
   L.hS = o;    o = al16(o + 8 * (size_t)NSLOT * hot_cap);
-  L.sd = o;    o = al16(o + 16 * (size_t)P.k2_scap);
-  L.rr = o;    o = al16(o + 4 * (size_t)P.entry_cap);
-  L.sxy = o;   o = al16(o + 4 * (size_t)P.k2_scap);
-  L.srr = o;   o = al16(o + 4 * (size_t)P.k2_scap);
+  L.sd = o;    o = al16(o + 16 * (size_t)P.k2_rcap);
+  L.rr = o;    o = al16(o + 4 * (size_t)P.k2_rcap);
+  L.xy = o;    o = al16(o + 4 * (size_t)P.k2_rcap);
   L.hcell = o; o = al16(o + 2 * (size_t)NSLOT * hot_cap);
   L.hraw = o;  o = al16(o + 2 * (size_t)NSLOT * hot_cap);
   L.task = o;  o = al16(o + 2 * (size_t)G * hot_cap);
   L.cand = o;  o = al16(o + 2 * (size_t)G * hot_cap);
   L.cdef = o;  o = al16(o + 2 * 2 * (size_t)hot_cap);
-  L.touch = o; o = al16(o + 2 * (size_t)L.tseg * NW);
-  L.act = o;   o = al16(o + 2 * (size_t)P.entry_cap);
+  L.act = o;   o = al16(o + 2 * 2 * (size_t)P.entry_cap);
   L.hcnt = o;  o = al16(o + 4 * (size_t)(nlev + 32));
   L.w = o;     o = al16(o + 2 * (size_t)nlev * P.wstride);
   L.k = o;     o = al16(o + 4 * (size_t)nlev);
   L.tn = o;    o = al16(o + 8 * (size_t)nlev);
+  L.dummy = o; o = al16(o + 4 * 32);
   L.total = (int)o;
+  L.rawp_magic = (uint32_t)((1ull << 32) / (uint64_t)L.rawp + 1);
   return o;
 }
 
@@ -121,21 +115,20 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
   uint32_t* raw32 = SM(uint32_t, raw);          // [G] levels of packed counters
   cell_t* rawc = SM(cell_t, raw);
   unsigned long long* hS = SM(unsigned long long, hS);   // [NSLOT][hot_cap] S
-  double2* sd = SM(double2, sd);                // [scap] staged (s*dx, s*dy)
-  uint32_t* rr_s = SM(uint32_t, rr);            // [entry_cap] level interval ra | rb<<16 of every ray
-  uint32_t* sxy = SM(uint32_t, sxy);            // [scap] staged x | y<<16 (frame coordinates)
-  uint32_t* srr = SM(uint32_t, srr);            // [scap] staged level interval
+  double2* sd = SM(double2, sd);                // [rcap] the tile's rays: (s*dx, s*dy)
+  uint32_t* rr_s = SM(uint32_t, rr);            // [rcap] level interval ra | rb<<16
+  uint32_t* sxy = SM(uint32_t, xy);             // [rcap] x | y<<16 (frame coordinates)
   uint16_t* hcell = SM(uint16_t, hcell);        // [NSLOT][hot_cap] iy<<8 | ix (ring coordinates)
   uint16_t* hraw = SM(uint16_t, hraw);          // [NSLOT][hot_cap] raw count
   uint16_t* tasks = SM(uint16_t, task);         // [G*hot_cap] g<<12 | h (small K front, large K back)
   uint16_t* cand = SM(uint16_t, cand);          // [G*hot_cap] g<<12 | h
   uint16_t* cdef = SM(uint16_t, cdef);          // [2][hot_cap] h, top level of a step
-  uint16_t* touch = SM(uint16_t, touch);        // [NW][tseg] raw32 word indices
-  uint16_t* act = SM(uint16_t, act);            // [entry_cap] active rays beyond the staging
+  uint16_t* act = SM(uint16_t, act);            // [2][entry_cap] rays active in the step, by parity
   int* hcnt = SM(int, hcnt);                    // [nlev] hotspots per level + counters
   uint16_t* tW = SM(uint16_t, w);               // [nlev][wstride] w_r(d)
   int* tK = SM(int, k);                         // [nlev] K_r
   double* tTn = SM(double, tn);                 // [nlev] T_norm(r)
+  uint32_t* dummy_w = SM(uint32_t, dummy);      // [32] targets of masked-out votes (+0)
 #undef SM
   const int nlev = P.n_levels;
   int* cnt = hcnt + nlev;
@@ -144,13 +137,12 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
   int* s_ntask = cnt + 4;   // [2] small-K tasks from the front, large-K from the back
   int* s_ncand = cnt + 6;
   int* s_ndef = cnt + 8;    // [2] by step parity
-  int* s_bulk = cnt + 10;   // [2] by step parity: an undo segment overflowed
   int* s_item = cnt + 12;
   int* s_ovf = cnt + 13;    // a byte counter passed 255
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int T = P.k2t, hal = P.hal, hot_cap = P.hot_cap;
-  const int rawp = P.k2o.rawp, lvlc = P.k2o.lvlc, tseg = P.k2o.tseg, scap = P.k2_scap;
+  const int rawp = P.k2o.rawp, lvlc = P.k2o.lvlc, rcap = P.k2_rcap, ecap = P.entry_cap;
   const int ntiles = P.ntx * P.nty;
   const uint32_t T_raw = (uint32_t)P.T_raw;
   // CB = 2 is also the redo pass: work items are then the tiles of the frames in the redo list
@@ -159,12 +151,16 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
 
   unsigned long long t_acc[6] = {0, 0, 0, 0, 0, 0};
   long long t_last = clock64();
+#ifdef RD_K2_PROF   // per-phase cycle accounting (rd_phase_cycles); compiled in on request only
 #define PMARK(i)                                      \
   if (P.prof && tid == 0) {                           \
     const long long t_ = clock64();                   \
     t_acc[i] += (unsigned long long)(t_ - t_last);    \
     t_last = t_;                                      \
   }
+#else
+#define PMARK(i)
+#endif
 
   // once per CTA: level tables, zeroed counters and raw levels (the undo keeps them zero)
   for (int i = tid; i < nlev * P.wstride; i += NT) tW[i] = (uint16_t)P.lvlW[i];
@@ -176,7 +172,10 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
     uint4* r4 = reinterpret_cast<uint4*>(raw32);
     for (int i = tid; i < (CB * G * lvlc) / 16; i += NT) r4[i] = make_uint4(0, 0, 0, 0);
   }
-  for (int i = tid; i < 32; i += NT) cnt[i] = 0;
+  for (int i = tid; i < 32; i += NT) {
+    cnt[i] = 0;
+    dummy_w[i] = 0;
+  }
   __syncthreads();
 
   for (;;) {
@@ -195,34 +194,30 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
     const int64_t gbase = tl * P.entry_cap;
     int my_votes = 0, my_hot = 0;
 
-    // select the rays active in the step starting at level L0s (count: s_nact[p]) and issue
-    // the asynchronous copies that stage them; the caller waits (cp.async.wait_all)
+    // list the rays active in the step starting at level L0s (count: s_nact[p])
     auto setup = [&](int L0s, int p) {
       const int Lhs = min(L0s + G - 1, nlev - 1);
       for (int e0 = warp * 32; e0 < ne; e0 += NT) {
         const int e = e0 + lane;
-        const uint32_t rr = e < ne ? rr_s[e] : 0xFFFFu;
+        const uint32_t rr = e < ne ? (e < rcap ? rr_s[e] : __ldg(P.ray_r + gbase + e)) : 0xFFFFu;
         const bool a = (int)(rr & 0xFFFFu) <= Lhs && (int)(rr >> 16) >= L0s;
         const unsigned bal = __ballot_sync(FULL, a);
         if (!bal) continue;
         int base = 0;
         if (lane == 0) base = atomicAdd(&s_nact[p], __popc(bal));
         base = __shfl_sync(FULL, base, 0);
-        if (!a) continue;
-        const int k = base + __popc(bal & lanemask_lt());
-        if (k < scap) {
-          cp_async16(&sd[k], P.ray_d + gbase + e);
-          cp_async4(&sxy[k], P.ray_xy + gbase + e);
-          srr[k] = rr;
-        } else {
-          act[k] = (uint16_t)e;
-        }
+        if (a) act[p * ecap + base + __popc(bal & lanemask_lt())] = (uint16_t)e;
       }
     };
-    for (int e = tid; e < ne; e += NT) rr_s[e] = __ldg(P.ray_r + gbase + e);
+    // the tile's rays (up to rcap) become resident in shared memory
+    for (int e = tid; e < min(ne, rcap); e += NT) {
+      cp_async16(&sd[e], P.ray_d + gbase + e);
+      cp_async4(&sxy[e], P.ray_xy + gbase + e);
+      cp_async4(&rr_s[e], P.ray_r + gbase + e);
+    }
+    cp_async_wait_all();
     __syncthreads();
     setup(0, 0);
-    cp_async_wait_all();
     PMARK(0);
 
     for (int L0 = 0, step = 0; L0 < nlev; L0 += G, ++step) {
@@ -234,37 +229,39 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
         s_nact[par ^ 1] = 0;
         s_ncand[0] = 0;
         s_ndef[par] = 0;
-        s_bulk[par ^ 1] = 0;
       }
       // ---------------- (1) votes of levels L0..Lhi
-      int tw = 0;   // words in this warp's undo segment (warp-uniform)
       {
         const int nact = s_nact[par];
         const double rb0 = (double)(P.r_lo + L0);
-        uint16_t* seg = touch + warp * tseg;
+        int slot_of[G];   // hotspot-list slot of each level of the step
+#pragma unroll
+        for (int g = 0; g < G; ++g) slot_of[g] = (L0 + g) % NSLOT;
         const uint32_t raw_base = smem_u32(raw32);
+        const uint32_t dummy = smem_u32(dummy_w) + 4u * lane;   // masked votes add 0 to a private word
         const int bx0 = max(0, -RX0), bxs = min(P.k2o.raws - 1, P.W - 1 - RX0) - bx0;
         const int by0 = max(0, -RY0), bys = min(P.k2o.raws - 1, P.H - 1 - RY0) - by0;
         bool ovf = false;
         for (int i0 = warp * 32; i0 < nact; i0 += NT) {
           const int i = i0 + lane;
-          int ga = G, gb = -1, xr = 0, yr = 0;
+          unsigned lm = 0;   // levels of the step inside the ray's interval
+          int xr = 0, yr = 0;
           double dx = 0.0, dy = 0.0;
           if (i < nact) {
             uint32_t rr, xy;
             double2 d;
-            if (i < scap) {
-              d = sd[i];
-              xy = sxy[i];
-              rr = srr[i];
-            } else {
-              const int e = act[i];
+            const int e = act[par * ecap + i];
+            if (e < rcap) {
+              d = sd[e];
+              xy = sxy[e];
+              rr = rr_s[e];
+            } else {   // beyond the resident capacity: from global memory
               xy = __ldg(P.ray_xy + gbase + e);
               d = __ldg(P.ray_d + gbase + e);
-              rr = rr_s[e];
+              rr = __ldg(P.ray_r + gbase + e);
             }
-            ga = max((int)(rr & 0xFFFFu) - L0, 0);
-            gb = min((int)(rr >> 16) - L0, G - 1);
+            const int ga = max((int)(rr & 0xFFFFu) - L0, 0), gb = min((int)(rr >> 16) - L0, G - 1);
+            lm = gb >= ga ? (2u << gb) - (1u << ga) : 0u;
             dx = d.x;
             dy = d.y;
             xr = (int)(xy & 0xFFFFu) - RX0;
@@ -272,45 +269,38 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
           }
           // targets of the G levels, branch-free: a vote counts if its level is in the ray's
           // interval and its cell lies in the raw buffer and in the frame (cells outside a
-          // level's box, tile + K_r + 1, are never read by that level's windows; undo clears them)
-          int cell[G], hc[G];
-          uint32_t old[G];
-          unsigned okm = 0, ringm = 0;
+          // level's box, tile + K_r + 1, are never read by that level's windows; the clear
+          // resets them)
+          uint32_t addr[G], sh[G], old[G];
+          unsigned okm = 0;
 #pragma unroll
           for (int g = 0; g < G; ++g) {
             const double rd = rb0 + (double)g;
             const int cx = xr + round_half_away_i(__dmul_rn(rd, dx));
             const int cy = yr + round_half_away_i(__dmul_rn(rd, dy));
-            const bool ok = (g >= ga) & (g <= gb) & ((unsigned)(cx - bx0) <= (unsigned)bxs) &
+            const bool ok = ((lm >> g) & 1u) & ((unsigned)(cx - bx0) <= (unsigned)bxs) &
                             ((unsigned)(cy - by0) <= (unsigned)bys);
-            cell[g] = g * lvlc + cy * rawp + cx;
-            const int ix = cx - (hal - 1), iy = cy - (hal - 1);
-            hc[g] = (iy << 8) | ix;
+            const int cell = cy * rawp + cx;
+            sh[g] = (uint32_t)(cell & ((1 << CSH) - 1)) * BITS;
+            addr[g] = ok ? raw_base + (uint32_t)(g * lvlc * CB) + 4u * (uint32_t)(cell >> CSH) : dummy;
             okm |= (unsigned)ok << g;
-            ringm |= (unsigned)(ok & ((unsigned)ix < (unsigned)(T + 2)) & ((unsigned)iy < (unsigned)(T + 2))) << g;
-            my_votes += ok & ((unsigned)(ix - 1) < (unsigned)T) & ((unsigned)(iy - 1) < (unsigned)T);
+            my_votes += ok & ((unsigned)(cx - hal) < (unsigned)T) & ((unsigned)(cy - hal) < (unsigned)T);
           }
 #pragma unroll
-          for (int g = 0; g < G; ++g)
-            old[g] = atom_add_shared_if(raw_base + 4u * (uint32_t)(cell[g] >> CSH),
-                                        1u << ((cell[g] & ((1 << CSH) - 1)) * BITS), (okm >> g) & 1u);
+          for (int g = 0; g < G; ++g) old[g] = atom_add_shared(addr[g], ((okm >> g) & 1u) << sh[g]);
 #pragma unroll
           for (int g = 0; g < G; ++g) {
-            const bool first = old[g] == 0u;   // this vote found its 32-bit word zero: undo entry
-            const unsigned bal = __ballot_sync(FULL, first);
-            const int k = tw + __popc(bal & lanemask_lt());
-            if (first && k < tseg) seg[k] = (uint16_t)(cell[g] >> CSH);
-            tw += __popc(bal);
-          }
-#pragma unroll
-          for (int g = 0; g < G; ++g) {
-            const uint32_t oc = (old[g] >> ((cell[g] & ((1 << CSH) - 1)) * BITS)) & CMASK;
-            if (CB == 1) ovf |= ((okm >> g) & 1u) && oc == CMASK;
-            if (((ringm >> g) & 1u) && oc == T_raw) {   // rare: this vote lifted the counter past T_raw
+            const uint32_t oc = (old[g] >> sh[g]) & CMASK;
+            if (CB == 1) ovf |= ((okm >> g) & 1u) & (oc >= (uint32_t)P.u8_limit);
+            if (((okm >> g) & 1u) && oc == T_raw) {   // this vote lifted the counter past T_raw
+              const int cell = (int)(((addr[g] - raw_base - (uint32_t)(g * lvlc * CB)) >> 2) << CSH) + (int)(sh[g] / BITS);
+              const int cy = (int)__umulhi((uint32_t)cell, P.k2o.rawp_magic), cx = cell - cy * rawp;
+              const int ix = cx - (hal - 1), iy = cy - (hal - 1);
+              if ((unsigned)ix >= (unsigned)(T + 2) || (unsigned)iy >= (unsigned)(T + 2)) continue;   // not in the ring
               const int li = L0 + g;
               const int h = atomicAdd(&hcnt[li], 1);
               if (h < hot_cap) {
-                hcell[(li % NSLOT) * hot_cap + h] = (uint16_t)hc[g];
+                hcell[slot_of[g] * hot_cap + h] = (uint16_t)((iy << 8) | ix);
                 const int slot = tK[li] <= SMALL_K ? atomicAdd(&s_ntask[0], 1)
                                                    : G * hot_cap - 1 - atomicAdd(&s_ntask[1], 1);
                 tasks[slot] = (uint16_t)((g << 12) | h);
@@ -320,7 +310,6 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
             }
           }
         }
-        if (tw > tseg && lane == 0) s_bulk[par] = 1;
         if (CB == 1 && __any_sync(FULL, ovf) && lane == 0) *s_ovf = 1;
       }
       __syncthreads();
@@ -329,7 +318,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
       //     each hotspot and the candidate test
       {
         if (L0 + G < nlev) setup(L0 + G, par ^ 1);
-        const int nsmall = s_ntask[0], nlarge = s_ntask[1];
+        const int nsmall = (P.ablate & 4) ? 0 : s_ntask[0], nlarge = (P.ablate & 4) ? 0 : s_ntask[1];
         const int half = lane >> 4;
         // small-K hotspots: a half-warp each; large-K: a warp each (lanes over window rows)
         const int nsp = (nsmall + 1) >> 1;
@@ -353,7 +342,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
           const cell_t* ctr = rawc + g * lvlc + (iy - 1 + hal) * rawp + (ix - 1 + hal);   // the hotspot's cell
           const int sub = small ? (lane & 15) : lane;
           unsigned long long acc = 0;
-          if (valid && sub <= 2 * K) {
+          if (valid && sub <= 2 * K && !(P.ablate & 1)) {
             const int row = sub;   // 2K+1 <= 31 rows (K <= 15), one per lane
             const cell_t* rowp = ctr + (row - K) * rawp;
             if (kWide) {
@@ -417,24 +406,27 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
             }
           }
         }
-        cp_async_wait_all();
       }
       __syncthreads();
       PMARK(3);
       // ---------------- (3) undo the step's counters, then peaks of levels L0-1 .. Lhi-1
       {
-        if (!s_bulk[par]) {
-          const uint16_t* seg = touch + warp * tseg;
-          for (int k = lane; k < tw; k += 32) raw32[seg[k]] = 0u;
-        } else {   // an undo segment overflowed: clear the step's level buffers
+        {   // clear the step's level buffers
           uint4* r4 = reinterpret_cast<uint4*>(raw32);
-          for (int i = tid; i < (CB * G * lvlc) / 16; i += NT) r4[i] = make_uint4(0u, 0u, 0u, 0u);
+          constexpr int U = 4;
+          const int n16 = (CB * G * lvlc) / 16;
+          int i = tid;
+          for (; i + (U - 1) * NT < n16; i += U * NT) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) r4[i + u * NT] = make_uint4(0u, 0u, 0u, 0u);
+          }
+          for (; i < n16; i += NT) r4[i] = make_uint4(0u, 0u, 0u, 0u);
         }
         if (tid == 0) {
           s_ntask[0] = 0;
           s_ntask[1] = 0;
         }
-        const int nd = L0 > 0 ? s_ndef[par ^ 1] : 0, nc = s_ncand[0];
+        const int nd = (L0 > 0 && !(P.ablate & 2)) ? s_ndef[par ^ 1] : 0, nc = (P.ablate & 2) ? 0 : s_ncand[0];
         for (int p = warp; p < nd + nc; p += NW) {
           int lc, h;
           if (p < nd) {

@@ -256,8 +256,8 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   det->k2_impl = 2;
   if (const char* env = getenv("RD_K2_IMPL")) det->k2_impl = atoi(env) == 1 ? 1 : 2;
   if (det->k2_impl == 2) {
-    // persistent K2, T = 64: the first (G, threads, CTAs/SM) candidate whose layout fits, with
-    // undo segments of 64*G words per warp and as many staged rays (>= 256) as fit.
+    // persistent K2, T = 64: the first (G, threads, CTAs/SM) candidate whose layout fits with at
+    // least 256 resident rays per tile, then as many resident rays as fit (up to entry_cap).
     // RD_K2_SHAPE2="G,threads,ctas" puts a shape first; RD_K2_CB=2 forces 16-bit counters.
     auto pick = [&](Params& Q, int cb, int& G, int& nt, int& minb) {
       std::vector<Shape> sh = cb == 1 ? std::vector<Shape>{{64, 4, 256, 3}, {64, 4, 384, 2}, {64, 8, 512, 1}}
@@ -274,18 +274,16 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
         Q.k2t = s.T;
         const size_t limit = s.minb == 1 ? smax : std::min(smax, sm_sm / s.minb - 1024);
         const int raws = s.T + 2 * Q.hal;
-        if ((int64_t)s.G * raws * (raws + 4) * cb / 4 > 65535) continue;   // undo entries: 16-bit word indices
-        Q.k2_tcap = 64 * s.G * (s.nt / 32);   // two full vote iterations per warp and step
-        Q.k2_scap = 256;
+        Q.k2_rcap = 256;
         if (k_hough2_layout(Q, s.G, s.nt, cb) > limit) continue;
-        while (Q.k2_scap < Q.entry_cap) {
-          Q.k2_scap += 64;
+        while (Q.k2_rcap < Q.entry_cap) {   // as many resident rays as fit
+          Q.k2_rcap += 64;
           if (k_hough2_layout(Q, s.G, s.nt, cb) > limit) {
-            Q.k2_scap -= 64;
+            Q.k2_rcap -= 64;
             break;
           }
         }
-        Q.k2_scap = std::min(Q.k2_scap, Q.entry_cap);
+        Q.k2_rcap = std::min(Q.k2_rcap, Q.entry_cap);
         k_hough2_layout(Q, s.G, s.nt, cb);
         G = s.G;
         nt = s.nt;
@@ -301,8 +299,7 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
     if (det->G == 0 && det->G16 != 0) {   // 16-bit counters as the only pass
       det->k2_cb = 2;
       P.k2t = det->P16.k2t;
-      P.k2_tcap = det->P16.k2_tcap;
-      P.k2_scap = det->P16.k2_scap;
+      P.k2_rcap = det->P16.k2_rcap;
       P.k2o = det->P16.k2o;
       det->G = det->G16;
       det->k2_threads = det->k2_threads16;
@@ -325,10 +322,10 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
     }
   }
   if (getenv("RD_K2_VERBOSE"))
-    fprintf(stderr, "rd: K2 impl %d cb %d G %d threads %d ctas/SM %d smem %d scap %d tcap %d | redo G %d threads %d "
-            "ctas/SM %d smem %d scap %d\n", det->k2_impl, det->k2_cb, det->G, det->k2_threads, det->k2_minb,
-            det->k2_impl == 2 ? P.k2o.total : (int)k_hough_smem(P, det->G), P.k2_scap, P.k2_tcap, det->G16,
-            det->k2_threads16, det->k2_minb16, det->P16.k2o.total, det->P16.k2_scap);
+    fprintf(stderr, "rd: K2 impl %d cb %d G %d threads %d ctas/SM %d smem %d rcap %d | redo G %d threads %d "
+            "ctas/SM %d smem %d rcap %d\n", det->k2_impl, det->k2_cb, det->G, det->k2_threads, det->k2_minb,
+            det->k2_impl == 2 ? P.k2o.total : (int)k_hough_smem(P, det->G), P.k2_rcap, det->G16,
+            det->k2_threads16, det->k2_minb16, det->P16.k2o.total, det->P16.k2_rcap);
   P.ntx = (c.width + P.k2t - 1) / P.k2t;
   P.nty = (c.height + P.k2t - 1) / P.k2t;
   if (k_ridges_smem(P.Ks) > smax || det->G == 0 || k_fit_smem(P) > smax) {
@@ -388,6 +385,9 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   P.redo = P.k2_work + 4;
   P.redo_list = nullptr;
   P.force_redo = getenv("RD_K2_FORCE_REDO") ? 1 : 0;
+  P.u8_limit = 255;
+  P.ablate = getenv("RD_K2_ABLATE") ? atoi(getenv("RD_K2_ABLATE")) : 0;
+  if (const char* env = getenv("RD_K2_U8_LIMIT")) P.u8_limit = std::max(1, std::min(255, atoi(env)));
   P.ray_d = (double2*)det->d_ray_d;
   P.ray_xy = (uint32_t*)det->d_ray_xy;
   P.ray_r = (uint32_t*)det->d_ray_r;
@@ -396,8 +396,7 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   {   // the redo pass: same buffers, its own layout, shape and the redo list
     Params Q = P;
     Q.k2t = det->P16.k2t;
-    Q.k2_tcap = det->P16.k2_tcap;
-    Q.k2_scap = det->P16.k2_scap;
+    Q.k2_rcap = det->P16.k2_rcap;
     Q.k2o = det->P16.k2o;
     e = cudaMalloc(&det->d_redo_list, sizeof(int) * (B + 1));
     if (e != cudaSuccess) { rd_destroy(det); return cuda_fail(e, "cudaMalloc redo_list"); }

@@ -31,8 +31,9 @@ struct Stats {         // per-frame counters (same layout as rd_frame_stats)
 
 // Shared-memory layout of the persistent Hough kernel (byte offsets; host-computed)
 struct K2Layout {
-  int cb, raws, rawp, lvlc, tseg;   // counter bytes, raw side, row pitch (cells), cells per level, undo words/warp
-  int raw, hS, sd, rr, hcell, hraw, task, cand, cdef, touch, act, sxy, srr, hcnt, w, k, tn, total;
+  int cb, raws, rawp, lvlc;   // counter bytes, raw side, row pitch (cells), cells per level
+  int raw, hS, sd, rr, xy, hcell, hraw, task, cand, cdef, act, hcnt, w, k, tn, dummy, total;
+  uint32_t rawp_magic;        // ceil(2^32 / rawp): cell / rawp = umulhi(cell, magic) for cells < 2^16
 };
 
 // Everything the kernels need, passed by value (< 4 KB).
@@ -70,8 +71,9 @@ struct Params {
   int* redo;                    // [F] frames whose byte counters overflowed (zeroed per call)
   int* redo_list;               // redo pass only: [0] count, [1..] frames; null in the main pass
   int force_redo;               // test knob (RD_K2_FORCE_REDO): every frame takes the 16-bit redo pass
-  int k2_tcap;                  // K2 undo-list capacity (32-bit words per step, all warps)
-  int k2_scap;                  // K2 staged active rays per step
+  int ablate;                   // timing experiments only (RD_K2_ABLATE bits: 1 no window sums, 2 no NMS, 4 no S tasks)
+  int u8_limit;                 // byte-counter value that triggers the redo (255; RD_K2_U8_LIMIT in tests)
+  int k2_rcap;                  // K2: rays of a tile resident in shared memory (the rest read from global)
   K2Layout k2o;
   int ring_cap;
   Peak* peaks;                  // [F][ring_cap]

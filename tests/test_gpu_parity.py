@@ -286,3 +286,19 @@ def test_detect_host_pitched_frames(rdmod):
     p = oracle.params(**params)
     for i in range(5):
         _compare_rings(hr[i, : hc[i]], oracle.detect(p, frames[i])[0])
+
+
+# ---------------------------------------------------------------- K2 counter width
+@pytest.mark.parametrize("knob", [("RD_K2_FORCE_REDO", "1"), ("RD_K2_U8_LIMIT", "170"), ("RD_K2_CB", "2")])
+def test_k2_counter_width_paths_bit_exact(rdmod, knob, monkeypatch):
+    """Byte counters are exact below 255; a frame whose counter reaches the limit is
+    recomputed with 16-bit counters.  Forcing every frame through the redo pass, lowering
+    the limit to 170 so that only some frames take it (the oracle's raw maxima of these
+    six frames are 187, 184, 157, 169, 166, 171: frames 0, 1, 5 are redone), or running
+    16-bit counters only must all give the oracle's results bit for bit."""
+    monkeypatch.setenv(*knob)
+    params = synth.preset(3)
+    frames = synth.batch(3, 0, 0, 6)
+    det, rings = _run(rdmod, params, frames)
+    for i in range(6):
+        _check_frame(rdmod, det, i, params, frames[i], rings[i], full=(i < 2))

@@ -56,7 +56,8 @@ def build_rd(force=False):
         glob.glob(os.path.join(ROOT, "include", "*.h"))
     if not (force or _stale(out, deps)):
         return out
-    cmd = [NVCC, "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
+    prof = ["-DRD_K2_PROF"] if os.environ.get("RD_BUILD_PROF") else []   # K2 phase-cycle counters (tools/phase_probe.py)
+    cmd = [NVCC, "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo"] + prof + [
            "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off", "-shared",
            "-Xptxas", "-v", "-I", os.path.join(ROOT, "include"), "-o", out] + srcs + ["-lcudart"]
     r = _run(cmd)
