@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(512, MINB) k_hough(Params P) {
     my_hot += __shfl_xor_sync(0xffffffffu, my_hot, o);
   }
   if (lane == 0) {
-    if (my_votes) atomicAdd(&P.stats[f].votes, (unsigned long long)my_votes);
+    (void)my_votes;   // the per-frame vote count comes from K1.5 (k_rays.cu)
     if (my_hot) atomicAdd(&P.stats[f].hotspots, (unsigned long long)my_hot);
   }
   if (tid == 0 && *s_flags) atomicOr(&P.flags[f], *s_flags);

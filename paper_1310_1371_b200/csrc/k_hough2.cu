@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
     const int64_t tl = (int64_t)f * ntiles + tile;
     const int ne = min(P.ray_count[tl], P.entry_cap);
     const int64_t gbase = tl * P.entry_cap;
-    int my_votes = 0, my_hot = 0;
+    int my_hot = 0;   // interior hotspots (the per-frame vote count comes from K1.5)
 
     // list the rays active in the step starting at level L0s (count: s_nact[p])
     auto setup = [&](int L0s, int p) {
@@ -284,7 +284,6 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
             sh[g] = (uint32_t)(cell & ((1 << CSH) - 1)) * BITS;
             addr[g] = ok ? raw_base + (uint32_t)(g * lvlc * CB) + 4u * (uint32_t)(cell >> CSH) : dummy;
             okm |= (unsigned)ok << g;
-            my_votes += ok & ((unsigned)(cx - hal) < (unsigned)T) & ((unsigned)(cy - hal) < (unsigned)T);
           }
 #pragma unroll
           for (int g = 0; g < G; ++g) old[g] = atom_add_shared(addr[g], ((okm >> g) & 1u) << sh[g]);
@@ -474,12 +473,8 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
       PMARK(4);
     }
     // ---------------- per-frame counters of this tile
-    my_votes = __reduce_add_sync(FULL, my_votes);
     my_hot = __reduce_add_sync(FULL, my_hot);
-    if (lane == 0) {
-      if (my_votes) atomicAdd(&P.stats[f].votes, (unsigned long long)my_votes);
-      if (my_hot) atomicAdd(&P.stats[f].hotspots, (unsigned long long)my_hot);
-    }
+    if (lane == 0 && my_hot) atomicAdd(&P.stats[f].hotspots, (unsigned long long)my_hot);
     __syncthreads();
     if (tid == 0) {
       if (*s_flags) atomicOr(&P.flags[f], *s_flags);
@@ -496,8 +491,8 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
 #undef PMARK
 }
 
-// Frames marked by the byte-counter pass: discard their K2 results (peaks, K2 counters and
-// flag bits) and list them for the 16-bit pass.  One CTA.
+// Frames marked by the byte-counter pass: discard their K2 results (peaks, the hotspot
+// count, debug records and K2 flag bits) and list them for the 16-bit pass.  One CTA.
 __global__ void k_redo_reset(Params P, int n_frames) {
   __shared__ int n;
   if (threadIdx.x == 0) n = 0;
@@ -505,7 +500,6 @@ __global__ void k_redo_reset(Params P, int n_frames) {
   for (int f = threadIdx.x; f < n_frames; f += blockDim.x) {
     if (!P.redo[f] && !P.force_redo) continue;
     P.peak_count[f] = 0;
-    P.stats[f].votes = 0;
     P.stats[f].hotspots = 0;
     P.dbg_count[f] = 0;
     P.flags[f] &= ~(OVF_HOTSPOTS | OVF_RINGS | OVF_DEBUG);

@@ -14,6 +14,23 @@
 namespace rd {
 
 namespace {
+// llround of an exactly computed product (|v| < 2^31), as in K2 (reading R9)
+__device__ __forceinline__ int rnd_half_away(double v) { return __double2int_rz(__dadd_rz(v, copysign(0.5, v))); }
+
+// Largest r in [rlo - 1, rhi] such that c + llround(r' d) lies in [0, n - 1] for every r' in
+// [rlo, r]: the target coordinate is monotone in r and starts inside the frame (r = 0), so
+// the in-frame levels of a ray are a prefix of the level range (binary search).
+__device__ int inframe_prefix(int c, double d, int n, int rlo, int rhi) {
+  int lo = rlo - 1, hi = rhi;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    const int t = c + rnd_half_away(__dmul_rn((double)mid, d));
+    if (t >= 0 && t <= n - 1) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
 __device__ __forceinline__ void half_ge(float a, float b, float& lo, float& hi) {
   if (a > 0.f) lo = fmaxf(lo, __fdividef(b, a));
   else if (a < 0.f) hi = fminf(hi, __fdividef(b, a));
@@ -37,6 +54,7 @@ __global__ void __launch_bounds__(128) k_rays(Params P) {
   const int reach = rhi + hal + 1;
   const int wx0 = max((bx * T1 - reach) / T, 0), wx1 = min((bx * T1 + T1 - 1 + reach) / T, P.ntx - 1);
   const int wy0 = max((by * T1 - reach) / T, 0), wy1 = min((by * T1 + T1 - 1 + reach) / T, P.nty - 1);
+  int my_votes = 0;
   for (int j0 = 0; j0 < 2 * cnt; j0 += blockDim.x) {   // uniform trip count across the CTA
     const int j = j0 + threadIdx.x;
     const bool valid = j < 2 * cnt;
@@ -50,6 +68,10 @@ __global__ void __launch_bounds__(128) k_rays(Params P) {
     const double sgn = (j & 1) ? -1.0 : 1.0;
     const int x = (int)(xy & 0xFFFFu), y = (int)(xy >> 16);
     const double u = sgn * d.x, v = sgn * d.y;
+    if (valid) {   // the ray's in-frame votes (per-frame vote count)
+      const int px = inframe_prefix(x, u, W, rlo, rhi), py = inframe_prefix(y, v, H, rlo, rhi);
+      my_votes += max(0, min(px, py) - rlo + 1);
+    }
     const float fu = (float)u, fv = (float)v, fx = (float)x, fy = (float)y;
     // bounding box of the target segment, widened by the largest halo and rounding
     const float ax = fx + fu * rlo, bxp = fx + fu * rhi, ay = fy + fv * rlo, byp = fy + fv * rhi;
@@ -92,6 +114,8 @@ __global__ void __launch_bounds__(128) k_rays(Params P) {
         }
       }
   }
+  my_votes = __reduce_add_sync(0xffffffffu, my_votes);
+  if (lane == 0 && my_votes) atomicAdd(&P.stats[f].votes, (unsigned long long)my_votes);
 }
 
 cudaError_t launch_rays(int n_frames, const Params& P, cudaStream_t st) {
