@@ -65,6 +65,7 @@ __global__ void __launch_bounds__(128) k_rays(Params P) {
       xy = P.bin_xy[g];
       d = P.bin_d[g];
     }
+    if (!__any_sync(0xffffffffu, valid)) continue;   // warps past the bin's rays skip the window walk
     const double sgn = (j & 1) ? -1.0 : 1.0;
     const int x = (int)(xy & 0xFFFFu), y = (int)(xy >> 16);
     const double u = sgn * d.x, v = sgn * d.y;

@@ -328,6 +328,14 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
             det->k2_threads16, det->k2_minb16, det->P16.k2o.total, det->P16.k2_rcap);
   P.ntx = (c.width + P.k2t - 1) / P.k2t;
   P.nty = (c.height + P.k2t - 1) / P.k2t;
+  {   // K1.5 tests a bin's rays against a window of at most 64 Hough tiles
+    const int reach = P.r_hi + P.hal + 1, wspan = (2 * reach + T1) / P.k2t + 2;
+    if (wspan * wspan > 64) {
+      delete det;
+      snprintf(g_err, sizeof g_err, "search radius %d too large for the %d-px Hough tiles", c.r_max, P.k2t);
+      return RD_ERR_CONFIG;
+    }
+  }
   if (k_ridges_smem(P.Ks) > smax || det->G == 0 || k_fit_smem(P) > smax) {
     delete det;
     snprintf(g_err, sizeof g_err, "shared memory: K1 %zu K2 %zu K3 %zu > %zu", k_ridges_smem(P.Ks),
