@@ -1,0 +1,286 @@
+// k_ridges2.cu — K1 (column-streaming form): scale-selection smoothing, 5x5 Sobel Hessian,
+// least principal curvature and directed-ridge test, with ridges compacted straight into
+// the 32x32 bins.
+//
+// Rows A1-A4 of DESIGN.md §1 ("Directed ridge detection"; SI steps 1-2,
+// PAPER.md:919-931).  A CTA owns a vertical strip of KS_COLS = 256 frame columns (224
+// output columns = 7 ridge bins, 16 halo columns on each side) and a segment of rows; thread
+// t owns column X0 - 16 + t and the CTA walks down the rows, RB input rows per step:
+//   R = q (x) I along x      from the input rows in shared memory         (int32, exact)
+//   G = q (x) R along y      2K_s+1 R values in a register window          (fp64, exact)
+//   HA|HB|HC = d2|s5|d1 (x) G along x   from the G rows in shared memory   (fp64, exact)
+//   Ixx|Iyy|Ixy = s5|d2|d1 (x) H along y   5-row register windows          (fp64, exact)
+//   kappa (fixed fp64 recipe, no FMA) and rho of the candidates kappa < t, into row rings
+//   ridge test one row behind against the kappa ring (R6)
+// Three CTA barriers per step of RB rows; the RB rows of a phase are independent chains.
+// Pixels, taps and arithmetic are those of the tiled K1 (k_ridges.cu) and of the oracle:
+// every integer stage is exact, so evaluation order is free; kappa/rho use the shared
+// explicit-rounding recipe (rd_internal.cuh).  Replicate border: input rows and columns are
+// clamped at load time.
+#include <algorithm>
+
+#include "rd_internal.cuh"
+
+namespace rd {
+
+namespace {
+constexpr int KS_COLS = 256;        // strip columns = threads per CTA
+constexpr int KS_HALO = 16;         // halo columns on each side (>= K_s + 3)
+constexpr int KS_OUT = KS_COLS - 2 * KS_HALO;   // 224 output columns = 7 bins
+constexpr int KS_NB = KS_OUT / 32;  // bins per strip
+constexpr double NOT_CAND = 2.0;    // rho.x of a pixel that is not a ridge candidate (|rho.x| <= 1)
+}  // namespace
+
+template <typename PixT, int KS, int RB>
+__global__ void __launch_bounds__(KS_COLS, 2)
+k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, int seg_rows, Params P) {
+  constexpr int NTAP = 2 * KS + 1;
+  constexpr int NR = RB + 2;        // kappa / rho ring rows
+  struct Smem {
+    double2 sD[NR][KS_COLS];             // rho ring (x = NOT_CAND: no candidate)
+    double sK[NR][KS_COLS];              // kappa ring
+    double sG[RB][KS_COLS];              // G rows
+    int sI[RB][KS_COLS];                 // input rows (as int)
+    unsigned sBal[2][RB][KS_COLS / 32];  // ridge ballots of a step's rows, by parity
+    int sCur[KS_NB];                     // ridges so far in the current row of each bin
+  };
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem& S = *reinterpret_cast<Smem*>(smem_raw);
+  auto& sD = S.sD;
+  auto& sK = S.sK;
+  auto& sG = S.sG;
+  auto& sI = S.sI;
+  auto& sBal = S.sBal;
+  auto& sCur = S.sCur;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int W = P.W, H = P.H;
+  const int f = blockIdx.z;
+  const int X0 = blockIdx.x * KS_OUT;                 // first output column of the strip
+  const int Y0 = blockIdx.y * seg_rows;               // first output row of the segment
+  const int Y1 = min(Y0 + seg_rows, H);               // one past the last output row
+  const int x = X0 - KS_HALO + tid;                   // this thread's column
+  const int xc = min(max(x, 0), W - 1);               // clamped (replicate border)
+  const uint8_t* frame = frames + (int64_t)f * fstride;
+  int q[NTAP];
+#pragma unroll
+  for (int j = 0; j < NTAP; ++j) q[j] = P.q[j];
+  const double t_int = P.t_int;
+  // which columns compute what: R on [KS, 256-KS), G..H on [13, 243), output on [16, 240)
+  const bool doR = tid >= KS && tid < KS_COLS - KS;
+  const bool doH = tid >= KS_HALO - 3 && tid < KS_COLS - KS_HALO + 3;
+  const bool outc = tid >= KS_HALO && tid < KS_COLS - KS_HALO && x < W;
+  const bool colH = doH && x >= 2 && x <= W - 3;      // Hessian valid in this column
+  const bool colR = outc && x >= 3 && x <= W - 4;     // ridge candidates in this column
+
+  // Rows, relative to the input row yi of a phase row: G row yi - KS, kappa row yi - KS - 2,
+  // ridge row yi - KS - 3.  The first G needed is row Y0 - 3 (kappa row Y0 - 1 needs H rows
+  // Y0 - 3 .. Y0 + 1), so input starts at Y0 - 3 - KS.  Ring slots are (row - ybase) mod NR.
+  const int ys0 = Y0 - 3 - KS;
+  const int ybase = ys0 - KS - 8 * NR;                // <= every ring row, keeps the mod positive
+  const int n_rows = (Y1 - 1) + KS + 3 - ys0 + 1;     // input rows through ridge row Y1 - 1
+  const int n_steps = (n_rows + RB - 1) / RB;
+
+  double wR[NTAP];                 // R rows yi - 2KS .. yi (this column)
+  double wA[5], wB[5], wC[5];      // HA, HB, HC rows yg - 4 .. yg
+#pragma unroll
+  for (int j = 0; j < NTAP; ++j) wR[j] = 0.0;
+#pragma unroll
+  for (int j = 0; j < 5; ++j) wA[j] = wB[j] = wC[j] = 0.0;
+  // input prefetch: the next step's RB rows
+  PixT pf[RB];
+#pragma unroll
+  for (int r = 0; r < RB; ++r) {
+    const int yy = min(max(ys0 + r, 0), H - 1);
+    pf[r] = reinterpret_cast<const PixT*>(frame + (int64_t)yy * pitch)[xc];
+  }
+  // bin output: bin b of the strip covers threads 16 + 32b .. 47 + 32b (upper half of warp b,
+  // lower half of warp b + 1).  A step's ridges are written in the next step, once both
+  // halves' ballots are in shared memory, so every bin keeps row-major order.
+  const int b_own = (tid - KS_HALO) >> 5, b_i = (tid - KS_HALO) & 31;   // bin and index in it
+  const int64_t fbase = (int64_t)f * P.nbx * P.nby;
+  if (tid < KS_NB) sCur[tid] = 0;
+  unsigned rd_bits = 0;            // ridge flags of the previous step's RB test rows
+  int rd_y0 = 0;                   // first test row of the previous step
+  bool rd_any = false;             // the previous step tested rows of this segment
+  int rd_cur = 0;                  // the bin cursor after the emitted rows
+
+  for (int st = 0; st <= n_steps; ++st) {   // the extra step only emits the last rows
+    const int yi0 = ys0 + st * RB;
+    const bool compute = st < n_steps;
+    // 1. input rows -> shared memory; prefetch the next step's rows
+    if (compute) {
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        sI[r][tid] = (int)pf[r];
+        const int yy = min(max(yi0 + RB + r, 0), H - 1);
+        pf[r] = reinterpret_cast<const PixT*>(frame + (int64_t)yy * pitch)[xc];
+      }
+    }
+    __syncthreads();
+    // ridges of the previous step's test rows (ballots of parity (st - 1) & 1): slots follow
+    // from the bin cursor and the popcounts of earlier rows, so no shared state changes here
+    const bool in_bin = b_own >= 0 && b_own < KS_NB;
+    if (rd_any && in_bin) {
+      const int p = (st - 1) & 1;
+      int base = sCur[b_own];
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        const int yr = rd_y0 + r;
+        if (yr < Y0 || yr >= Y1) continue;   // uniform across the CTA
+        const unsigned m = (sBal[p][r][b_own] >> 16) | (sBal[p][r][b_own + 1] << 16);
+        if ((rd_bits >> r) & 1u) {
+          const int slot = base + __popc(m & ((1u << b_i) - 1u));
+          const int64_t bin = fbase + (int64_t)(yr / T1) * P.nbx + X0 / T1 + b_own;
+          if (slot < P.ridge_cap) {
+            const int64_t o = bin * P.ridge_cap + slot;
+            P.bin_xy[o] = (uint32_t)x | ((uint32_t)yr << 16);
+            P.bin_d[o] = sD[(yr - ybase) % NR][tid];
+          }
+        }
+        base += __popc(m);
+        if ((yr & (T1 - 1)) == T1 - 1 || yr == Y1 - 1) {   // the bin row is complete
+          const int bx = X0 / T1 + b_own;
+          if (b_i == 0 && bx < P.nbx) {
+            const int64_t bin = fbase + (int64_t)(yr / T1) * P.nbx + bx;
+            P.bin_count[bin] = min(base, P.ridge_cap);
+            if (base > P.ridge_cap) atomicOr(&P.flags[f], OVF_RIDGES);
+            if (base) atomicAdd(&P.stats[f].ridges, (unsigned long long)base);
+          }
+          base = 0;
+        }
+      }
+      rd_cur = base;   // the bin owner stores it after the next barrier
+    }
+    if (!compute) break;
+    // 2. row passes R(yi) (int32 exact) -> column window; G(yg) (fp64 exact), RB rows
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      int acc = 0;
+      if (doR) {
+#pragma unroll
+        for (int j = 0; j < NTAP; ++j) acc += q[j] * sI[r][tid - KS + j];
+      }
+#pragma unroll
+      for (int j = 0; j < NTAP - 1; ++j) wR[j] = wR[j + 1];
+      wR[NTAP - 1] = (double)acc;
+      double g0 = 0.0, g1 = 0.0;   // two exact partial sums (integers < 2^53: order-free)
+#pragma unroll
+      for (int j = 0; j < NTAP; ++j) {
+        if (j & 1) g1 = fma((double)q[j], wR[j], g1);
+        else g0 = fma((double)q[j], wR[j], g0);
+      }
+      sG[r][tid] = g0 + g1;
+    }
+    __syncthreads();
+    if (rd_any && in_bin && b_i == 0) sCur[b_own] = rd_cur;
+    // 3. horizontal Sobel passes, vertical windows, kappa and rho of the kappa rows, RB rows
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      const int yk = yi0 + r - KS - 2;
+      double ha = 0.0, hb = 0.0, hc = 0.0;
+      if (doH) {
+        const double g0 = sG[r][tid - 2], g1 = sG[r][tid - 1], g2 = sG[r][tid], g3 = sG[r][tid + 1],
+                     g4 = sG[r][tid + 2];
+        ha = (g0 + g4) - 2.0 * g2;                       // d2 = [1,0,-2,0,1]
+        hb = (g0 + g4) + 4.0 * (g1 + g3) + 6.0 * g2;     // s5 = [1,4,6,4,1]
+        hc = (g4 - g0) + 2.0 * (g3 - g1);                // d1 = [-1,-2,0,2,1]
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        wA[j] = wA[j + 1];
+        wB[j] = wB[j + 1];
+        wC[j] = wC[j + 1];
+      }
+      wA[4] = ha;
+      wB[4] = hb;
+      wC[4] = hc;
+      double kap = HUGE_VAL;
+      double2 dir = make_double2(NOT_CAND, 0.0);
+      if (colH && yk >= 2 && yk <= H - 3) {
+        const double Ixx = (wA[0] + wA[4]) + 4.0 * (wA[1] + wA[3]) + 6.0 * wA[2];
+        const double Iyy = (wB[0] + wB[4]) - 2.0 * wB[2];
+        const double Ixy = (wC[4] - wC[0]) + 2.0 * (wC[3] - wC[1]);
+        double sq, e;
+        kap = kappa_of(Ixx, Ixy, Iyy, &sq, &e);
+        double dx, dy;
+        if (kap < t_int && direction_of(Ixy, e, sq, &dx, &dy)) dir = make_double2(dx, dy);   // R3
+      }
+      const int slot = (yk - ybase) % NR;
+      sK[slot][tid] = kap;
+      sD[slot][tid] = dir;
+    }
+    __syncthreads();
+    // 4. ridge tests of the rows one behind the kappa rows (R6)
+    rd_bits = 0;
+    rd_y0 = yi0 - KS - 3;
+    rd_any = false;
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      const int yr = rd_y0 + r;
+      bool is_r = false;
+      if (colR && yr >= Y0 && yr < Y1 && yr >= 3 && yr <= H - 4) {
+        const int s0 = (yr - ybase) % NR, sm = (yr - 1 - ybase) % NR, sp = (yr + 1 - ybase) % NR;
+        const double2 dir = sD[s0][tid];
+        if (dir.x != NOT_CAND) {
+          const double kp = sK[s0][tid];
+          const int ox = (int)llround(dir.x), oy = (int)llround(dir.y);
+          const bool after_plus = (oy > 0) || (oy == 0 && ox > 0);
+          const double kplus = sK[oy > 0 ? sp : (oy < 0 ? sm : s0)][tid + ox];
+          const double kminus = sK[oy > 0 ? sm : (oy < 0 ? sp : s0)][tid - ox];
+          const double kafter = after_plus ? kplus : kminus, kbefore = after_plus ? kminus : kplus;
+          is_r = (kp <= kafter) && (kp < kbefore);
+        }
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, is_r);
+      if (lane == 0) sBal[st & 1][r][warp] = bal;
+      rd_bits |= (unsigned)is_r << r;
+      rd_any |= yr >= Y0 && yr < Y1;
+    }
+  }
+}
+
+template <typename PixT, int KS>
+static cudaError_t launch_s(const void* frames, int64_t pitch, int64_t fstride, int n_frames, const Params& P,
+                            cudaStream_t st) {
+  constexpr int RB = 4;
+  // segments of whole bin rows: about two per frame
+  const int seg = std::max(T1, ((P.H + 1) / 2 + T1 - 1) / T1 * T1);
+  dim3 grid((P.W + KS_OUT - 1) / KS_OUT, (P.H + seg - 1) / seg, n_frames);
+  // dynamic shared memory: rings + rows (NR = RB + 2 rows of rho and kappa)
+  const size_t sm = (size_t)(RB + 2) * KS_COLS * 24 + (size_t)RB * KS_COLS * 12 + 2 * RB * (KS_COLS / 32) * 4 + 64;
+  cudaFuncSetAttribute(k_ridges2<PixT, KS, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_ridges2<PixT, KS, RB><<<grid, KS_COLS, sm, st>>>((const uint8_t*)frames, pitch, fstride, seg, P);
+  return cudaGetLastError();
+}
+
+template <typename PixT>
+static cudaError_t launch_sp(const void* frames, int64_t pitch, int64_t fstride, int n, const Params& P,
+                             cudaStream_t st) {
+  switch (P.Ks) {
+    case 1: return launch_s<PixT, 1>(frames, pitch, fstride, n, P, st);
+    case 2: return launch_s<PixT, 2>(frames, pitch, fstride, n, P, st);
+    case 3: return launch_s<PixT, 3>(frames, pitch, fstride, n, P, st);
+    case 4: return launch_s<PixT, 4>(frames, pitch, fstride, n, P, st);
+    case 5: return launch_s<PixT, 5>(frames, pitch, fstride, n, P, st);
+    case 6: return launch_s<PixT, 6>(frames, pitch, fstride, n, P, st);
+    case 7: return launch_s<PixT, 7>(frames, pitch, fstride, n, P, st);
+    case 8: return launch_s<PixT, 8>(frames, pitch, fstride, n, P, st);
+    case 9: return launch_s<PixT, 9>(frames, pitch, fstride, n, P, st);
+    case 10: return launch_s<PixT, 10>(frames, pitch, fstride, n, P, st);
+    case 11: return launch_s<PixT, 11>(frames, pitch, fstride, n, P, st);
+    case 12: return launch_s<PixT, 12>(frames, pitch, fstride, n, P, st);
+    case 13: return launch_s<PixT, 13>(frames, pitch, fstride, n, P, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// K_s <= 13 (the 16-column halo covers K_s + 3); larger K_s use the tiled K1
+bool ridges_stream_ok(const Params& P) { return P.Ks >= 1 && P.Ks <= KS_HALO - 3; }
+
+cudaError_t launch_ridges_stream(const void* frames, int64_t pitch, int64_t fstride, int n_frames, const Params& P,
+                                 cudaStream_t st) {
+  if (P.pixel_bytes == 1) return launch_sp<uint8_t>(frames, pitch, fstride, n_frames, P, st);
+  return launch_sp<uint16_t>(frames, pitch, fstride, n_frames, P, st);
+}
+
+}  // namespace rd
