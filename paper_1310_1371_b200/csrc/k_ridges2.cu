@@ -28,7 +28,20 @@ constexpr int KS_COLS = 256;        // strip columns = threads per CTA
 constexpr int KS_HALO = 16;         // halo columns on each side (>= K_s + 3)
 constexpr int KS_OUT = KS_COLS - 2 * KS_HALO;   // 224 output columns = 7 bins
 constexpr int KS_NB = KS_OUT / 32;  // bins per strip
+#ifndef RD_K1_RB
+#define RD_K1_RB 4
+#endif
 constexpr double NOT_CAND = 2.0;    // rho.x of a pixel that is not a ridge candidate (|rho.x| <= 1)
+
+template <int RB>
+struct K1SSmem {                       // dynamic shared memory of k_ridges2
+  double2 sD[RB + 2][KS_COLS];         // rho ring (x = NOT_CAND: no candidate)
+  double sK[RB + 2][KS_COLS];          // kappa ring
+  double sG[RB][KS_COLS];              // G rows
+  int sI[RB][KS_COLS];                 // input rows (as int)
+  unsigned sBal[2][RB][KS_COLS / 32];  // ridge ballots of a step's rows, by parity
+  int sCur[KS_NB];                     // ridges so far in the current row of each bin
+};
 }  // namespace
 
 template <typename PixT, int KS, int RB>
@@ -36,16 +49,8 @@ __global__ void __launch_bounds__(KS_COLS, 2)
 k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, int seg_rows, Params P) {
   constexpr int NTAP = 2 * KS + 1;
   constexpr int NR = RB + 2;        // kappa / rho ring rows
-  struct Smem {
-    double2 sD[NR][KS_COLS];             // rho ring (x = NOT_CAND: no candidate)
-    double sK[NR][KS_COLS];              // kappa ring
-    double sG[RB][KS_COLS];              // G rows
-    int sI[RB][KS_COLS];                 // input rows (as int)
-    unsigned sBal[2][RB][KS_COLS / 32];  // ridge ballots of a step's rows, by parity
-    int sCur[KS_NB];                     // ridges so far in the current row of each bin
-  };
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  Smem& S = *reinterpret_cast<Smem*>(smem_raw);
+  K1SSmem<RB>& S = *reinterpret_cast<K1SSmem<RB>*>(smem_raw);
   auto& sD = S.sD;
   auto& sK = S.sK;
   auto& sG = S.sG;
@@ -61,9 +66,7 @@ k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, in
   const int x = X0 - KS_HALO + tid;                   // this thread's column
   const int xc = min(max(x, 0), W - 1);               // clamped (replicate border)
   const uint8_t* frame = frames + (int64_t)f * fstride;
-  int q[NTAP];
-#pragma unroll
-  for (int j = 0; j < NTAP; ++j) q[j] = P.q[j];
+  const int* q = P.q;   // taps stay in the constant bank
   const double t_int = P.t_int;
   // which columns compute what: R on [KS, 256-KS), G..H on [13, 243), output on [16, 240)
   const bool doR = tid >= KS && tid < KS_COLS - KS;
@@ -80,10 +83,10 @@ k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, in
   const int n_rows = (Y1 - 1) + KS + 3 - ys0 + 1;     // input rows through ridge row Y1 - 1
   const int n_steps = (n_rows + RB - 1) / RB;
 
-  double wR[NTAP];                 // R rows yi - 2KS .. yi (this column)
+  uint32_t wR[NTAP];               // R rows yi - 2KS .. yi (this column; R < 2^31)
   double wA[5], wB[5], wC[5];      // HA, HB, HC rows yg - 4 .. yg
 #pragma unroll
-  for (int j = 0; j < NTAP; ++j) wR[j] = 0.0;
+  for (int j = 0; j < NTAP; ++j) wR[j] = 0u;
 #pragma unroll
   for (int j = 0; j < 5; ++j) wA[j] = wB[j] = wC[j] = 0.0;
   // input prefetch: the next step's RB rows
@@ -162,14 +165,12 @@ k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, in
       }
 #pragma unroll
       for (int j = 0; j < NTAP - 1; ++j) wR[j] = wR[j + 1];
-      wR[NTAP - 1] = (double)acc;
-      double g0 = 0.0, g1 = 0.0;   // two exact partial sums (integers < 2^53: order-free)
+      wR[NTAP - 1] = (uint32_t)acc;
+      // G = sum q_j R_j < 2^53 in 64-bit integers (symmetric taps), then exactly to fp64
+      unsigned long long g = (unsigned long long)(uint32_t)q[KS] * wR[KS];
 #pragma unroll
-      for (int j = 0; j < NTAP; ++j) {
-        if (j & 1) g1 = fma((double)q[j], wR[j], g1);
-        else g0 = fma((double)q[j], wR[j], g0);
-      }
-      sG[r][tid] = g0 + g1;
+      for (int j = 0; j < KS; ++j) g += (unsigned long long)(uint32_t)q[j] * (unsigned long long)(wR[j] + wR[NTAP - 1 - j]);
+      sG[r][tid] = (double)g;
     }
     __syncthreads();
     if (rd_any && in_bin && b_i == 0) sCur[b_own] = rd_cur;
@@ -242,12 +243,12 @@ k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, in
 template <typename PixT, int KS>
 static cudaError_t launch_s(const void* frames, int64_t pitch, int64_t fstride, int n_frames, const Params& P,
                             cudaStream_t st) {
-  constexpr int RB = 4;
+  constexpr int RB = RD_K1_RB;
   // segments of whole bin rows: about two per frame
   const int seg = std::max(T1, ((P.H + 1) / 2 + T1 - 1) / T1 * T1);
   dim3 grid((P.W + KS_OUT - 1) / KS_OUT, (P.H + seg - 1) / seg, n_frames);
   // dynamic shared memory: rings + rows (NR = RB + 2 rows of rho and kappa)
-  const size_t sm = (size_t)(RB + 2) * KS_COLS * 24 + (size_t)RB * KS_COLS * 12 + 2 * RB * (KS_COLS / 32) * 4 + 64;
+  const size_t sm = sizeof(K1SSmem<RB>);
   cudaFuncSetAttribute(k_ridges2<PixT, KS, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   k_ridges2<PixT, KS, RB><<<grid, KS_COLS, sm, st>>>((const uint8_t*)frames, pitch, fstride, seg, P);
   return cudaGetLastError();

@@ -273,8 +273,7 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
         if (!k_hough2_has_shape(cb, s.G, s.nt, s.minb)) continue;
         Q.k2t = s.T;
         const size_t limit = s.minb == 1 ? smax : std::min(smax, sm_sm / s.minb - 1024);
-        const int raws = s.T + 2 * Q.hal;
-        Q.k2_rcap = 256;
+          Q.k2_rcap = 256;
         if (k_hough2_layout(Q, s.G, s.nt, cb) > limit) continue;
         while (Q.k2_rcap < Q.entry_cap) {   // as many resident rays as fit
           Q.k2_rcap += 64;
