@@ -180,6 +180,19 @@ def run_gpu(args):
     det.sync()
     stats = det.stats(B)
     votes_per_step = int(stats["votes"].sum())
+    # window cells of the hotspots (A7's unit of work): a debug pass over a
+    # few frames lists every interior hotspot with its r; cells = sum (2 K_r + 1)^2
+    nd = min(B, 8)
+    dbg = rd.Detector(dict(params, debug=1), max_batch=nd, device=local)
+    dbg.detect(frames_d[:nd])
+    dbg.sync()
+    win_cells = 0
+    for i in range(nd):
+        r = dbg.dump_hotspots(i)["r"].astype(np.int64)
+        K = (3 * (params["sig_a"] * r + params["sig_b"]) + params["sig_den"] - 1) // params["sig_den"]
+        win_cells += int(((2 * K + 1) ** 2).sum())
+    win_cells_per_frame = win_cells / nd
+    dbg.close()
 
     # ---------------- timed region: device time, CUDA events on the launching stream
     barrier()
@@ -263,6 +276,12 @@ def run_gpu(args):
     # (tools/microbench, profiles/microbench_r01.log) x 148 SM x sm_max
     atom_peak = 11.0 * 148 * sm_max * 1e6 / 1e9
     k2_ach = votes_per_step / (kms_step[1] / 1e3) / 1e9
+    # K2 as an ALU-issue-bound kernel: algorithmic lane operations per frame =
+    # 11 per in-frame vote (~10 ops + 1 atomic) + 2 per hotspot window cell
+    # (multiply-add); the NMS compares (<1 %) are left out; peak = 148 SM x 128 lanes x sm_max
+    k2_ops = 11 * votes_per_step + 2 * win_cells_per_frame * B
+    lane_peak = 148 * 128 * sm_max * 1e6 / 1e12
+    k2_alu = k2_ops / (kms_step[1] / 1e3) / 1e12
     summ = {}
     sp = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
     if os.path.exists(sp):
@@ -275,6 +294,11 @@ def run_gpu(args):
          "unit": "TFLOP/s", "frac": round(k1_ach / fp64_peak, 4), "traffic": summ.get("k_ridges"),
          "peak_note": "fp64 DFMA issue: 148 SM x 64/clk x sm_max (guide unit counts); ops = fp64 instructions of "
                       "the exact separable Gaussian + Sobel + kappa per pixel (DESIGN.md §6)"},
+        {"kernel": "k_hough", "bound": "alu", "achieved": round(k2_alu, 4), "peak": round(lane_peak, 2),
+         "unit": "T lane-op/s", "frac": round(k2_alu / lane_peak, 5), "traffic": summ.get("k_hough"),
+         "peak_note": "ALU issue: 148 SM x 128 lanes x sm_max (guide unit counts); ops = 11 per in-frame vote + "
+                      "2 per hotspot window cell (SURVEY.md §8(d), DESIGN.md §6); window cells "
+                      f"{win_cells_per_frame:.0f}/frame measured by a debug pass"},
         {"kernel": "k_hough", "bound": "alu", "achieved": round(k2_ach, 3), "peak": round(atom_peak, 1),
          "unit": "Gvote/s", "frac": round(k2_ach / atom_peak, 5), "traffic": summ.get("k_hough"),
          "peak_note": "shared-memory atomic issue: measured 11.0 ATOMS/clk/SM x 148 SM x sm_max; one atomic per "
@@ -314,7 +338,7 @@ def run_gpu(args):
                     "h2d_bytes_per_step": B * fbytes * world,
                     "d2h_bytes_per_step": (B * det.ring_cap * 64 + 4 * B) * world,
                     "api": "Detector.detect_host -> rd_detect_host (pinned host buffers)"},
-            "gpu_launches": 4 * args.steps,
+            "gpu_launches": 6 * args.steps,   # K1, K1.5, K2, K2 redo reset, K2 redo pass, K3 per step
             "clocks": clocks}
     if gather_ms is not None:
         line["gather_ms"] = round(gather_ms, 3)
@@ -332,7 +356,7 @@ def main():
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=10)
-    ap.add_argument("--cpu-frames", type=int, default=48)
+    ap.add_argument("--cpu-frames", type=int, default=256)
     ap.add_argument("--ref-frames", type=int, default=32)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
