@@ -509,7 +509,8 @@ rd_status rd_detect(rd_detector* det, const void* d_frames, int64_t pitch, int64
 
 static rd_status ensure_host_path(rd_detector* det) {
   if (det->s_comp) return RD_OK;
-  det->chunk = std::min(det->max_batch, 32);
+  det->chunk = std::min(det->max_batch, 64);
+  if (const char* env = getenv("RD_HOST_CHUNK")) det->chunk = std::max(1, std::min(det->max_batch, atoi(env)));
   const size_t fbytes = (size_t)det->cfg.width * det->cfg.height * det->P.pixel_bytes;
   for (int i = 0; i < 2; ++i) {
     CK(cudaMalloc(&det->d_stage[i], fbytes * det->chunk));
@@ -536,10 +537,12 @@ rd_status rd_detect_host(rd_detector* det, const void* h_frames, int64_t pitch, 
   const int W = det->cfg.width, H = det->cfg.height, pb = det->P.pixel_bytes;
   const size_t row = (size_t)W * pb, fbytes = row * H;
   const int C = det->chunk, rc = det->P.ring_cap;
-  const int nchunks = (n + C - 1) / C;
+  // the first chunk is a quarter chunk: its copy is the only one nothing overlaps
+  const int C0 = std::max(1, C / 4);
+  const int nchunks = n <= C0 ? 1 : 1 + (n - C0 + C - 1) / C;
   rd_status result = RD_OK;
   for (int k = 0; k < nchunks; ++k) {
-    const int b = k & 1, f0 = k * C, m = std::min(C, n - f0);
+    const int b = k & 1, f0 = k == 0 ? 0 : C0 + (k - 1) * C, m = std::min(k == 0 ? C0 : C, n - f0);
     // H2D of chunk k may overwrite stage b only after chunk k-2 finished computing
     if (k >= 2) CK(cudaStreamWaitEvent(det->s_h2d, det->ev_done[b], 0));
     const char* src = (const char*)h_frames + (size_t)f0 * fstride;
