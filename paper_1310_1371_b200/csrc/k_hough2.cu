@@ -300,8 +300,8 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
               const int h = atomicAdd(&hcnt[li], 1);
               if (h < hot_cap) {
                 hcell[slot_of[g] * hot_cap + h] = (uint16_t)((iy << 8) | ix);
-                const int slot = tK[li] <= SMALL_K ? atomicAdd(&s_ntask[0], 1)
-                                                   : G * hot_cap - 1 - atomicAdd(&s_ntask[1], 1);
+                const int slot = (CB == 1 || tK[li] <= SMALL_K) ? atomicAdd(&s_ntask[0], 1)
+                                                                : G * hot_cap - 1 - atomicAdd(&s_ntask[1], 1);
                 tasks[slot] = (uint16_t)((g << 12) | h);
               } else {
                 atomicOr(s_flags, OVF_HOTSPOTS);
@@ -317,6 +317,84 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
       //     each hotspot and the candidate test
       {
         if (L0 + G < nlev) setup(L0 + G, par ^ 1);
+        if (CB == 1) {
+          // byte counters: a half-warp per hotspot, each lane two window rows (hl, hl + 16);
+          // a row is summed over whole 32-bit words with dp4a against the level's byte-plane
+          // weights for the row's alignment (w = 64 wh + wl): exact integer S as below
+          constexpr int NWW = 9;   // weight words per row: (3 + 2K + 1 + 3) / 4 <= 9 for K <= 15
+          const int ntask = (P.ablate & 4) ? 0 : s_ntask[0];
+          const int half = lane >> 4, hl = lane & 15;
+          for (int t0 = 2 * warp; t0 < ntask; t0 += 2 * NW) {
+            const int t = t0 + half;
+            const bool valid = t < ntask;
+            const int tk = tasks[valid ? t : t0];
+            const int g = tk >> 12, h = tk & 0xFFF;
+            const int li = L0 + g, sl = li % NSLOT;
+            const int K = tK[li];
+            const int c = hcell[sl * hot_cap + h];
+            const int iy = c >> 8, ix = c & 0xFF;
+            const int cx0 = ix - 1 + hal - K;        // first window column (raw-local)
+            const int al = cx0 & 3, nw = (al + 2 * K + 4) >> 2;
+            const uint32_t* wp = P.lvlWP + (size_t)((li * 4 + al) * P.wp_nw) * 2;
+            uint32_t wl[NWW], wh[NWW];
+#pragma unroll
+            for (int k = 0; k < NWW; ++k) {
+              wl[k] = k < nw ? __ldg(wp + 2 * k) : 0u;
+              wh[k] = k < nw ? __ldg(wp + 2 * k + 1) : 0u;
+            }
+            const uint16_t* w = tW + li * P.wstride;
+            const uint32_t* lvlw = raw32 + ((g * lvlc) >> 2);
+            unsigned long long acc = 0;
+#pragma unroll
+            for (int q2 = 0; q2 < 2; ++q2) {
+              const int row = hl + 16 * q2;
+              if (valid && row <= 2 * K && !(P.ablate & 1)) {
+                const uint32_t* rowp = lvlw + (((iy - 1 + hal + row - K) * rawp + cx0 - al) >> 2);
+                uint32_t lo = 0, hi = 0;
+#pragma unroll
+                for (int k = 0; k < NWW; ++k)
+                  if (k < nw) {
+                    const uint32_t v = rowp[k];
+                    lo = __dp4a(v, wl[k], lo);
+                    hi = __dp4a(v, wh[k], hi);
+                  }
+                acc += (unsigned long long)(hi * 64u + lo) * (unsigned long long)w[abs(row - K)];
+              }
+            }
+            // lane terms < 2^45: 24-bit halves, each half-warp reduced separately
+            const unsigned lo = (unsigned)(acc & 0xFFFFFFull), hi = (unsigned)(acc >> 24);
+            const unsigned lo0 = __reduce_add_sync(FULL, half ? 0u : lo);
+            const unsigned hi0 = __reduce_add_sync(FULL, half ? 0u : hi);
+            const unsigned lo1 = __reduce_add_sync(FULL, half ? lo : 0u);
+            const unsigned hi1 = __reduce_add_sync(FULL, half ? hi : 0u);
+            const unsigned long long S = ((unsigned long long)(half ? hi1 : hi0) << 24) + (half ? lo1 : lo0);
+            if (valid && hl == 0) {
+              hS[sl * hot_cap + h] = S;
+              const uint16_t rv = rawc[g * lvlc + (iy - 1 + hal) * rawp + (ix - 1 + hal)];
+              hraw[sl * hot_cap + h] = rv;
+              if (ix >= 1 && ix <= T && iy >= 1 && iy <= T) {   // interior hotspot
+                ++my_hot;
+                if (P.debug) {
+                  const int kd = atomicAdd(&P.dbg_count[f], 1);
+                  if (kd < P.dbg_cap) {
+                    HotRec rec;
+                    rec.r = P.r_lo + li; rec.y = Y0 - 1 + iy; rec.x = X0 - 1 + ix; rec.raw = rv;
+                    rec.S = (long long)S;
+                    P.dbg_hot[(int64_t)f * P.dbg_cap + kd] = rec;
+                  } else {
+                    atomicOr(&P.flags[f], OVF_DEBUG);
+                  }
+                }
+                // candidate: r in [r_min, r_max] and S > T_norm(r);
+                // the top level of the step waits for the next step's S of its upper neighbour
+                if (li >= 1 && li <= nlev - 2 && (double)(long long)S > tTn[li]) {
+                  if (li == Lhi) cdef[par * hot_cap + atomicAdd(&s_ndef[par], 1)] = (uint16_t)h;
+                  else cand[atomicAdd(s_ncand, 1)] = (uint16_t)tk;
+                }
+              }
+            }
+          }
+        } else {
         const int nsmall = (P.ablate & 4) ? 0 : s_ntask[0], nlarge = (P.ablate & 4) ? 0 : s_ntask[1];
         const int half = lane >> 4;
         // small-K hotspots: a half-warp each; large-K: a warp each (lanes over window rows)
@@ -405,6 +483,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
             }
           }
         }
+        }   // CB == 2
       }
       __syncthreads();
       PMARK(3);

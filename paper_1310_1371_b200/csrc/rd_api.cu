@@ -203,6 +203,7 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   P.k_icpt = (float)(3.0 * c.sig_b / c.sig_den + 1.0) + 0.01f;
   P.hal = Kmax + 1;
   P.wstride = Kmax + 1;
+  P.wp_nw = (2 * Kmax + 1 + 3 + 3) / 4;   // K2 dp4a weight words per window row (table below)
   std::vector<int> lvlW((size_t)P.n_levels * P.wstride, 0);
   double max_wsum = 0;
   for (int li = 0; li < P.n_levels; ++li) {
@@ -343,7 +344,27 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   }
 
   const int64_t B = max_batch, nbins = (int64_t)P.nbx * P.nby;
-  size_t tb = sizeof(int) * P.n_levels * 2 + sizeof(double) * P.n_levels + sizeof(int) * lvlW.size() + 64;
+  // byte-plane weight words for K2's dp4a window rows (byte counters): for level li, row start
+  // alignment a = (segment start) mod 4 and word k, byte b is the weight of segment cell
+  // o = 4k + b - a (0 outside [0, 2K]); w = 64 wh + wl with wl < 64, wh <= 64 (both bytes)
+  std::vector<uint32_t> lvlWP((size_t)P.n_levels * 4 * P.wp_nw * 2, 0);
+  for (int li = 0; li < P.n_levels; ++li)
+    for (int a = 0; a < 4; ++a)
+      for (int k = 0; k < P.wp_nw; ++k) {
+        uint32_t lo = 0, hi = 0;
+        for (int b = 0; b < 4; ++b) {
+          const int o = 4 * k + b - a, K = lvlK[li];
+          if (o < 0 || o > 2 * K) continue;
+          const int w = lvlW[(size_t)li * P.wstride + std::abs(o - K)];
+          lo |= (uint32_t)(w & 63) << (8 * b);
+          hi |= (uint32_t)(w >> 6) << (8 * b);
+        }
+        const size_t base = (((size_t)li * 4 + a) * P.wp_nw + k) * 2;
+        lvlWP[base] = lo;
+        lvlWP[base + 1] = hi;
+      }
+  size_t tb = sizeof(int) * P.n_levels * 2 + sizeof(double) * P.n_levels + sizeof(int) * lvlW.size() +
+              sizeof(uint32_t) * lvlWP.size() + 64;
 #define ALLOC(ptr, bytes)                                          \
   do {                                                             \
     e = cudaMalloc(&(ptr), (bytes));                               \
@@ -376,6 +397,10 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
     o += sizeof(int) * P.n_levels;
     memcpy(h.data() + o, lvlW.data(), sizeof(int) * lvlW.size());
     P.lvlW = reinterpret_cast<const int*>((char*)det->d_tables + o);
+    o += sizeof(int) * lvlW.size();
+    o = (o + 15) & ~size_t(15);
+    memcpy(h.data() + o, lvlWP.data(), sizeof(uint32_t) * lvlWP.size());
+    P.lvlWP = reinterpret_cast<const uint32_t*>((char*)det->d_tables + o);
     e = cudaMemcpy(det->d_tables, h.data(), tb, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) { rd_destroy(det); return cuda_fail(e, "cudaMemcpy tables"); }
   }

@@ -53,6 +53,8 @@ struct Params {
   const double* lvlTn;          // T_norm(r) in S units
   const int* lvlAnn;            // annulus half-width w(r)
   int wstride;
+  const uint32_t* lvlWP;        // [n_levels][4 alignments][wp_nw][2] byte-plane weight words (K2 dp4a rows)
+  int wp_nw;                    // weight words per row and alignment
   // ridge bins (K1 output)
   int nbx, nby;                 // 32x32 bins per frame
   int ridge_cap;                // per bin
