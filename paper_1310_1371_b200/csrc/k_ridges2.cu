@@ -28,8 +28,11 @@ constexpr int KS_COLS = 256;        // strip columns = threads per CTA
 constexpr int KS_HALO = 16;         // halo columns on each side (>= K_s + 3)
 constexpr int KS_OUT = KS_COLS - 2 * KS_HALO;   // 224 output columns = 7 bins
 constexpr int KS_NB = KS_OUT / 32;  // bins per strip
+#ifndef RD_K1_MINB
+#define RD_K1_MINB 3
+#endif
 #ifndef RD_K1_RB
-#define RD_K1_RB 4
+#define RD_K1_RB 2
 #endif
 constexpr double NOT_CAND = 2.0;    // rho.x of a pixel that is not a ridge candidate (|rho.x| <= 1)
 
@@ -45,7 +48,7 @@ struct K1SSmem {                       // dynamic shared memory of k_ridges2
 }  // namespace
 
 template <typename PixT, int KS, int RB>
-__global__ void __launch_bounds__(KS_COLS, 2)
+__global__ void __launch_bounds__(KS_COLS, RD_K1_MINB)
 k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, int seg_rows, Params P) {
   constexpr int NTAP = 2 * KS + 1;
   constexpr int NR = RB + 2;        // kappa / rho ring rows
