@@ -62,8 +62,8 @@ typedef struct rd_config {
   int32_t annulus_halfwidth;      /* 0: max(2, ceil(2 sigma(r))); else fixed w >= 1 */
   int32_t max_rings_per_frame;    /* output capacity per frame (default 1024) */
   int32_t max_ridges_per_tile;    /* ridges per 32x32 tile (default 512) */
-  int32_t max_entries_per_tile;   /* voting rays per 64x64 Hough tile (default 2048) */
-  int32_t max_hotspots_per_level; /* hotspots per Hough tile per level (default 160; cfg3/cfg4 peak at 76) */
+  int32_t max_entries_per_tile;   /* voting rays per Hough tile (default 3072; tiles are 96x96 or 64x64) */
+  int32_t max_hotspots_per_level; /* hotspots per Hough tile per level (default 224) */
   int32_t debug;                  /* 1: keep hotspot records for rd_dump_hotspots */
 } rd_config;
 

@@ -609,7 +609,7 @@ bool k_hough2_has_shape(int cb, int G, int nt, int minb) {
     return (G == 4 && nt == 384 && minb == 2) || (G == 4 && nt == 512 && minb == 2) ||
            (G == 8 && nt == 384 && minb == 2) || (G == 8 && nt == 512 && minb == 1) ||
            (G == 4 && nt == 256 && minb == 3) || (G == 8 && nt == 256 && minb == 2) ||
-           (G == 2 && nt == 256 && minb == 4) || (G == 2 && nt == 256 && minb == 3);
+           (G == 4 && nt == 512 && minb == 1) || (G == 4 && nt == 768 && minb == 1);
   return (G == 4 && nt == 384 && minb == 2) || (G == 4 && nt == 512 && minb == 2) ||
          (G == 8 && nt == 512 && minb == 1) || (G == 4 && nt == 512 && minb == 1);
 }
@@ -630,8 +630,8 @@ cudaError_t launch_hough2(int n_frames, const Params& P, bool wide, int G, int n
     CASE(1, 8, 512, 1)
     CASE(1, 4, 256, 3)
     CASE(1, 8, 256, 2)
-    CASE(1, 2, 256, 4)
-    CASE(1, 2, 256, 3)
+    CASE(1, 4, 512, 1)
+    CASE(1, 4, 768, 1)
     CASE(2, 4, 384, 2)
     CASE(2, 4, 512, 2)
     CASE(2, 8, 512, 1)

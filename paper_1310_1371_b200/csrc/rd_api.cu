@@ -123,8 +123,8 @@ rd_status rd_config_init(rd_config* c, int32_t width, int32_t height, int32_t pi
   c->annulus_halfwidth = 0;
   c->max_rings_per_frame = 1024;
   c->max_ridges_per_tile = 512;
-  c->max_entries_per_tile = 2048;
-  c->max_hotspots_per_level = 160;
+  c->max_entries_per_tile = 3072;
+  c->max_hotspots_per_level = 224;
   c->debug = 0;
   return RD_OK;
 }
@@ -154,8 +154,8 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   rd_config c = *cin;
   if (!c.max_rings_per_frame) c.max_rings_per_frame = 1024;
   if (!c.max_ridges_per_tile) c.max_ridges_per_tile = 512;
-  if (!c.max_entries_per_tile) c.max_entries_per_tile = 2048;
-  if (!c.max_hotspots_per_level) c.max_hotspots_per_level = 160;
+  if (!c.max_entries_per_tile) c.max_entries_per_tile = 3072;
+  if (!c.max_hotspots_per_level) c.max_hotspots_per_level = 224;
   if (c.max_ridges_per_tile > T1 * T1) c.max_ridges_per_tile = T1 * T1;
   if (c.max_hotspots_per_level > 4095) return RD_ERR_PARAM;   // 12-bit hotspot index in K2 task lists
   if (c.max_entries_per_tile > k_hough_max_entries()) c.max_entries_per_tile = k_hough_max_entries();
@@ -257,22 +257,28 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   det->k2_impl = 2;
   if (const char* env = getenv("RD_K2_IMPL")) det->k2_impl = atoi(env) == 1 ? 1 : 2;
   if (det->k2_impl == 2) {
-    // persistent K2, T = 64: the first (G, threads, CTAs/SM) candidate whose layout fits with at
+    // persistent K2: the first (T, G, threads, CTAs/SM) candidate whose layout fits with at
     // least 256 resident rays per tile, then as many resident rays as fit (up to entry_cap).
-    // RD_K2_SHAPE2="G,threads,ctas" puts a shape first; RD_K2_CB=2 forces 16-bit counters.
-    auto pick = [&](Params& Q, int cb, int& G, int& nt, int& minb) {
-      std::vector<Shape> sh = cb == 1 ? std::vector<Shape>{{64, 4, 256, 3}, {64, 4, 384, 2}, {64, 8, 512, 1}}
+    // The 16-bit redo pass must use the main pass's tile side (K1.5 routes rays per tile).
+    // RD_K2_SHAPE2="G,threads,ctas" or "T,G,threads,ctas" puts a shape first;
+    // RD_K2_CB=2 forces 16-bit counters.
+    auto pick = [&](Params& Q, int cb, int& G, int& nt, int& minb, int forceT) {
+      std::vector<Shape> sh = cb == 1 ? std::vector<Shape>{{96, 4, 512, 2}, {64, 4, 256, 3}, {64, 4, 384, 2},
+                                                           {64, 8, 512, 1}}
                                       : std::vector<Shape>{{64, 4, 384, 2}, {64, 4, 512, 2}, {64, 8, 512, 1},
                                                            {64, 4, 512, 1}};
-      if (const char* env = getenv("RD_K2_SHAPE2")) {
+      if (const char* env = getenv("RD_K2_SHAPE2")) {   // "G,threads,ctas" or "T,G,threads,ctas"
         Shape s{64, 0, 0, 0};
-        if (sscanf(env, "%d,%d,%d", &s.G, &s.nt, &s.minb) == 3 && k_hough2_has_shape(cb, s.G, s.nt, s.minb))
+        const int n = sscanf(env, "%d,%d,%d,%d", &s.T, &s.G, &s.nt, &s.minb);
+        if (n == 3) s = Shape{64, s.T, s.G, s.nt};
+        if ((n == 3 || n == 4) && s.T >= 32 && s.T <= 128 && k_hough2_has_shape(cb, s.G, s.nt, s.minb))
           sh.insert(sh.begin(), s);
       }
       G = 0;
       for (const Shape& s : sh) {
         if (!k_hough2_has_shape(cb, s.G, s.nt, s.minb)) continue;
-        Q.k2t = s.T;
+        if (cb == 1 && Q.wstride - 1 > 15) break;   // byte-counter windows: 2K + 1 <= 31 rows per half-warp
+        Q.k2t = forceT ? forceT : s.T;
         const size_t limit = s.minb == 1 ? smax : std::min(smax, sm_sm / s.minb - 1024);
           Q.k2_rcap = 256;
         if (k_hough2_layout(Q, s.G, s.nt, cb) > limit) continue;
@@ -293,9 +299,9 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
     };
     det->k2_cb = 1;
     if (const char* env = getenv("RD_K2_CB")) det->k2_cb = atoi(env) == 2 ? 2 : 1;
+    if (det->k2_cb == 1) pick(P, 1, det->G, det->k2_threads, det->k2_minb, 0);
     det->P16 = P;
-    pick(det->P16, 2, det->G16, det->k2_threads16, det->k2_minb16);
-    if (det->k2_cb == 1) pick(P, 1, det->G, det->k2_threads, det->k2_minb);
+    pick(det->P16, 2, det->G16, det->k2_threads16, det->k2_minb16, det->G ? P.k2t : 0);
     if (det->G == 0 && det->G16 != 0) {   // 16-bit counters as the only pass
       det->k2_cb = 2;
       P.k2t = det->P16.k2t;
