@@ -59,7 +59,8 @@ __global__ void __launch_bounds__(K3_THREADS) k_fit(Params P, Ring* __restrict__
   }
   __syncthreads();
   const int64_t fbins = (int64_t)f * P.nbx * P.nby;
-  for (int p = warp; p < npk; p += K3_THREADS / 32) {
+  // the frame's rings are dealt to gridDim.y CTAs (each ranks all peaks: the sort is cheap)
+  for (int p = warp * gridDim.y + blockIdx.y; p < npk; p += (K3_THREADS / 32) * gridDim.y) {
     const Peak pk = sp[order[p]];
     const int w = P.lvlAnn[pk.r - P.r_lo];
     const long long lo = max(pk.r - w, 0), hi = (long long)pk.r + w;
@@ -131,7 +132,7 @@ __global__ void __launch_bounds__(K3_THREADS) k_fit(Params P, Ring* __restrict__
       rings[(int64_t)f * P.ring_cap + p] = g;
     }
   }
-  if (tid == 0) {
+  if (tid == 0 && blockIdx.y == 0) {
     counts[f] = npk;
     P.stats[f].peaks = (unsigned long long)npk;
   }
@@ -142,7 +143,7 @@ size_t k_fit_smem(const Params& P) { return (size_t)P.ring_cap * (sizeof(Peak) +
 cudaError_t launch_fit(int n_frames, const Params& P, void* rings, int* counts, cudaStream_t st) {
   size_t sm = k_fit_smem(P);
   cudaFuncSetAttribute(k_fit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_fit<<<n_frames, K3_THREADS, sm, st>>>(P, reinterpret_cast<Ring*>(rings), counts);
+  k_fit<<<dim3(n_frames, 4), K3_THREADS, sm, st>>>(P, reinterpret_cast<Ring*>(rings), counts);
   return cudaGetLastError();
 }
 
