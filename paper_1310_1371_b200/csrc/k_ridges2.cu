@@ -18,6 +18,7 @@
 // explicit-rounding recipe (rd_internal.cuh).  Replicate border: input rows and columns are
 // clamped at load time.
 #include <algorithm>
+#include <cmath>
 
 #include "rd_internal.cuh"
 
@@ -247,12 +248,33 @@ template <typename PixT, int KS>
 static cudaError_t launch_s(const void* frames, int64_t pitch, int64_t fstride, int n_frames, const Params& P,
                             cudaStream_t st) {
   constexpr int RB = RD_K1_RB;
-  // segments of whole bin rows: about two per frame
-  const int seg = std::max(T1, ((P.H + 1) / 2 + T1 - 1) / T1 * T1);
-  dim3 grid((P.W + KS_OUT - 1) / KS_OUT, (P.H + seg - 1) / seg, n_frames);
   // dynamic shared memory: rings + rows (NR = RB + 2 rows of rho and kappa)
   const size_t sm = sizeof(K1SSmem<RB>);
   cudaFuncSetAttribute(k_ridges2<PixT, KS, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  // segments of whole bin rows: the count that best fills the resident CTA slots, each
+  // segment paying 3K_s + 6 rows of pipeline warm-up
+  static int slots = 0;
+  if (!slots) {
+    int dev = 0, nsm = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_ridges2<PixT, KS, RB>, KS_COLS, sm);
+    slots = std::max(1, nsm * std::max(per, 1));
+  }
+  const int strips = (P.W + KS_OUT - 1) / KS_OUT, bin_rows = (P.H + T1 - 1) / T1;
+  int seg = bin_rows * T1;
+  double best = -1.0;
+  for (int nseg = 1; nseg <= std::min(bin_rows, 8); ++nseg) {
+    const int sr = (bin_rows + nseg - 1) / nseg * T1;            // rows per segment
+    const int ns = (P.H + sr - 1) / sr;
+    const double ctas = (double)strips * ns * n_frames, waves = ctas / slots;
+    const double eff = waves / std::ceil(waves) * (double)P.H / (P.H + ns * (3.0 * KS + 6.0));
+    if (eff > best + 1e-9) {
+      best = eff;
+      seg = sr;
+    }
+  }
+  dim3 grid(strips, (P.H + seg - 1) / seg, n_frames);
   k_ridges2<PixT, KS, RB><<<grid, KS_COLS, sm, st>>>((const uint8_t*)frames, pitch, fstride, seg, P);
   return cudaGetLastError();
 }
