@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define RD_ABI_VERSION 1
+#define RD_ABI_VERSION 2
 
 typedef enum rd_status {
   RD_OK = 0,
@@ -65,7 +65,16 @@ typedef struct rd_config {
   int32_t max_entries_per_tile;   /* voting rays per Hough tile (default 3072; tiles are 96x96 or 64x64) */
   int32_t max_hotspots_per_level; /* hotspots per Hough tile per level (default 224) */
   int32_t debug;                  /* 1: keep hotspot records for rd_dump_hotspots */
+  /* ABI 2: feature selection ("replaced by directed edges ... replacing the
+   * Hessian by the Gradient ... the gradient magnitude ... a local maximum along the gradient
+   * direction"; reading R19).  RD_FEATURE_EDGE uses the 5x5 first-order Sobel gradient;
+   * curvature_threshold is then ignored and edge_threshold (> 0, counts/px of the smoothed
+   * image) selects candidates |grad| > edge_threshold.  Requires sigma_s <= 4.3 (K_s <= 13). */
+  int32_t feature;                /* RD_FEATURE_RIDGE (0, default) | RD_FEATURE_EDGE (1)  -> RD_ERR_PARAM */
+  double edge_threshold;          /* > 0 when feature == RD_FEATURE_EDGE                   -> RD_ERR_PARAM */
 } rd_config;
+
+enum { RD_FEATURE_RIDGE = 0, RD_FEATURE_EDGE = 1 };
 
 /* One detected ring, 64 bytes.  (cx, cy, r, raw_votes, score_fixed, inliers,
  * fit_ok) are bit-exact; (fx, fy, fr, rms) agree with the oracle to 1e-4 px. */

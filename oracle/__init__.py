@@ -21,7 +21,8 @@ class Params(C.Structure):
                 ("smoothing_sigma", C.c_double), ("curvature_threshold", C.c_double),
                 ("r_min", C.c_int32), ("r_max", C.c_int32), ("vote_threshold_raw", C.c_int32),
                 ("vote_threshold_norm", C.c_double), ("sig_a", C.c_int32), ("sig_b", C.c_int32),
-                ("sig_den", C.c_int32), ("annulus_halfwidth", C.c_int32)]
+                ("sig_den", C.c_int32), ("annulus_halfwidth", C.c_int32), ("feature", C.c_int32),
+                ("edge_threshold", C.c_double)]
 
 
 RIDGE_DTYPE = np.dtype([("x", "i4"), ("y", "i4"), ("dx", "f8"), ("dy", "f8"), ("kappa", "f8")])
@@ -54,6 +55,10 @@ def lib():
         L.orc_norm_threshold.restype = C.c_double
         L.orc_curvature_threshold_int.argtypes = [P]
         L.orc_curvature_threshold_int.restype = C.c_double
+        L.orc_edge_threshold_int2.argtypes = [P]
+        L.orc_edge_threshold_int2.restype = C.c_double
+        L.orc_gradient.argtypes = [P, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.orc_gradient.restype = None
         L.orc_smooth.argtypes = [P, C.c_void_p, C.c_int64, C.c_void_p]
         L.orc_hessian.argtypes = [P, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.orc_eigen.argtypes = [C.c_double, C.c_double, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_double),
@@ -141,6 +146,18 @@ def hessian(p, G):
     out = [np.zeros((p.height, p.width), dtype=np.float64) for _ in range(3)]
     lib().orc_hessian(C.byref(p), G.ctypes.data, *[o.ctypes.data for o in out])
     return tuple(out)  # Ixx, Iyy, Ixy
+
+
+def gradient(p, G):
+    """Edge variant (NEXT-2, R19): 5x5 first-order Sobel gradient (Ix, Iy) of G."""
+    G = np.ascontiguousarray(G, dtype=np.float64)
+    Ix, Iy = (np.zeros((p.height, p.width), dtype=np.float64) for _ in range(2))
+    lib().orc_gradient(C.byref(p), G.ctypes.data, Ix.ctypes.data, Iy.ctypes.data)
+    return Ix, Iy
+
+
+def edge_threshold_int2(p):
+    return lib().orc_edge_threshold_int2(C.byref(p))
 
 
 def eigen(a, b, c):

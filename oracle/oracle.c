@@ -155,6 +155,54 @@ void orc_hessian(const orc_params* p, const double* G, double* Ixx, double* Iyy,
   free(hd1);
 }
 
+/* Edge variant (NEXT-2): "replacing the Hessian by the Gradient ... the gradient magnitude
+ * replacing kappa has to be a local maximum along the gradient direction".
+ * Reading R19: OpenCV's first-order 5x5 Sobel, correlation form, Ix = s5_y (x) d1_x and
+ * Iy = d1_y (x) s5_x, evaluated separably like orc_hessian; valid on [2,W-3]x[2,H-3]. */
+void orc_gradient(const orc_params* p, const double* G, double* Ix, double* Iy) {
+  const int W = p->width, H = p->height;
+  memset(Ix, 0, sizeof(double) * (size_t)W * H);
+  memset(Iy, 0, sizeof(double) * (size_t)W * H);
+  double* hs5 = (double*)calloc((size_t)W * H, sizeof(double));
+  double* hd1 = (double*)calloc((size_t)W * H, sizeof(double));
+  for (int y = 0; y < H; ++y)
+    for (int x = 2; x <= W - 3; ++x) {
+      double b = 0, c = 0;
+      for (int j = -2; j <= 2; ++j) {
+        double g = G[(size_t)y * W + x + j];
+        b += S5[j + 2] * g;
+        c += D1[j + 2] * g;
+      }
+      hs5[(size_t)y * W + x] = b;
+      hd1[(size_t)y * W + x] = c;
+    }
+  for (int y = 2; y <= H - 3; ++y)
+    for (int x = 2; x <= W - 3; ++x) {
+      double gx = 0, gy = 0;
+      for (int i = -2; i <= 2; ++i) {
+        size_t k = (size_t)(y + i) * W + x;
+        gx += S5[i + 2] * hd1[k];
+        gy += D1[i + 2] * hs5[k];
+      }
+      Ix[(size_t)y * W + x] = gx;
+      Iy[(size_t)y * W + x] = gy;
+    }
+  free(hs5);
+  free(hd1);
+}
+
+/* A ramp I = g x gives Ix = 8 (d1) * 16 (s5) * (sum q)^2 * g, so a threshold t_e in counts/px
+ * is t_e * 128 (sum q)^2 in gradient units; squared (fp64) because magnitudes are compared
+ * squared (R19). */
+double orc_edge_threshold_int2(const orc_params* p) {
+  int32_t q[64];
+  int32_t K = orc_gauss_taps(p->smoothing_sigma, q, 64);
+  int64_t sq = 0;
+  for (int i = 0; i <= 2 * K; ++i) sq += q[i];
+  double t = p->edge_threshold * (128.0 * (double)sq * (double)sq);
+  return t * t;
+}
+
 /* ------------------------------------------------------------------ step 3 */
 /* kappa = smaller eigenvalue of the Hessian [[a,b],[b,c]], rho = its unit
  * eigenvector ("the smaller principal curvature and the
@@ -214,6 +262,54 @@ static void ws_free(ws_t* w) {
   free(w->G); free(w->Ixx); free(w->Iyy); free(w->Ixy); free(w->K); free(w->DX); free(w->DY); free(w->DEG);
 }
 
+/* Edge pixels (NEXT-2, reading R19): m2 = Ix*Ix + Iy*Iy (each operation
+ * rounded, no FMA) replaces kappa; a candidate has m2 > (t_e 128 (sum q)^2)^2; rho = (Ix, Iy)/
+ * sqrt(m2); m2 must be a local maximum along rho with the R6 tie rule mirrored:
+ * m2_p >= m2(after) and m2_p > m2(before).  Candidates lie in [3,W-4]x[3,H-4].  The edge list
+ * reuses orc_ridge records (kappa field = m2).  w->G holds the smoothed frame. */
+static int64_t edges_ws(const orc_params* p, ws_t* w, orc_ridge* out, int64_t cap) {
+  const int W = p->width, H = p->height;
+  orc_gradient(p, w->G, w->Ixx, w->Iyy);   /* Ix, Iy in the Ixx, Iyy buffers */
+  for (size_t k = 0; k < (size_t)W * H; ++k) {
+    double gx = w->Ixx[k], gy = w->Iyy[k];
+    double m2 = gx * gx + gy * gy;
+    w->K[k] = m2;
+    if (m2 > 0.0) {
+      double n = sqrt(m2);
+      w->DX[k] = gx / n;
+      w->DY[k] = gy / n;
+    } else {
+      w->DX[k] = 0.0;
+      w->DY[k] = 0.0;
+    }
+  }
+  const double t2 = orc_edge_threshold_int2(p);
+  int64_t n = 0;
+  for (int y = 3; y <= H - 4; ++y)
+    for (int x = 3; x <= W - 4; ++x) {
+      size_t k = (size_t)y * W + x;
+      double mp = w->K[k];
+      if (!(mp > t2)) continue;
+      int ox = (int)llround(w->DX[k]), oy = (int)llround(w->DY[k]);
+      int after_plus = (oy > 0) || (oy == 0 && ox > 0);
+      double m_plus = w->K[(size_t)(y + oy) * W + (x + ox)];
+      double m_minus = w->K[(size_t)(y - oy) * W + (x - ox)];
+      double m_after = after_plus ? m_plus : m_minus;
+      double m_before = after_plus ? m_minus : m_plus;
+      if (mp >= m_after && mp > m_before) {
+        if (n < cap) {
+          out[n].x = x;
+          out[n].y = y;
+          out[n].dx = w->DX[k];
+          out[n].dy = w->DY[k];
+          out[n].kappa = mp;
+        }
+        ++n;
+      }
+    }
+  return n;
+}
+
 /* Ridge pixels ("(i) kappa < 0; (ii) kappa is a local minimum
  * along rho"; SI step 2 PAPER.md:926-931 "smaller than a pre-defined curvature
  * threshold (the latter is no greater than zero) ... local minimum along the
@@ -225,6 +321,7 @@ static int64_t ridges_ws(const orc_params* p, ws_t* w, const void* frame, int64_
                          int64_t cap) {
   const int W = p->width, H = p->height;
   orc_smooth(p, frame, pitch, w->G);
+  if (p->feature == 1) return edges_ws(p, w, out, cap);
   orc_hessian(p, w->G, w->Ixx, w->Iyy, w->Ixy);
   for (int y = 2; y <= H - 3; ++y)
     for (int x = 2; x <= W - 3; ++x) {
@@ -454,7 +551,9 @@ static int params_ok(const orc_params* p) {
   if (p->width < 5 || p->height < 5) return 0;
   if (p->pixel_bytes != 1 && p->pixel_bytes != 2) return 0;
   if (!(p->smoothing_sigma > 0) || p->smoothing_sigma > 10) return 0;
-  if (!(p->curvature_threshold <= 0)) return 0;
+  if (p->feature != 0 && p->feature != 1) return 0;
+  if (p->feature == 0 && !(p->curvature_threshold <= 0)) return 0;
+  if (p->feature == 1 && !(p->edge_threshold > 0)) return 0;
   if (p->r_min < 2 || p->r_max <= p->r_min) return 0;
   if (p->vote_threshold_raw < 1 || !(p->vote_threshold_norm > 0)) return 0;
   if (p->sig_a < 0 || p->sig_den <= 0 || p->sig_a * p->r_min + p->sig_b <= 0) return 0;

@@ -30,6 +30,8 @@ typedef struct orc_params {
   double vote_threshold_norm;   /* tau: candidate iff N > tau*2*pi */
   int32_t sig_a, sig_b, sig_den;/* sigma(r) = (a r + b)/den = 0.05 r + 0.25 */
   int32_t annulus_halfwidth;    /* 0: max(2, ceil(2 sigma(r))) */
+  int32_t feature;              /* 0: directed ridges (Hessian); 1: directed edges (gradient) */
+  double edge_threshold;        /* edges: |grad| > this, counts/px of the sigma_s-smoothed image (R19) */
 } orc_params;
 
 typedef struct orc_ridge { int32_t x, y; double dx, dy, kappa; } orc_ridge;
@@ -56,6 +58,11 @@ int32_t orc_annulus_halfwidth(const orc_params* p, int32_t r);
 void orc_smooth(const orc_params* p, const void* frame, int64_t pitch_bytes, double* G);
 /* step 2: 5x5 second-order Sobel (correlation) on [2,W-3]x[2,H-3]; outside = 0 */
 void orc_hessian(const orc_params* p, const double* G, double* Ixx, double* Iyy, double* Ixy);
+/* step 2 (edge variant, R19): 5x5 first-order Sobel gradient Ix = s5_y (x) d1_x, Iy = d1_y (x) s5_x
+ * on [2,W-3]x[2,H-3]; outside = 0 */
+void orc_gradient(const orc_params* p, const double* G, double* Ix, double* Iy);
+/* edge threshold in the units of the squared integer gradient: (t_e * 128 * (sum q)^2)^2 */
+double orc_edge_threshold_int2(const orc_params* p);
 /* step 3: least principal curvature and its unit eigenvector; returns 1 if degenerate */
 int orc_eigen(double a, double b, double c, double* kappa, double* dx, double* dy);
 /* steps 1-4: ridge list in row-major order; returns count (<= cap written) */

@@ -25,7 +25,8 @@ class rd_config(C.Structure):
                 ("vote_threshold_norm", C.c_double), ("sig_a", C.c_int32), ("sig_b", C.c_int32),
                 ("sig_den", C.c_int32), ("annulus_halfwidth", C.c_int32), ("max_rings_per_frame", C.c_int32),
                 ("max_ridges_per_tile", C.c_int32), ("max_entries_per_tile", C.c_int32),
-                ("max_hotspots_per_level", C.c_int32), ("debug", C.c_int32)]
+                ("max_hotspots_per_level", C.c_int32), ("debug", C.c_int32), ("feature", C.c_int32),
+                ("edge_threshold", C.c_double)]
 
 
 RING_DTYPE = np.dtype([("cx", "i4"), ("cy", "i4"), ("r", "i4"), ("raw_votes", "i4"), ("score_fixed", "i8"),

@@ -434,7 +434,9 @@ cudaError_t launch_ridges(const void* frames, int64_t pitch, int64_t fstride, in
                           cudaStream_t st) {
   // column-streaming K1 (k_ridges2.cu) unless K_s exceeds its halo or RD_K1_IMPL=1 asks for the tiled one
   static const bool tiled = getenv("RD_K1_IMPL") && atoi(getenv("RD_K1_IMPL")) == 1;
-  if (!tiled && ridges_stream_ok(P)) return launch_ridges_stream(frames, pitch, fstride, n_frames, P, st);
+  if ((!tiled || P.feature == 1) && ridges_stream_ok(P))   // edges exist in the streaming K1 only
+    return launch_ridges_stream(frames, pitch, fstride, n_frames, P, st);
+  if (P.feature == 1) return cudaErrorInvalidValue;
   if (P.pixel_bytes == 1) return launch_p<uint8_t>(frames, pitch, fstride, n_frames, P, st);
   return launch_p<uint16_t>(frames, pitch, fstride, n_frames, P, st);
 }

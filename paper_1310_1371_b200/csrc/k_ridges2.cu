@@ -48,7 +48,7 @@ struct K1SSmem {                       // dynamic shared memory of k_ridges2
 };
 }  // namespace
 
-template <typename PixT, int KS, int RB>
+template <typename PixT, int KS, int RB, bool EDGE>
 __global__ void __launch_bounds__(KS_COLS, RD_K1_MINB)
 k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, int seg_rows, Params P) {
   constexpr int NTAP = 2 * KS + 1;
@@ -71,7 +71,8 @@ k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, in
   const int xc = min(max(x, 0), W - 1);               // clamped (replicate border)
   const uint8_t* frame = frames + (int64_t)f * fstride;
   const int* q = P.q;   // taps stay in the constant bank
-  const double t_int = P.t_int;
+  const double t_int = P.t_int, t_edge2 = P.t_edge2;
+  constexpr bool edge = EDGE;   // directed edges (NEXT-2) instead of ridges, a separate instance
   // which columns compute what: R on [KS, 256-KS), G..H on [13, 243), output on [16, 240)
   const bool doR = tid >= KS && tid < KS_COLS - KS;
   const bool doH = tid >= KS_HALO - 3 && tid < KS_COLS - KS_HALO + 3;
@@ -199,16 +200,26 @@ k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, in
       wA[4] = ha;
       wB[4] = hb;
       wC[4] = hc;
-      double kap = HUGE_VAL;
+      double kap = edge ? 0.0 : HUGE_VAL;
       double2 dir = make_double2(NOT_CAND, 0.0);
       if (colH && yk >= 2 && yk <= H - 3) {
-        const double Ixx = (wA[0] + wA[4]) + 4.0 * (wA[1] + wA[3]) + 6.0 * wA[2];
-        const double Iyy = (wB[0] + wB[4]) - 2.0 * wB[2];
-        const double Ixy = (wC[4] - wC[0]) + 2.0 * (wC[3] - wC[1]);
-        double sq, e;
-        kap = kappa_of(Ixx, Ixy, Iyy, &sq, &e);
-        double dx, dy;
-        if (kap < t_int && direction_of(Ixy, e, sq, &dx, &dy)) dir = make_double2(dx, dy);   // R3
+        if (!edge) {
+          const double Ixx = (wA[0] + wA[4]) + 4.0 * (wA[1] + wA[3]) + 6.0 * wA[2];
+          const double Iyy = (wB[0] + wB[4]) - 2.0 * wB[2];
+          const double Ixy = (wC[4] - wC[0]) + 2.0 * (wC[3] - wC[1]);
+          double sq, e;
+          kap = kappa_of(Ixx, Ixy, Iyy, &sq, &e);
+          double dx, dy;
+          if (kap < t_int && direction_of(Ixy, e, sq, &dx, &dy)) dir = make_double2(dx, dy);   // R3
+        } else {   // edge variant (NEXT-2, R19): Ix = s5_y (x) d1_x, Iy = d1_y (x) s5_x, m2 = |grad|^2
+          const double Ix = (wC[0] + wC[4]) + 4.0 * (wC[1] + wC[3]) + 6.0 * wC[2];
+          const double Iy = (wB[4] - wB[0]) + 2.0 * (wB[3] - wB[1]);
+          kap = __dadd_rn(__dmul_rn(Ix, Ix), __dmul_rn(Iy, Iy));
+          if (kap > t_edge2) {
+            const double n = __dsqrt_rn(kap);
+            dir = make_double2(__ddiv_rn(Ix, n), __ddiv_rn(Iy, n));
+          }
+        }
       }
       const int slot = (yk - ybase) % NR;
       sK[slot][tid] = kap;
@@ -233,7 +244,8 @@ k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, in
           const double kplus = sK[oy > 0 ? sp : (oy < 0 ? sm : s0)][tid + ox];
           const double kminus = sK[oy > 0 ? sm : (oy < 0 ? sp : s0)][tid - ox];
           const double kafter = after_plus ? kplus : kminus, kbefore = after_plus ? kminus : kplus;
-          is_r = (kp <= kafter) && (kp < kbefore);
+          // ridges: kappa a local minimum along rho (R6); edges: |grad|^2 a local maximum (R19)
+          is_r = edge ? (kp >= kafter) && (kp > kbefore) : (kp <= kafter) && (kp < kbefore);
         }
       }
       const unsigned bal = __ballot_sync(0xffffffffu, is_r);
@@ -244,13 +256,13 @@ k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, in
   }
 }
 
-template <typename PixT, int KS>
+template <typename PixT, int KS, bool EDGE>
 static cudaError_t launch_s(const void* frames, int64_t pitch, int64_t fstride, int n_frames, const Params& P,
                             cudaStream_t st) {
   constexpr int RB = RD_K1_RB;
   // dynamic shared memory: rings + rows (NR = RB + 2 rows of rho and kappa)
   const size_t sm = sizeof(K1SSmem<RB>);
-  cudaFuncSetAttribute(k_ridges2<PixT, KS, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaFuncSetAttribute(k_ridges2<PixT, KS, RB, EDGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   // segments of whole bin rows: the count that best fills the resident CTA slots, each
   // segment paying 3K_s + 6 rows of pipeline warm-up
   static int slots = 0;
@@ -258,7 +270,7 @@ static cudaError_t launch_s(const void* frames, int64_t pitch, int64_t fstride, 
     int dev = 0, nsm = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_ridges2<PixT, KS, RB>, KS_COLS, sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_ridges2<PixT, KS, RB, EDGE>, KS_COLS, sm);
     slots = std::max(1, nsm * std::max(per, 1));
   }
   const int strips = (P.W + KS_OUT - 1) / KS_OUT, bin_rows = (P.H + T1 - 1) / T1;
@@ -275,27 +287,27 @@ static cudaError_t launch_s(const void* frames, int64_t pitch, int64_t fstride, 
     }
   }
   dim3 grid(strips, (P.H + seg - 1) / seg, n_frames);
-  k_ridges2<PixT, KS, RB><<<grid, KS_COLS, sm, st>>>((const uint8_t*)frames, pitch, fstride, seg, P);
+  k_ridges2<PixT, KS, RB, EDGE><<<grid, KS_COLS, sm, st>>>((const uint8_t*)frames, pitch, fstride, seg, P);
   return cudaGetLastError();
 }
 
-template <typename PixT>
+template <typename PixT, bool EDGE>
 static cudaError_t launch_sp(const void* frames, int64_t pitch, int64_t fstride, int n, const Params& P,
                              cudaStream_t st) {
   switch (P.Ks) {
-    case 1: return launch_s<PixT, 1>(frames, pitch, fstride, n, P, st);
-    case 2: return launch_s<PixT, 2>(frames, pitch, fstride, n, P, st);
-    case 3: return launch_s<PixT, 3>(frames, pitch, fstride, n, P, st);
-    case 4: return launch_s<PixT, 4>(frames, pitch, fstride, n, P, st);
-    case 5: return launch_s<PixT, 5>(frames, pitch, fstride, n, P, st);
-    case 6: return launch_s<PixT, 6>(frames, pitch, fstride, n, P, st);
-    case 7: return launch_s<PixT, 7>(frames, pitch, fstride, n, P, st);
-    case 8: return launch_s<PixT, 8>(frames, pitch, fstride, n, P, st);
-    case 9: return launch_s<PixT, 9>(frames, pitch, fstride, n, P, st);
-    case 10: return launch_s<PixT, 10>(frames, pitch, fstride, n, P, st);
-    case 11: return launch_s<PixT, 11>(frames, pitch, fstride, n, P, st);
-    case 12: return launch_s<PixT, 12>(frames, pitch, fstride, n, P, st);
-    case 13: return launch_s<PixT, 13>(frames, pitch, fstride, n, P, st);
+    case 1: return launch_s<PixT, 1, EDGE>(frames, pitch, fstride, n, P, st);
+    case 2: return launch_s<PixT, 2, EDGE>(frames, pitch, fstride, n, P, st);
+    case 3: return launch_s<PixT, 3, EDGE>(frames, pitch, fstride, n, P, st);
+    case 4: return launch_s<PixT, 4, EDGE>(frames, pitch, fstride, n, P, st);
+    case 5: return launch_s<PixT, 5, EDGE>(frames, pitch, fstride, n, P, st);
+    case 6: return launch_s<PixT, 6, EDGE>(frames, pitch, fstride, n, P, st);
+    case 7: return launch_s<PixT, 7, EDGE>(frames, pitch, fstride, n, P, st);
+    case 8: return launch_s<PixT, 8, EDGE>(frames, pitch, fstride, n, P, st);
+    case 9: return launch_s<PixT, 9, EDGE>(frames, pitch, fstride, n, P, st);
+    case 10: return launch_s<PixT, 10, EDGE>(frames, pitch, fstride, n, P, st);
+    case 11: return launch_s<PixT, 11, EDGE>(frames, pitch, fstride, n, P, st);
+    case 12: return launch_s<PixT, 12, EDGE>(frames, pitch, fstride, n, P, st);
+    case 13: return launch_s<PixT, 13, EDGE>(frames, pitch, fstride, n, P, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -305,8 +317,11 @@ bool ridges_stream_ok(const Params& P) { return P.Ks >= 1 && P.Ks <= KS_HALO - 3
 
 cudaError_t launch_ridges_stream(const void* frames, int64_t pitch, int64_t fstride, int n_frames, const Params& P,
                                  cudaStream_t st) {
-  if (P.pixel_bytes == 1) return launch_sp<uint8_t>(frames, pitch, fstride, n_frames, P, st);
-  return launch_sp<uint16_t>(frames, pitch, fstride, n_frames, P, st);
+  if (P.feature == 1)
+    return P.pixel_bytes == 1 ? launch_sp<uint8_t, true>(frames, pitch, fstride, n_frames, P, st)
+                              : launch_sp<uint16_t, true>(frames, pitch, fstride, n_frames, P, st);
+  return P.pixel_bytes == 1 ? launch_sp<uint8_t, false>(frames, pitch, fstride, n_frames, P, st)
+                            : launch_sp<uint16_t, false>(frames, pitch, fstride, n_frames, P, st);
 }
 
 }  // namespace rd

@@ -134,7 +134,11 @@ static rd_status validate(const rd_config* c) {
   if (c->pixel != RD_U8 && c->pixel != RD_U16) return RD_ERR_PARAM;
   if (c->max_value < 1 || c->max_value > (c->pixel == RD_U8 ? 255 : 65535)) return RD_ERR_PARAM;
   if (!(c->smoothing_sigma > 0.0) || !(c->smoothing_sigma <= 5.0)) return RD_ERR_PARAM;
-  if (!(c->curvature_threshold <= 0.0) || !std::isfinite(c->curvature_threshold)) return RD_ERR_PARAM;
+  if (c->feature != RD_FEATURE_RIDGE && c->feature != RD_FEATURE_EDGE) return RD_ERR_PARAM;
+  if (c->feature == RD_FEATURE_RIDGE && (!(c->curvature_threshold <= 0.0) || !std::isfinite(c->curvature_threshold)))
+    return RD_ERR_PARAM;
+  if (c->feature == RD_FEATURE_EDGE && (!(c->edge_threshold > 0.0) || !std::isfinite(c->edge_threshold)))
+    return RD_ERR_PARAM;
   if (c->r_min < 2 || c->r_max <= c->r_min || c->r_max > 1000) return RD_ERR_PARAM;
   if (c->vote_threshold_raw < 1 || c->vote_threshold_raw > 60000) return RD_ERR_PARAM;
   if (!(c->vote_threshold_norm > 0.0) || !std::isfinite(c->vote_threshold_norm)) return RD_ERR_PARAM;
@@ -178,6 +182,13 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   if ((int64_t)c.max_value * sq >= (int64_t(1) << 31)) return RD_ERR_CONFIG;
   if ((double)c.max_value * (double)sq * (double)sq * 64.0 >= 9007199254740992.0) return RD_ERR_CONFIG;
   P.t_int = c.curvature_threshold * (64.0 * (double)sq * (double)sq);
+  P.feature = c.feature;
+  if (c.feature == RD_FEATURE_EDGE && P.Ks > 13) return RD_ERR_CONFIG;   // the streaming K1's 16-column halo
+  if (c.feature == RD_FEATURE_EDGE) {   // R19: |grad| of the 5x5 Sobel of G, compared squared in fp64
+    if ((double)c.max_value * (double)sq * (double)sq * 96.0 >= 9007199254740992.0) return RD_ERR_CONFIG;
+    const double te = c.edge_threshold * (128.0 * (double)sq * (double)sq);
+    P.t_edge2 = te * te;
+  }
   P.r_min = c.r_min;
   P.r_max = c.r_max;
   P.r_lo = c.r_min - 1;

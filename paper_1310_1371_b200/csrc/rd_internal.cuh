@@ -42,6 +42,8 @@ struct Params {
   int Ks;
   int q[2 * KS_MAX + 1];        // smoothing taps, 2^10 fixed point (A1)
   double t_int;                 // curvature threshold in integer-Hessian units
+  int feature;                  // 0: directed ridges; 1: directed edges (NEXT-2, R19)
+  double t_edge2;               // edges: (t_e * 128 (sum q)^2)^2, compared with |grad|^2 in fp64
   int r_lo, r_hi, r_min, r_max, n_levels;
   int T_raw;
   int K_max;                    // largest level half-width

@@ -11,7 +11,8 @@ from ._rd import HOT_DTYPE, RIDGE_DTYPE, RING_DTYPE, STATS_DTYPE, check, lib
 
 _CFG_KEYS = ("max_value", "smoothing_sigma", "curvature_threshold", "r_min", "r_max", "vote_threshold_raw",
              "vote_threshold_norm", "sig_a", "sig_b", "sig_den", "annulus_halfwidth", "max_rings_per_frame",
-             "max_ridges_per_tile", "max_entries_per_tile", "max_hotspots_per_level", "debug")
+             "max_ridges_per_tile", "max_entries_per_tile", "max_hotspots_per_level", "debug", "feature",
+             "edge_threshold")
 
 
 class Detector:

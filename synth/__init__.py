@@ -11,7 +11,7 @@ import os
 
 import numpy as np
 
-from .presets import PRESETS, preset  # noqa: F401
+from .presets import EDGE_THRESHOLD, PRESETS, edge_preset, preset  # noqa: F401
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB = None

@@ -34,7 +34,7 @@ def test_exports_match_header(rdlib):
 
 def test_status_strings_and_version(rdlib):
     L = rdlib.lib()
-    assert L.rd_abi_version() == 1
+    assert L.rd_abi_version() == 2
     for s in range(7):
         assert len(L.rd_status_string(s)) > 0
 

@@ -302,3 +302,25 @@ def test_k2_counter_width_paths_bit_exact(rdmod, knob, monkeypatch):
     det, rings = _run(rdmod, params, frames)
     for i in range(6):
         _check_frame(rdmod, det, i, params, frames[i], rings[i], full=(i < 2))
+
+
+# ---------------------------------------------------------------- NEXT-2: directed edges
+@pytest.mark.parametrize("cfg,n,full", [(1, 4, 4), (2, 4, 2), (3, 2, 1)])
+def test_edge_variant_parity(rdmod, cfg, n, full):
+    """The directed-edge variant (reading R19: 5x5 first-order Sobel,
+    |grad|^2 a local maximum along the gradient) against the oracle: edge sets with the bits
+    of rho, hotspots, peaks and stats bit-exact, fits within 1e-4 px."""
+    params = synth.edge_preset(cfg)
+    frames = np.stack([synth.frame(cfg, 0, i)[0] for i in range(n)]) if cfg == 1 else synth.batch(cfg, 0, 0, n)
+    det, rings = _run(rdmod, params, frames, max_entries_per_tile=4096)
+    for i in range(n):
+        _check_frame(rdmod, det, i, params, frames[i], rings[i], full=(i < full))
+
+
+def test_edge_config_validated(rdmod):
+    """feature must be 0 or 1; edges need a positive, finite edge_threshold."""
+    base = synth.preset(3)
+    for bad in (dict(feature=2), dict(feature=1, edge_threshold=0.0), dict(feature=1, edge_threshold=-3.0)):
+        with pytest.raises(rdmod.RDError):
+            _det(rdmod, dict(base, **bad))
+    _det(rdmod, dict(base, feature=1, edge_threshold=5.0)).close()
