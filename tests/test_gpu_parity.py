@@ -324,3 +324,17 @@ def test_edge_config_validated(rdmod):
         with pytest.raises(rdmod.RDError):
             _det(rdmod, dict(base, **bad))
     _det(rdmod, dict(base, feature=1, edge_threshold=5.0)).close()
+
+
+# ---------------------------------------------------------------- NEXT-3: robustness corpus
+def test_robustness_corpus_gpu_equals_oracle(rdmod):
+    """The GPU rings on the robustness corpus (PAPER.md:611-627 shape) are the oracle's, and
+    their detection rate is what the method reaches there (> 90 %)."""
+    from synth import robust
+    frames, truth = robust.corpus(2026, 32)
+    det, rings = _run(rdmod, robust.PARAMS, frames, debug=0)
+    exp, _ = oracle.detect_batch(oracle.params(**robust.PARAMS), frames)
+    for g, e in zip(rings, exp):
+        _compare_rings(g, e)
+    rates, _ = robust.score(truth, rings)
+    assert rates["detection_rate"] > 0.9 and rates["false_rate"] < 0.05
