@@ -338,3 +338,30 @@ def test_robustness_corpus_gpu_equals_oracle(rdmod):
         _compare_rings(g, e)
     rates, _ = robust.score(truth, rings)
     assert rates["detection_rate"] > 0.9 and rates["false_rate"] < 0.05
+
+
+# ---------------------------------------------------------------- NEXT-4: streaming ingest
+def test_stream_detector_matches_batch(rdmod):
+    """Frames pushed one at a time (a 500 Hz producer thread) through StreamDetector give the
+    batch detector's rings, every frame reported once, in order."""
+    import threading
+    import time
+    from paper_1310_1371_b200.stream import StreamDetector
+    params = synth.preset(2)
+    frames = synth.batch(2, 0, 0, 16)
+    det, ref = _run(rdmod, params, frames, debug=0)
+    sd = StreamDetector(params, slots=8, max_batch=4)
+    seen = []
+
+    def on_result(i, rings, dt):
+        seen.append(i)
+        _compare_rings(rings, ref[i % 16])
+
+    cons = threading.Thread(target=sd.run, kwargs=dict(on_result=on_result))
+    cons.start()
+    for i in range(40):
+        sd.push(frames[i % 16])
+        time.sleep(0.002)
+    sd.close()
+    cons.join()
+    assert seen == list(range(40))
