@@ -90,7 +90,7 @@ size_t k_hough2_layout(Params& P, int G, int nt, int cb) {
   L.task = o;  o = al16(o + 2 * (size_t)G * hot_cap);
   L.cand = o;  o = al16(o + 2 * (size_t)G * hot_cap);
   L.cdef = o;  o = al16(o + 2 * 2 * (size_t)hot_cap);
-  L.act = o;   o = al16(o + 2 * 2 * (size_t)P.entry_cap);
+  L.act = o;   o = al16(o + 2 * (size_t)P.entry_cap);   // one list: written in phase (2), read in (1)
   L.hcnt = o;  o = al16(o + 4 * (size_t)(nlev + 32));
   L.w = o;     o = al16(o + 2 * (size_t)nlev * P.wstride);
   L.k = o;     o = al16(o + 4 * (size_t)nlev);
@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
   uint16_t* tasks = SM(uint16_t, task);         // [G*hot_cap] g<<12 | h (small K front, large K back)
   uint16_t* cand = SM(uint16_t, cand);          // [G*hot_cap] g<<12 | h
   uint16_t* cdef = SM(uint16_t, cdef);          // [2][hot_cap] h, top level of a step
-  uint16_t* act = SM(uint16_t, act);            // [2][entry_cap] rays active in the step, by parity
+  uint16_t* act = SM(uint16_t, act);            // [entry_cap] rays active in the step (next step's from phase 2)
   int* hcnt = SM(int, hcnt);                    // [nlev] hotspots per level + counters
   uint16_t* tW = SM(uint16_t, w);               // [nlev][wstride] w_r(d)
   int* tK = SM(int, k);                         // [nlev] K_r
@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
         int base = 0;
         if (lane == 0) base = atomicAdd(&s_nact[p], __popc(bal));
         base = __shfl_sync(FULL, base, 0);
-        if (a) act[p * ecap + base + __popc(bal & lanemask_lt())] = (uint16_t)e;
+        if (a) act[base + __popc(bal & lanemask_lt())] = (uint16_t)e;
       }
     };
     // the tile's rays (up to rcap) become resident in shared memory
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
           if (i < nact) {
             uint32_t rr, xy;
             double2 d;
-            const int e = act[par * ecap + i];
+            const int e = act[i];
             if (e < rcap) {
               d = sd[e];
               xy = sxy[e];

@@ -274,7 +274,7 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
     // RD_K2_SHAPE2="G,threads,ctas" or "T,G,threads,ctas" puts a shape first;
     // RD_K2_CB=2 forces 16-bit counters.
     auto pick = [&](Params& Q, int cb, int& G, int& nt, int& minb, int forceT) {
-      std::vector<Shape> sh = cb == 1 ? std::vector<Shape>{{96, 4, 512, 2}, {64, 4, 256, 3}, {64, 4, 384, 2},
+      std::vector<Shape> sh = cb == 1 ? std::vector<Shape>{{104, 4, 512, 2}, {96, 4, 512, 2}, {64, 4, 256, 3}, {64, 4, 384, 2},
                                                            {64, 8, 512, 1}}
                                       : std::vector<Shape>{{64, 4, 384, 2}, {64, 4, 512, 2}, {64, 8, 512, 1},
                                                            {64, 4, 512, 1}};

@@ -117,7 +117,7 @@ def test_parity_cfg3_sample(rdmod):
 def test_parity_cfg4_sample(rdmod):
     params = synth.preset(4)
     frames = synth.batch(4, 0, 0, 2)
-    det, rings = _run(rdmod, params, frames, max_entries_per_tile=4096)
+    det, rings = _run(rdmod, params, frames, max_entries_per_tile=6144)
     for i in range(2):
         _check_frame(rdmod, det, i, params, frames[i], rings[i], full=(i < 1))
 
@@ -250,7 +250,7 @@ def test_detect_host_matches_device(rdmod):
 def test_full_batch_cfg4_dense(rdmod):
     """cfg4 at BASELINE size (512 frames of 1024x1024, 200 rings): sampled frames vs the
     oracle; every frame valid (no capacity overflow with the dense-config capacities)."""
-    params = dict(synth.preset(4), max_entries_per_tile=4096, max_hotspots_per_level=512)
+    params = dict(synth.preset(4), max_entries_per_tile=6144, max_hotspots_per_level=512)
     frames = synth.batch(4, 0, 0, 512)
     det = _det(rdmod, params, max_batch=512)
     rings, counts = det.detect(torch.from_numpy(frames).cuda())
