@@ -6,9 +6,9 @@
 // ray's target segment can touch, the ray is appended to the tile's list together with a
 // conservative level interval [ra, rb] (necessary conditions, linear in r because
 // K_r <= m r + c; exactness is restored per vote in K2).
-// One CTA per 32x32 ridge bin: the bin's rays can only reach the tiles of a small window
-// around it, which the CTA walks uniformly; the rays that hit a tile are appended with one
-// global atomic per warp (ballot + popc), so list appends do not contend per ray.
+// A bin's rays can only reach the tiles of a small window around the 32x32 ridge bin, which
+// a warp walks uniformly; the rays that hit a tile are appended with one global atomic per
+// warp and tile (ballot + popc), so list appends do not contend per ray.
 #include "rd_internal.cuh"
 
 namespace rd {
@@ -19,16 +19,19 @@ __device__ __forceinline__ int rnd_half_away(double v) { return __double2int_rz(
 
 // Largest r in [rlo - 1, rhi] such that c + llround(r' d) lies in [0, n - 1] for every r' in
 // [rlo, r]: the target coordinate is monotone in r and starts inside the frame (r = 0), so
-// the in-frame levels of a ray are a prefix of the level range (binary search).
+// the in-frame levels of a ray are a prefix of the level range.  A float estimate of the
+// crossing, then exact steps to the boundary.
+__device__ __forceinline__ bool inframe_at(int c, double d, int n, int r) {
+  const int t = c + rnd_half_away(__dmul_rn((double)r, d));
+  return t >= 0 && t <= n - 1;
+}
 __device__ int inframe_prefix(int c, double d, int n, int rlo, int rhi) {
-  int lo = rlo - 1, hi = rhi;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    const int t = c + rnd_half_away(__dmul_rn((double)mid, d));
-    if (t >= 0 && t <= n - 1) lo = mid;
-    else hi = mid - 1;
-  }
-  return lo;
+  const float fd = (float)d;
+  const float lim = fd > 0.f ? ((float)n - 0.5f - (float)c) / fd : fd < 0.f ? (-0.5f - (float)c) / fd : 1e9f;
+  int r = (int)fminf(fmaxf(floorf(lim), (float)(rlo - 1)), (float)rhi);
+  while (r < rhi && inframe_at(c, d, n, r + 1)) ++r;
+  while (r >= rlo && !inframe_at(c, d, n, r)) --r;
+  return r;
 }
 
 __device__ __forceinline__ void half_ge(float a, float b, float& lo, float& hi) {
@@ -38,89 +41,100 @@ __device__ __forceinline__ void half_ge(float a, float b, float& lo, float& hi) 
 }
 }  // namespace
 
-__global__ void __launch_bounds__(128) k_rays(Params P) {
+// One CTA per (row of ridge bins, frame), one warp per bin at a time (32 rays per pass).
+// The clip of a ray's level interval splits into frame constraints (per ray), row
+// constraints (per tile row ty) and column constraints (per tile column tx), so the inner
+// tile loop evaluates two half-planes with precomputed reciprocals.
+__global__ void __launch_bounds__(256) k_rays(Params P) {
   const int f = blockIdx.y;
-  const int bin = blockIdx.x;
-  const int by = bin / P.nbx, bx = bin - by * P.nbx;
-  const int64_t fb = (int64_t)f * P.nbx * P.nby + bin;
-  const int cnt = P.bin_count[fb];
-  if (cnt == 0) return;
+  const int by = blockIdx.x;
   const int T = P.k2t, hal = P.hal, W = P.W, H = P.H;
   const int rlo = P.r_lo, rhi = P.r_hi;
   const float m = P.k_slope, c = P.k_icpt;
-  const int ntiles = P.ntx * P.nty;
-  const int lane = threadIdx.x & 31;
-  // tiles any ray of this bin can reach: |offset| <= r_hi, halo <= hal
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t tile0 = (int64_t)f * P.ntx * P.nty;
+  // tiles any ray of a bin can reach: |offset| <= r_hi, halo <= hal
   const int reach = rhi + hal + 1;
-  const int wx0 = max((bx * T1 - reach) / T, 0), wx1 = min((bx * T1 + T1 - 1 + reach) / T, P.ntx - 1);
   const int wy0 = max((by * T1 - reach) / T, 0), wy1 = min((by * T1 + T1 - 1 + reach) / T, P.nty - 1);
   int my_votes = 0;
-  for (int j0 = 0; j0 < 2 * cnt; j0 += blockDim.x) {   // uniform trip count across the CTA
-    const int j = j0 + threadIdx.x;
-    const bool valid = j < 2 * cnt;
-    uint32_t xy = 0;
-    double2 d = make_double2(0.0, 0.0);
-    if (valid) {
-      const int64_t g = fb * P.ridge_cap + (j >> 1);
-      xy = P.bin_xy[g];
-      d = P.bin_d[g];
-    }
-    if (!__any_sync(0xffffffffu, valid)) continue;   // warps past the bin's rays skip the window walk
-    const double sgn = (j & 1) ? -1.0 : 1.0;
-    const int x = (int)(xy & 0xFFFFu), y = (int)(xy >> 16);
-    const double u = sgn * d.x, v = sgn * d.y;
-    if (valid) {   // the ray's in-frame votes (per-frame vote count)
-      const int px = inframe_prefix(x, u, W, rlo, rhi), py = inframe_prefix(y, v, H, rlo, rhi);
-      my_votes += max(0, min(px, py) - rlo + 1);
-    }
-    const float fu = (float)u, fv = (float)v, fx = (float)x, fy = (float)y;
-    // bounding box of the target segment, widened by the largest halo and rounding
-    const float ax = fx + fu * rlo, bxp = fx + fu * rhi, ay = fy + fv * rlo, byp = fy + fv * rhi;
-    const float sx0 = fminf(ax, bxp) - hal - 1.f, sx1 = fmaxf(ax, bxp) + hal + 1.f;
-    const float sy0 = fminf(ay, byp) - hal - 1.f, sy1 = fmaxf(ay, byp) + hal + 1.f;
-    for (int ty = wy0; ty <= wy1; ++ty)
-      for (int tx = wx0; tx <= wx1; ++tx) {
-        const int X0 = tx * T, Y0 = ty * T;
-        bool hit = valid && sx1 >= X0 && sx0 <= X0 + T - 1 && sy1 >= Y0 && sy0 <= Y0 + T - 1;
-        int ra = 0, rb = -1;
-        if (hit) {
-          float lo = (float)rlo, hi = (float)rhi;
-          half_ge(fu + m, (float)X0 - 1.5f - c - fx, lo, hi);
-          half_ge(m - fu, fx - (float)(X0 + T) - 0.5f - c, lo, hi);
-          half_ge(fu, -0.5f - fx, lo, hi);
-          half_ge(-fu, fx - (float)W + 0.5f, lo, hi);
-          half_ge(fv + m, (float)Y0 - 1.5f - c - fy, lo, hi);
-          half_ge(m - fv, fy - (float)(Y0 + T) - 0.5f - c, lo, hi);
-          half_ge(fv, -0.5f - fy, lo, hi);
-          half_ge(-fv, fy - (float)H + 0.5f, lo, hi);
-          ra = max((int)floorf(lo) - 1, rlo);
-          rb = min((int)ceilf(hi) + 1, rhi);
-          hit = hi >= lo - 2.f && ra <= rb;
-        }
-        const unsigned bal = __ballot_sync(0xffffffffu, hit);
-        if (!bal) continue;
-        const int64_t t = (int64_t)f * ntiles + ty * P.ntx + tx;
-        int base = 0;
-        if (lane == __ffs(bal) - 1) base = atomicAdd(&P.ray_count[t], __popc(bal));
-        base = __shfl_sync(0xffffffffu, base, __ffs(bal) - 1);
-        if (!hit) continue;
-        const int e = base + __popc(bal & ((1u << lane) - 1u));
-        if (e < P.entry_cap) {
-          const int64_t o = t * P.entry_cap + e;
-          P.ray_d[o] = make_double2(u, v);
-          P.ray_xy[o] = xy;
-          P.ray_r[o] = (uint32_t)(ra - rlo) | ((uint32_t)(rb - rlo) << 16);
-        } else {
-          atomicOr(&P.flags[f], OVF_ENTRIES);
+  for (int bx = warp; bx < P.nbx; bx += blockDim.x >> 5) {
+    const int64_t fb = (int64_t)f * P.nbx * P.nby + by * P.nbx + bx;
+    const int cnt = P.bin_count[fb];
+    if (cnt == 0) continue;
+    const int wx0 = max((bx * T1 - reach) / T, 0), wx1 = min((bx * T1 + T1 - 1 + reach) / T, P.ntx - 1);
+    for (int j0 = 0; j0 < 2 * cnt; j0 += 32) {
+      const int j = j0 + lane;
+      const bool valid = j < 2 * cnt;
+      uint32_t xy = 0;
+      double2 d = make_double2(0.0, 0.0);
+      if (valid) {
+        const int64_t gi = fb * P.ridge_cap + (j >> 1);
+        xy = P.bin_xy[gi];
+        d = P.bin_d[gi];
+      }
+      const double sgn = (j & 1) ? -1.0 : 1.0;
+      const int x = (int)(xy & 0xFFFFu), y = (int)(xy >> 16);
+      const double u = sgn * d.x, v = sgn * d.y;
+      if (valid) {   // the ray's in-frame votes (per-frame vote count)
+        const int px = inframe_prefix(x, u, W, rlo, rhi), py = inframe_prefix(y, v, H, rlo, rhi);
+        my_votes += max(0, min(px, py) - rlo + 1);
+      }
+      const float fu = (float)u, fv = (float)v, fx = (float)x, fy = (float)y;
+      // frame constraints (tile independent)
+      float flo = (float)rlo, fhi = (float)rhi;
+      half_ge(fu, -0.5f - fx, flo, fhi);
+      half_ge(-fu, fx - (float)W + 0.5f, flo, fhi);
+      half_ge(fv, -0.5f - fy, flo, fhi);
+      half_ge(-fv, fy - (float)H + 0.5f, flo, fhi);
+      // bounding box of the target segment, widened by the largest halo and rounding
+      const float ax = fx + fu * rlo, bxp = fx + fu * rhi, ay = fy + fv * rlo, byp = fy + fv * rhi;
+      const float sx0 = fminf(ax, bxp) - hal - 1.f, sx1 = fmaxf(ax, bxp) + hal + 1.f;
+      const float sy0 = fminf(ay, byp) - hal - 1.f, sy1 = fmaxf(ay, byp) + hal + 1.f;
+      for (int ty = wy0; ty <= wy1; ++ty) {
+        const int Y0 = ty * T;
+        float ylo = flo, yhi = fhi;
+        half_ge(fv + m, (float)Y0 - 1.5f - c - fy, ylo, yhi);
+        half_ge(m - fv, fy - (float)(Y0 + T) - 0.5f - c, ylo, yhi);
+        const bool yhit = valid && sy1 >= Y0 && sy0 <= Y0 + T - 1 && yhi >= ylo - 2.f;
+        if (!__any_sync(0xffffffffu, yhit)) continue;
+        for (int tx = wx0; tx <= wx1; ++tx) {
+          const int X0 = tx * T;
+          bool hit = yhit && sx1 >= X0 && sx0 <= X0 + T - 1;
+          int ra = 0, rb = -1;
+          if (hit) {
+            float lo = ylo, hi = yhi;
+            half_ge(fu + m, (float)X0 - 1.5f - c - fx, lo, hi);
+            half_ge(m - fu, fx - (float)(X0 + T) - 0.5f - c, lo, hi);
+            ra = max((int)floorf(lo) - 1, rlo);
+            rb = min((int)ceilf(hi) + 1, rhi);
+            hit = hi >= lo - 2.f && ra <= rb;
+          }
+          const unsigned bal = __ballot_sync(0xffffffffu, hit);
+          if (!bal) continue;
+          const int64_t t = tile0 + ty * P.ntx + tx;
+          int base = 0;
+          if (lane == __ffs(bal) - 1) base = atomicAdd(&P.ray_count[t], __popc(bal));
+          base = __shfl_sync(0xffffffffu, base, __ffs(bal) - 1);
+          if (!hit) continue;
+          const int e = base + __popc(bal & ((1u << lane) - 1u));
+          if (e < P.entry_cap) {
+            const int64_t o = t * P.entry_cap + e;
+            P.ray_d[o] = make_double2(u, v);
+            P.ray_xy[o] = xy;
+            P.ray_r[o] = (uint32_t)(ra - rlo) | ((uint32_t)(rb - rlo) << 16);
+          } else {
+            atomicOr(&P.flags[f], OVF_ENTRIES);
+          }
         }
       }
+    }
   }
   my_votes = __reduce_add_sync(0xffffffffu, my_votes);
   if (lane == 0 && my_votes) atomicAdd(&P.stats[f].votes, (unsigned long long)my_votes);
 }
 
 cudaError_t launch_rays(int n_frames, const Params& P, cudaStream_t st) {
-  k_rays<<<dim3(P.nbx * P.nby, n_frames), 128, 0, st>>>(P);
+  k_rays<<<dim3(P.nby, n_frames), 256, 0, st>>>(P);
   return cudaGetLastError();
 }
 
