@@ -34,6 +34,10 @@ namespace {
 
 inline size_t al16(size_t v) { return (v + 15) & ~size_t(15); }
 
+#ifndef RD_K2_HSL
+#define RD_K2_HSL 0
+#endif
+constexpr int HSL = RD_K2_HSL;   // byte-counter S tasks: lanes per hotspot (power of two <= 32; 0: per step)
 constexpr int SMALL_K = 7;   // window rows 2K+1 <= 15: a half-warp per hotspot
 
 // llround of an exactly computed product (|v| < 2^31): copysign(0.5) added toward zero,
@@ -318,14 +322,23 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
       {
         if (L0 + G < nlev) setup(L0 + G, par ^ 1);
         if (CB == 1) {
-          // byte counters: a half-warp per hotspot, each lane two window rows (hl, hl + 16);
+          // byte counters: HSL lanes per hotspot, lane hl sums window rows hl, hl + HSL, ...;
           // a row is summed over whole 32-bit words with dp4a against the level's byte-plane
           // weights for the row's alignment (w = 64 wh + wl): exact integer S as below
           constexpr int NWW = 9;   // weight words per row: (3 + 2K + 1 + 3) / 4 <= 9 for K <= 15
           const int ntask = (P.ablate & 4) ? 0 : s_ntask[0];
-          const int half = lane >> 4, hl = lane & 15;
-          for (int t0 = 2 * warp; t0 < ntask; t0 += 2 * NW) {
-            const int t = t0 + half;
+#if RD_K2_HSL == 0
+          // lanes per hotspot: the widest power of two that still gives every warp its share
+          const int per_warp = (ntask + NW - 1) / NW;
+          int hsl = 32;
+          while (hsl > 4 && hsl * per_warp > 32) hsl >>= 1;
+#else
+          const int hsl = HSL;
+#endif
+          const int NGW = 32 / hsl;   // hotspots per warp pass
+          const int grp = lane / hsl, hl = lane & (hsl - 1);
+          for (int t0 = NGW * warp; t0 < ntask; t0 += NGW * NW) {
+            const int t = t0 + grp;
             const bool valid = t < ntask;
             const int tk = tasks[valid ? t : t0];
             const int g = tk >> 12, h = tk & 0xFFF;
@@ -345,10 +358,8 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
             const uint16_t* w = tW + li * P.wstride;
             const uint32_t* lvlw = raw32 + ((g * lvlc) >> 2);
             unsigned long long acc = 0;
-#pragma unroll
-            for (int q2 = 0; q2 < 2; ++q2) {
-              const int row = hl + 16 * q2;
-              if (valid && row <= 2 * K && !(P.ablate & 1)) {
+            if (valid && !(P.ablate & 1)) {
+              for (int row = hl; row <= 2 * K; row += hsl) {
                 const uint32_t* rowp = lvlw + (((iy - 1 + hal + row - K) * rawp + cx0 - al) >> 2);
                 uint32_t lo = 0, hi = 0;
 #pragma unroll
@@ -361,13 +372,9 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
                 acc += (unsigned long long)(hi * 64u + lo) * (unsigned long long)w[abs(row - K)];
               }
             }
-            // lane terms < 2^45: 24-bit halves, each half-warp reduced separately
-            const unsigned lo = (unsigned)(acc & 0xFFFFFFull), hi = (unsigned)(acc >> 24);
-            const unsigned lo0 = __reduce_add_sync(FULL, half ? 0u : lo);
-            const unsigned hi0 = __reduce_add_sync(FULL, half ? 0u : hi);
-            const unsigned lo1 = __reduce_add_sync(FULL, half ? lo : 0u);
-            const unsigned hi1 = __reduce_add_sync(FULL, half ? hi : 0u);
-            const unsigned long long S = ((unsigned long long)(half ? hi1 : hi0) << 24) + (half ? lo1 : lo0);
+#pragma unroll
+            for (int o = hsl / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
+            const unsigned long long S = acc;
             if (valid && hl == 0) {
               hS[sl * hot_cap + h] = S;
               const uint16_t rv = rawc[g * lvlc + (iy - 1 + hal) * rawp + (ix - 1 + hal)];

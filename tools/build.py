@@ -49,7 +49,7 @@ def build_oracle(force=False):
 
 def build_rd(force=False):
     pkg = os.path.join(ROOT, "paper_1310_1371_b200")
-    out = os.path.join(pkg, "librd.so")
+    out = os.environ.get("RD_BUILD_OUT") or os.path.join(pkg, "librd.so")
     csrc = os.path.join(pkg, "csrc")
     srcs = sorted(glob.glob(os.path.join(csrc, "*.cu")) + glob.glob(os.path.join(csrc, "*.cpp")))
     deps = srcs + glob.glob(os.path.join(csrc, "*.cuh")) + glob.glob(os.path.join(csrc, "*.h")) + \
@@ -57,6 +57,7 @@ def build_rd(force=False):
     if not (force or _stale(out, deps)):
         return out
     prof = ["-DRD_K2_PROF"] if os.environ.get("RD_BUILD_PROF") else []   # K2 phase-cycle counters (tools/phase_probe.py)
+    prof += os.environ.get("RD_BUILD_DEFS", "").split()   # variant builds for A/B runs (-DNAME=VALUE ...)
     cmd = [NVCC, "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo"] + prof + [
            "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off", "-shared",
            "-Xptxas", "-v", "-I", os.path.join(ROOT, "include"), "-o", out] + srcs + ["-lcudart"]
