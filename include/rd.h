@@ -120,10 +120,13 @@ rd_status rd_detect(rd_detector* det, const void* d_frames, int64_t pitch_bytes,
                     int32_t n_frames, rd_ring* d_rings, int32_t* d_counts, void* stream);
 
 /* End-to-end variant on HOST buffers (pinned memory recommended): copies frames
- * host->device in chunks of at most max_batch frames, overlapping the copy of
- * chunk k+1 with the detection of chunk k on the library's internal streams,
- * and copies rings/counts back.  Synchronous: returns when h_rings/h_counts are
- * filled.  h_rings: n_frames * max_rings_per_frame records. */
+ * host->device in chunks (at most min(48, max_batch/2) frames, the first ones
+ * smaller), up to 3 chunks ahead of the detection, which alternates between two
+ * internal streams working on disjoint halves of the internal buffers, and copies
+ * rings/counts back.  Any n_frames >= 1.  Synchronous: returns when h_rings/h_counts
+ * are filled.  h_rings: n_frames * max_rings_per_frame records.  rd_sync,
+ * rd_query_overflow and rd_get_stats do not describe rd_detect_host calls (the
+ * counts of overflowed frames are -1 and the call returns RD_ERR_CAPACITY). */
 rd_status rd_detect_host(rd_detector* det, const void* h_frames, int64_t pitch_bytes, int64_t frame_stride_bytes,
                          int32_t n_frames, rd_ring* h_rings, int32_t* h_counts);
 

@@ -71,11 +71,14 @@ struct rd_detector {
   void* d_redo_list = nullptr;
   // host-path staging
   int chunk = 0;
-  void* d_stage[2] = {nullptr, nullptr};
-  void* d_rings_stage[2] = {nullptr, nullptr};
-  int* d_counts_stage[2] = {nullptr, nullptr};
+  static constexpr int NSTAGE = 4;   // host-path chunk buffers: copies run up to 3 chunks ahead
+  void* d_stage[NSTAGE] = {};
+  void* d_rings_stage[NSTAGE] = {};
+  int* d_counts_stage[NSTAGE] = {};
   cudaStream_t s_comp = nullptr, s_h2d = nullptr, s_d2h = nullptr;
-  cudaEvent_t ev_h2d[2], ev_done[2], ev_d2h[2];
+  cudaStream_t s_comp2 = nullptr;   // chunks alternate between s_comp and s_comp2 (their tails overlap)
+  int n_slots = 1;                  // frame regions of the internal buffers used by concurrent chunks
+  cudaEvent_t ev_h2d[NSTAGE], ev_done[NSTAGE], ev_d2h[NSTAGE];
   cudaEvent_t ev_last = nullptr;
   bool timing = false;
   std::vector<cudaEvent_t> tev;  // 4 per timed call
@@ -447,7 +450,7 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
     Q.k2t = det->P16.k2t;
     Q.k2_rcap = det->P16.k2_rcap;
     Q.k2o = det->P16.k2o;
-    e = cudaMalloc(&det->d_redo_list, sizeof(int) * (B + 1));
+    e = cudaMalloc(&det->d_redo_list, sizeof(int) * 2 * (B + 1));   // one list per slot (frame_view)
     if (e != cudaSuccess) { rd_destroy(det); return cuda_fail(e, "cudaMalloc redo_list"); }
     Q.redo_list = (int*)det->d_redo_list;
     det->P16 = Q;
@@ -473,16 +476,17 @@ rd_status rd_destroy(rd_detector* det) {
   cudaFree(det->d_dbg);
   cudaFree(det->d_redo_list);
   cudaFree(det->d_prof);
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < rd_detector::NSTAGE; ++i) {
     cudaFree(det->d_stage[i]);
     cudaFree(det->d_rings_stage[i]);
     cudaFree(det->d_counts_stage[i]);
   }
   if (det->s_comp) {
     cudaStreamDestroy(det->s_comp);
+    if (det->s_comp2) cudaStreamDestroy(det->s_comp2);
     cudaStreamDestroy(det->s_h2d);
     cudaStreamDestroy(det->s_d2h);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < rd_detector::NSTAGE; ++i) {
       cudaEventDestroy(det->ev_h2d[i]);
       cudaEventDestroy(det->ev_done[i]);
       cudaEventDestroy(det->ev_d2h[i]);
@@ -494,9 +498,39 @@ rd_status rd_destroy(rd_detector* det) {
   return RD_OK;
 }
 
-static rd_status detect_impl(rd_detector* det, const void* d_frames, int64_t pitch, int64_t fstride, int n,
-                             void* d_rings, int* d_counts, cudaStream_t st) {
+// The parameters of a call working on frames [f0, f0 + n) of the internal buffers, with the
+// K2 work counters and redo list of slot `slot` (0 or 1): two such views are disjoint, so the
+// host path can run consecutive chunks on two streams and let their kernels overlap.
+static void frame_view(const rd_detector* det, int f0, int slot, Params& V, Params& V16) {
   const Params& P = det->P;
+  const int64_t nb = (int64_t)P.nbx * P.nby, ntl = (int64_t)P.ntx * P.nty;
+  V = P;
+  V.bin_count += f0 * nb;
+  V.bin_xy += f0 * nb * P.ridge_cap;
+  V.bin_d += f0 * nb * P.ridge_cap;
+  V.peaks += (int64_t)f0 * P.ring_cap;
+  V.stats += f0;
+  V.peak_count += f0;
+  V.flags += f0;
+  V.dbg_count += f0;
+  V.ray_count += f0 * ntl;
+  V.ray_d += f0 * ntl * P.entry_cap;
+  V.ray_xy += f0 * ntl * P.entry_cap;
+  V.ray_r += f0 * ntl * P.entry_cap;
+  if (V.dbg_hot) V.dbg_hot += (int64_t)f0 * P.dbg_cap;
+  V.redo += f0;
+  V.k2_work = P.k2_work + 2 * slot;   // [main, redo] work counters of the slot
+  V16 = V;
+  V16.k2t = det->P16.k2t;
+  V16.k2_rcap = det->P16.k2_rcap;
+  V16.k2o = det->P16.k2o;
+  V16.redo_list = det->P16.redo_list + (int64_t)slot * (det->max_batch + 1);
+}
+
+static rd_status detect_impl(rd_detector* det, const void* d_frames, int64_t pitch, int64_t fstride, int n,
+                             void* d_rings, int* d_counts, cudaStream_t st, int f0 = 0, int slot = 0) {
+  Params P, P16;
+  frame_view(det, f0, slot, P, P16);
   cudaEvent_t* ev = nullptr;
   if (det->timing) {
     size_t need = RD_NEV * (size_t)(det->n_timed + 1);
@@ -508,7 +542,19 @@ static rd_status detect_impl(rd_detector* det, const void* d_frames, int64_t pit
     ev = &det->tev[RD_NEV * (size_t)det->n_timed];
     det->n_timed++;
   }
-  CK(cudaMemsetAsync(det->d_counters, 0, det->counters_bytes, st));
+  // per-frame counters of the view and the slot's work counters
+  const int64_t ntl = (int64_t)P.ntx * P.nty;
+  if (f0 == 0 && slot == 0 && n == det->max_batch) {
+    CK(cudaMemsetAsync(det->d_counters, 0, det->counters_bytes, st));
+  } else {
+    CK(cudaMemsetAsync(P.stats, 0, sizeof(Stats) * n, st));
+    CK(cudaMemsetAsync(P.peak_count, 0, sizeof(int) * n, st));
+    CK(cudaMemsetAsync(P.flags, 0, sizeof(int) * n, st));
+    CK(cudaMemsetAsync(P.dbg_count, 0, sizeof(int) * n, st));
+    CK(cudaMemsetAsync(P.ray_count, 0, sizeof(int) * n * ntl, st));
+    CK(cudaMemsetAsync(P.k2_work, 0, sizeof(int) * 2, st));
+    CK(cudaMemsetAsync(P.redo, 0, sizeof(int) * n, st));
+  }
   if (ev) CK(cudaEventRecord(ev[0], st));
   CK(launch_ridges(d_frames, pitch, fstride, n, P, st));
   if (ev) CK(cudaEventRecord(ev[1], st));
@@ -517,8 +563,8 @@ static rd_status detect_impl(rd_detector* det, const void* d_frames, int64_t pit
   if (det->k2_impl == 2) {
     CK(launch_hough2(n, P, det->wide, det->G, det->k2_threads, det->k2_minb, det->k2_cb, det->n_sm, st));
     if (det->k2_cb == 1) {   // frames whose byte counters overflowed: recomputed with 16-bit counters
-      CK(launch_redo_reset(n, det->P16, st));
-      CK(launch_hough2(n, det->P16, det->wide, det->G16, det->k2_threads16, det->k2_minb16, 2, det->n_sm, st));
+      CK(launch_redo_reset(n, P16, st));
+      CK(launch_hough2(n, P16, det->wide, det->G16, det->k2_threads16, det->k2_minb16, 2, det->n_sm, st));
     }
   } else
     CK(launch_hough(n, P, det->wide, det->G, det->k2_threads, det->k2_minb, st));
@@ -551,10 +597,13 @@ rd_status rd_detect(rd_detector* det, const void* d_frames, int64_t pitch, int64
 
 static rd_status ensure_host_path(rd_detector* det) {
   if (det->s_comp) return RD_OK;
-  det->chunk = std::min(det->max_batch, 64);
-  if (const char* env = getenv("RD_HOST_CHUNK")) det->chunk = std::max(1, std::min(det->max_batch, atoi(env)));
+  // two chunks in flight use disjoint halves of the internal buffers (frame_view)
+  det->n_slots = det->max_batch >= 2 ? 2 : 1;
+  const int room = det->max_batch / det->n_slots;
+  det->chunk = std::min(room, 48);
+  if (const char* env = getenv("RD_HOST_CHUNK")) det->chunk = std::max(1, std::min(room, atoi(env)));
   const size_t fbytes = (size_t)det->cfg.width * det->cfg.height * det->P.pixel_bytes;
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < rd_detector::NSTAGE; ++i) {
     CK(cudaMalloc(&det->d_stage[i], fbytes * det->chunk));
     CK(cudaMalloc(&det->d_rings_stage[i], sizeof(rd_ring) * det->chunk * det->P.ring_cap));
     CK(cudaMalloc(&det->d_counts_stage[i], sizeof(int) * det->chunk));
@@ -563,6 +612,7 @@ static rd_status ensure_host_path(rd_detector* det) {
     CK(cudaEventCreateWithFlags(&det->ev_d2h[i], cudaEventDisableTiming));
   }
   CK(cudaStreamCreateWithFlags(&det->s_comp, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&det->s_comp2, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&det->s_h2d, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&det->s_d2h, cudaStreamNonBlocking));
   return RD_OK;
@@ -579,39 +629,72 @@ rd_status rd_detect_host(rd_detector* det, const void* h_frames, int64_t pitch, 
   const int W = det->cfg.width, H = det->cfg.height, pb = det->P.pixel_bytes;
   const size_t row = (size_t)W * pb, fbytes = row * H;
   const int C = det->chunk, rc = det->P.ring_cap;
-  // the first chunk is a quarter chunk: its copy is the only one nothing overlaps
-  const int C0 = std::max(1, C / 4);
-  const int nchunks = n <= C0 ? 1 : 1 + (n - C0 + C - 1) / C;
+  // chunk sizes ramp up from a quarter chunk by 3/2 per chunk: the first copy is the only one
+  // nothing overlaps, and each copy ends before the previous (smaller) chunk's compute does
+  // (a symmetric ramp-down at the end measured no better)
+  std::vector<int> cstart;
+  for (int f = 0, m = std::max(1, C / 4); f < n; f += m, m = std::min(C, std::max(m + 1, m * 3 / 2)))
+    cstart.push_back(f);
+  cstart.push_back(n);
+  const int nchunks = (int)cstart.size() - 1;
   rd_status result = RD_OK;
+  // RD_HOST_TRACE: per-chunk copy / compute / readback times on stderr (diagnostics only)
+  const bool trace = getenv("RD_HOST_TRACE") != nullptr;
+  std::vector<cudaEvent_t> tev;
+  auto mark = [&](cudaStream_t st) {
+    if (!trace) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    tev.push_back(e);
+  };
   for (int k = 0; k < nchunks; ++k) {
-    const int b = k & 1, f0 = k == 0 ? 0 : C0 + (k - 1) * C, m = std::min(k == 0 ? C0 : C, n - f0);
-    // H2D of chunk k may overwrite stage b only after chunk k-2 finished computing
-    if (k >= 2) CK(cudaStreamWaitEvent(det->s_h2d, det->ev_done[b], 0));
+    const int f0 = cstart[k], m = cstart[k + 1] - f0;
+    // buffer slot and stream b: chunk k overlaps chunk k - 1 (other slot) and follows chunk k - 2
+    // on the same stream; stage q holds its frames and rings
+    const int b = det->n_slots == 2 ? (k & 1) : 0, q = k % rd_detector::NSTAGE;
+    cudaStream_t sc = b ? det->s_comp2 : det->s_comp;
+    // H2D of chunk k may overwrite stage q only after the stage's previous chunk finished computing
+    if (k >= rd_detector::NSTAGE) CK(cudaStreamWaitEvent(det->s_h2d, det->ev_done[q], 0));
+    mark(det->s_h2d);
     const char* src = (const char*)h_frames + (size_t)f0 * fstride;
     if (pitch == (int64_t)row && fstride == (int64_t)fbytes) {
-      CK(cudaMemcpyAsync(det->d_stage[b], src, fbytes * m, cudaMemcpyHostToDevice, det->s_h2d));
+      CK(cudaMemcpyAsync(det->d_stage[q], src, fbytes * m, cudaMemcpyHostToDevice, det->s_h2d));
     } else {
       for (int i = 0; i < m; ++i)
-        CK(cudaMemcpy2DAsync((char*)det->d_stage[b] + fbytes * i, row, src + (size_t)i * fstride, pitch, row, H,
+        CK(cudaMemcpy2DAsync((char*)det->d_stage[q] + fbytes * i, row, src + (size_t)i * fstride, pitch, row, H,
                              cudaMemcpyHostToDevice, det->s_h2d));
     }
-    CK(cudaEventRecord(det->ev_h2d[b], det->s_h2d));
-    CK(cudaStreamWaitEvent(det->s_comp, det->ev_h2d[b], 0));
-    // the ring stage b is reused only after its previous D2H completed
-    if (k >= 2) CK(cudaStreamWaitEvent(det->s_comp, det->ev_d2h[b], 0));
-    s = detect_impl(det, det->d_stage[b], row, fbytes, m, det->d_rings_stage[b], det->d_counts_stage[b],
-                    det->s_comp);
+    CK(cudaEventRecord(det->ev_h2d[q], det->s_h2d));
+    mark(det->s_h2d);
+    CK(cudaStreamWaitEvent(sc, det->ev_h2d[q], 0));
+    // the ring stage q is reused only after its previous D2H completed
+    if (k >= rd_detector::NSTAGE) CK(cudaStreamWaitEvent(sc, det->ev_d2h[q], 0));
+    mark(sc);
+    s = detect_impl(det, det->d_stage[q], row, fbytes, m, det->d_rings_stage[q], det->d_counts_stage[q], sc,
+                    b * C, b);
     if (s != RD_OK) return s;
-    CK(cudaEventRecord(det->ev_done[b], det->s_comp));
-    CK(cudaStreamWaitEvent(det->s_d2h, det->ev_done[b], 0));
-    CK(cudaMemcpyAsync(h_rings + (size_t)f0 * rc, det->d_rings_stage[b], sizeof(rd_ring) * (size_t)m * rc,
+    CK(cudaEventRecord(det->ev_done[q], sc));
+    mark(sc);
+    CK(cudaStreamWaitEvent(det->s_d2h, det->ev_done[q], 0));
+    CK(cudaMemcpyAsync(h_rings + (size_t)f0 * rc, det->d_rings_stage[q], sizeof(rd_ring) * (size_t)m * rc,
                        cudaMemcpyDeviceToHost, det->s_d2h));
-    CK(cudaMemcpyAsync(h_counts + f0, det->d_counts_stage[b], sizeof(int) * m, cudaMemcpyDeviceToHost,
+    CK(cudaMemcpyAsync(h_counts + f0, det->d_counts_stage[q], sizeof(int) * m, cudaMemcpyDeviceToHost,
                        det->s_d2h));
-    CK(cudaEventRecord(det->ev_d2h[b], det->s_d2h));
+    CK(cudaEventRecord(det->ev_d2h[q], det->s_d2h));
+    mark(det->s_d2h);
   }
   CK(cudaStreamSynchronize(det->s_d2h));
   CK(cudaStreamSynchronize(det->s_comp));
+  CK(cudaStreamSynchronize(det->s_comp2));
+  if (trace) {   // per chunk: h2d start/end, compute start/end, d2h end (ms from the first copy)
+    for (size_t i = 0; i + 5 <= tev.size(); i += 5) {
+      float t[5];
+      for (int j = 0; j < 5; ++j) cudaEventElapsedTime(&t[j], tev[0], tev[i + j]);
+      fprintf(stderr, "rd: chunk %zu h2d %.3f-%.3f comp %.3f-%.3f d2h-end %.3f\n", i / 5, t[0], t[1], t[2], t[3], t[4]);
+    }
+    for (cudaEvent_t e : tev) cudaEventDestroy(e);
+  }
   for (int i = 0; i < n; ++i)
     if (h_counts[i] < 0) result = RD_ERR_CAPACITY;
   return result;

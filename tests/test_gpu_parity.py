@@ -247,6 +247,28 @@ def test_detect_host_matches_device(rdmod):
         assert hr[i, : hc[i]].tobytes() == dev_out[i].tobytes()
 
 
+@pytest.mark.parametrize("force_redo", [False, True])
+def test_detect_host_many_chunks_two_slots(rdmod, force_redo, monkeypatch):
+    """rd_detect_host with n_frames far above max_batch: ramped chunks alternate between two
+    streams on disjoint halves of the internal buffers (frame views with their own K2 work
+    counters and redo lists); every frame equals the device path, also when every frame
+    takes the 16-bit redo pass."""
+    if force_redo:
+        monkeypatch.setenv("RD_K2_FORCE_REDO", "1")
+    params = synth.preset(2)
+    frames = synth.batch(2, 0, 40, 37)
+    det = _det(rdmod, params, max_batch=8)
+    ref = []
+    for i in range(0, 37, 8):
+        rings, counts = det.detect(torch.from_numpy(frames[i:i + 8]).cuda())
+        det.sync()
+        ref += det.rings_to_numpy(rings, counts)
+    hr, hc = det.detect_host(torch.from_numpy(frames).pin_memory())
+    for i in range(37):
+        assert hc[i] == len(ref[i]) and hc[i] > 0
+        assert hr[i, : hc[i]].tobytes() == ref[i].tobytes()
+
+
 def test_full_batch_cfg4_dense(rdmod):
     """cfg4 at BASELINE size (512 frames of 1024x1024, 200 rings): sampled frames vs the
     oracle; every frame valid (no capacity overflow with the dense-config capacities)."""
