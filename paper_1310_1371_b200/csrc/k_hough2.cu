@@ -47,6 +47,17 @@ __device__ __forceinline__ int round_half_away_i(double v) {
 }
 
 // shared-memory atomic add on a 32-bit shared address: returns the old word
+// shifts with PTX semantics: amounts >= 32 give 0
+__device__ __forceinline__ uint32_t shl_clamp(uint32_t x, uint32_t n) {
+  uint32_t r;
+  asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(n));
+  return r;
+}
+__device__ __forceinline__ uint32_t shr_clamp(uint32_t x, uint32_t n) {
+  uint32_t r;
+  asm("shr.b32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(n));
+  return r;
+}
 __device__ __forceinline__ uint32_t atom_add_shared(uint32_t saddr, uint32_t v) {
   uint32_t old;
   asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(saddr), "r"(v) : "memory");
@@ -276,27 +287,29 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
           // level's box, tile + K_r + 1, are never read by that level's windows; the clear
           // resets them)
           uint32_t addr[G], sh[G], old[G];
-          unsigned okm = 0;
+          const uint32_t pb = raw_base + (uint32_t)(CB * (yr * rawp + xr));   // the ray's own cell (bytes)
+          const int ux = xr - bx0, uy = yr - by0;
 #pragma unroll
           for (int g = 0; g < G; ++g) {
             const double rd = rb0 + (double)g;
-            const int cx = xr + round_half_away_i(__dmul_rn(rd, dx));
-            const int cy = yr + round_half_away_i(__dmul_rn(rd, dy));
-            const bool ok = ((lm >> g) & 1u) & ((unsigned)(cx - bx0) <= (unsigned)bxs) &
-                            ((unsigned)(cy - by0) <= (unsigned)bys);
-            const int cell = cy * rawp + cx;
-            sh[g] = (uint32_t)(cell & ((1 << CSH) - 1)) * BITS;
-            addr[g] = ok ? raw_base + (uint32_t)(g * lvlc * CB) + 4u * (uint32_t)(cell >> CSH) : dummy;
-            okm |= (unsigned)ok << g;
+            const int ox = round_half_away_i(__dmul_rn(rd, dx));
+            const int oy = round_half_away_i(__dmul_rn(rd, dy));
+            const bool ok = ((lm >> g) & 1u) & ((unsigned)(ux + ox) <= (unsigned)bxs) &
+                            ((unsigned)(uy + oy) <= (unsigned)bys);
+            const uint32_t bc = pb + (uint32_t)(g * lvlc * CB) + (uint32_t)(CB * (oy * rawp + ox));   // byte address
+            // masked votes: shift 32 (shl/shr clamp to 0) on the lane's dummy word
+            sh[g] = ok ? (bc & 3u) * 8u : 32u;
+            addr[g] = ok ? (bc & ~3u) : dummy;
           }
 #pragma unroll
-          for (int g = 0; g < G; ++g) old[g] = atom_add_shared(addr[g], ((okm >> g) & 1u) << sh[g]);
+          for (int g = 0; g < G; ++g) old[g] = atom_add_shared(addr[g], shl_clamp(1u, sh[g]));
+          uint32_t omax = 0;
 #pragma unroll
           for (int g = 0; g < G; ++g) {
-            const uint32_t oc = (old[g] >> sh[g]) & CMASK;
-            if (CB == 1) ovf |= ((okm >> g) & 1u) & (oc >= (uint32_t)P.u8_limit);
-            if (((okm >> g) & 1u) && oc == T_raw) {   // this vote lifted the counter past T_raw
-              const int cell = (int)(((addr[g] - raw_base - (uint32_t)(g * lvlc * CB)) >> 2) << CSH) + (int)(sh[g] / BITS);
+            const uint32_t oc = shr_clamp(old[g], sh[g]) & CMASK;   // 0 for masked votes
+            omax = max(omax, oc);
+            if (oc == T_raw) {   // this vote lifted the counter past T_raw (T_raw >= 1)
+              const int cell = (int)((addr[g] - raw_base - (uint32_t)(g * lvlc * CB)) >> (CB - 1)) + (int)(sh[g] / BITS);
               const int cy = (int)__umulhi((uint32_t)cell, P.k2o.rawp_magic), cx = cell - cy * rawp;
               const int ix = cx - (hal - 1), iy = cy - (hal - 1);
               if ((unsigned)ix >= (unsigned)(T + 2) || (unsigned)iy >= (unsigned)(T + 2)) continue;   // not in the ring
@@ -304,14 +317,17 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
               const int h = atomicAdd(&hcnt[li], 1);
               if (h < hot_cap) {
                 hcell[slot_of[g] * hot_cap + h] = (uint16_t)((iy << 8) | ix);
-                const int slot = (CB == 1 || tK[li] <= SMALL_K) ? atomicAdd(&s_ntask[0], 1)
-                                                                : G * hot_cap - 1 - atomicAdd(&s_ntask[1], 1);
-                tasks[slot] = (uint16_t)((g << 12) | h);
+                if (CB == 2) {   // (byte counters take their S tasks straight from the level lists)
+                  const int slot = tK[li] <= SMALL_K ? atomicAdd(&s_ntask[0], 1)
+                                                     : G * hot_cap - 1 - atomicAdd(&s_ntask[1], 1);
+                  tasks[slot] = (uint16_t)((g << 12) | h);
+                }
               } else {
                 atomicOr(s_flags, OVF_HOTSPOTS);
               }
             }
           }
+          if (CB == 1) ovf |= omax >= (uint32_t)P.u8_limit;
         }
         if (CB == 1 && __any_sync(FULL, ovf) && lane == 0) *s_ovf = 1;
       }
@@ -326,7 +342,12 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
           // a row is summed over whole 32-bit words with dp4a against the level's byte-plane
           // weights for the row's alignment (w = 64 wh + wl): exact integer S as below
           constexpr int NWW = 9;   // weight words per row: (3 + 2K + 1 + 3) / 4 <= 9 for K <= 15
-          const int ntask = (P.ablate & 4) ? 0 : s_ntask[0];
+          // S tasks: the step's level lists back to back (task t -> level g, list index h)
+          auto lcount = [&](int g) { return L0 + g < nlev ? min(hcnt[L0 + g], hot_cap) : 0; };
+          int ntask = 0;
+#pragma unroll
+          for (int g = 0; g < G; ++g) ntask += lcount(g);
+          if (P.ablate & 4) ntask = 0;
 #if RD_K2_HSL == 0
           // lanes per hotspot: the widest power of two that still gives every warp its share
           const int per_warp = (ntask + NW - 1) / NW;
@@ -340,8 +361,14 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
           for (int t0 = NGW * warp; t0 < ntask; t0 += NGW * NW) {
             const int t = t0 + grp;
             const bool valid = t < ntask;
-            const int tk = tasks[valid ? t : t0];
-            const int g = tk >> 12, h = tk & 0xFFF;
+            const int tv = valid ? t : t0;
+            int g = 0, h = tv, cum = 0;
+#pragma unroll
+            for (int gg = 0; gg < G - 1; ++gg) {
+              cum += lcount(gg);
+              if (tv >= cum) g = gg + 1, h = tv - cum;
+            }
+            const int tk = (g << 12) | h;
             const int li = L0 + g, sl = li % NSLOT;
             const int K = tK[li];
             const int c = hcell[sl * hot_cap + h];
