@@ -101,8 +101,10 @@ size_t k_hough2_layout(Params& P, int G, int nt, int cb) {
   L.rr = o;    o = al16(o + 4 * (size_t)P.k2_rcap);
   L.xy = o;    o = al16(o + 4 * (size_t)P.k2_rcap);
   L.hcell = o; o = al16(o + 2 * (size_t)NSLOT * hot_cap);
-  L.hraw = o;  o = al16(o + 2 * (size_t)NSLOT * hot_cap);
-  L.task = o;  o = al16(o + 2 * (size_t)G * hot_cap);
+  // byte counters keep a hotspot's raw count in the low byte of its S word and take their
+  // S tasks straight from the level lists: no raw or task arrays
+  L.hraw = o;  o = al16(o + (cb == 1 ? 0 : 2 * (size_t)NSLOT * hot_cap));
+  L.task = o;  o = al16(o + (cb == 1 ? 0 : 2 * (size_t)G * hot_cap));
   L.cand = o;  o = al16(o + 2 * (size_t)G * hot_cap);
   L.cdef = o;  o = al16(o + 2 * 2 * (size_t)hot_cap);
   L.act = o;   o = al16(o + 2 * (size_t)P.entry_cap);   // one list: written in phase (2), read in (1)
@@ -403,9 +405,8 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
             for (int o = hsl / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
             const unsigned long long S = acc;
             if (valid && hl == 0) {
-              hS[sl * hot_cap + h] = S;
               const uint16_t rv = rawc[g * lvlc + (iy - 1 + hal) * rawp + (ix - 1 + hal)];
-              hraw[sl * hot_cap + h] = rv;
+              hS[sl * hot_cap + h] = (S << 8) | rv;   // S < 2^46, raw < 256
               if (ix >= 1 && ix <= T && iy >= 1 && iy <= T) {   // interior hotspot
                 ++my_hot;
                 if (P.debug) {
@@ -552,7 +553,9 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
           const int sc = lc % NSLOT;
           const int c = hcell[sc * hot_cap + h];
           const int iy = c >> 8, ix = c & 0xFF;
-          const long long S = (long long)hS[sc * hot_cap + h];
+          constexpr int SSH = CB == 1 ? 8 : 0;   // byte counters: raw count in the low byte
+          const unsigned long long hw = hS[sc * hot_cap + h];
+          const long long S = (long long)(hw >> SSH);
           const long long rc = P.r_lo + lc;
           bool beaten = false;
 #pragma unroll
@@ -564,7 +567,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
               const int u = hcell[sl * hot_cap + j];
               const int dy = (u >> 8) - iy, dx = (u & 0xFF) - ix;
               if (dy < -1 || dy > 1 || dx < -1 || dx > 1 || (dl == 0 && dy == 0 && dx == 0)) continue;
-              const long long Su = (long long)hS[sl * hot_cap + j];
+              const long long Su = (long long)(hS[sl * hot_cap + j] >> SSH);
               const long long lhs = S * ru, rhs = Su * rc;
               const bool v_first = dl > 0 || (dl == 0 && (dy > 0 || (dy == 0 && dx > 0)));
               if (!(lhs > rhs || (lhs == rhs && v_first))) beaten = true;
@@ -575,7 +578,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
             const int kk = atomicAdd(&P.peak_count[f], 1);
             if (kk < P.ring_cap) {
               Peak pk;
-              pk.x = X0 - 1 + ix; pk.y = Y0 - 1 + iy; pk.r = (int)rc; pk.raw = hraw[sc * hot_cap + h]; pk.S = S;
+              pk.x = X0 - 1 + ix; pk.y = Y0 - 1 + iy; pk.r = (int)rc; pk.raw = CB == 1 ? (int)(hw & 0xFFu) : hraw[sc * hot_cap + h]; pk.S = S;
               P.peaks[(int64_t)f * P.ring_cap + kk] = pk;
             } else {
               atomicOr(&P.flags[f], OVF_RINGS);
