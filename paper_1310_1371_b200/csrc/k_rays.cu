@@ -45,7 +45,10 @@ __device__ __forceinline__ void half_ge(float a, float b, float& lo, float& hi) 
 // The clip of a ray's level interval splits into frame constraints (per ray), row
 // constraints (per tile row ty) and column constraints (per tile column tx), so the inner
 // tile loop evaluates two half-planes with precomputed reciprocals.
-__global__ void __launch_bounds__(256) k_rays(Params P) {
+#ifndef RD_K15_MINB
+#define RD_K15_MINB 4   // 64 registers: occupancy decides this latency-bound kernel
+#endif
+__global__ void __launch_bounds__(256, RD_K15_MINB) k_rays(Params P) {
   const int f = blockIdx.y;
   const int by = blockIdx.x;
   const int T = P.k2t, hal = P.hal, W = P.W, H = P.H;
@@ -90,6 +93,58 @@ __global__ void __launch_bounds__(256) k_rays(Params P) {
       const float ax = fx + fu * rlo, bxp = fx + fu * rhi, ay = fy + fv * rlo, byp = fy + fv * rhi;
       const float sx0 = fminf(ax, bxp) - hal - 1.f, sx1 = fmaxf(ax, bxp) + hal + 1.f;
       const float sy0 = fminf(ay, byp) - hal - 1.f, sy1 = fmaxf(ay, byp) + hal + 1.f;
+      if (wx1 - wx0 < 3 && wy1 - wy0 < 3) {
+        // window of at most 3 x 3 tiles (the usual case): clip and ballot every tile first
+        // (lane k keeps tile k's ballot), reserve all the window's list slots with one
+        // round of atomics (lane k: tile k), then write; one global round trip per 32 rays
+        uint32_t rng[9];
+        unsigned kbal = 0, hits = 0;
+#pragma unroll
+        for (int ky = 0; ky < 3; ++ky) {
+          const int ty = wy0 + ky, Y0 = ty * T;
+          float ylo = flo, yhi = fhi;
+          half_ge(fv + m, (float)Y0 - 1.5f - c - fy, ylo, yhi);
+          half_ge(m - fv, fy - (float)(Y0 + T) - 0.5f - c, ylo, yhi);
+          const bool yhit = valid && ty <= wy1 && sy1 >= Y0 && sy0 <= Y0 + T - 1 && yhi >= ylo - 2.f;
+#pragma unroll
+          for (int kx = 0; kx < 3; ++kx) {
+            const int k = 3 * ky + kx, tx = wx0 + kx, X0 = tx * T;
+            bool hit = yhit && tx <= wx1 && sx1 >= X0 && sx0 <= X0 + T - 1;
+            int ra = 0, rb = -1;
+            if (hit) {
+              float lo = ylo, hi = yhi;
+              half_ge(fu + m, (float)X0 - 1.5f - c - fx, lo, hi);
+              half_ge(m - fu, fx - (float)(X0 + T) - 0.5f - c, lo, hi);
+              ra = max((int)floorf(lo) - 1, rlo);
+              rb = min((int)ceilf(hi) + 1, rhi);
+              hit = hi >= lo - 2.f && ra <= rb;
+            }
+            rng[k] = (uint32_t)(ra - rlo) | ((uint32_t)(rb - rlo) << 16);
+            const unsigned bal = __ballot_sync(0xffffffffu, hit);
+            if (lane == k) kbal = bal;
+            hits |= (unsigned)hit << k;
+          }
+        }
+        int base = 0;
+        if (kbal) base = atomicAdd(&P.ray_count[tile0 + (wy0 + lane / 3) * P.ntx + wx0 + lane % 3], __popc(kbal));
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+          const unsigned bal = __shfl_sync(0xffffffffu, kbal, k);
+          if (!bal) continue;
+          const int b = __shfl_sync(0xffffffffu, base, k);
+          if (!((hits >> k) & 1u)) continue;
+          const int e = b + __popc(bal & ((1u << lane) - 1u));
+          if (e < P.entry_cap) {
+            const int64_t o = (tile0 + (wy0 + k / 3) * P.ntx + wx0 + k % 3) * P.entry_cap + e;
+            P.ray_d[o] = make_double2(u, v);
+            P.ray_xy[o] = xy;
+            P.ray_r[o] = rng[k];
+          } else {
+            atomicOr(&P.flags[f], OVF_ENTRIES);
+          }
+        }
+        continue;
+      }
       for (int ty = wy0; ty <= wy1; ++ty) {
         const int Y0 = ty * T;
         float ylo = flo, yhi = fhi;
