@@ -34,6 +34,9 @@ namespace {
 
 inline size_t al16(size_t v) { return (v + 15) & ~size_t(15); }
 
+#ifndef RD_K2_SETUP3
+#define RD_K2_SETUP3 1   // list the next step's rays in phase (3) (1: first, 2: after the clear) instead of (2)
+#endif
 #ifndef RD_K2_HSL
 #define RD_K2_HSL 0
 #endif
@@ -338,7 +341,9 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
       // ---------------- (2) the next step's rays; S = sum_i w(i) sum_j w(j) raw(y+i, x+j) at
       //     each hotspot and the candidate test
       {
+#if !RD_K2_SETUP3
         if (L0 + G < nlev) setup(L0 + G, par ^ 1);
+#endif
         if (CB == 1) {
           // byte counters: HSL lanes per hotspot, lane hl sums window rows hl, hl + HSL, ...;
           // a row is summed over whole 32-bit words with dp4a against the level's byte-plane
@@ -524,6 +529,9 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
       PMARK(3);
       // ---------------- (3) undo the step's counters, then peaks of levels L0-1 .. Lhi-1
       {
+#if RD_K2_SETUP3 == 1
+        if (L0 + G < nlev) setup(L0 + G, par ^ 1);
+#endif
         {   // clear the step's level buffers
           uint4* r4 = reinterpret_cast<uint4*>(raw32);
           constexpr int U = 4;
@@ -539,6 +547,9 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
           s_ntask[0] = 0;
           s_ntask[1] = 0;
         }
+#if RD_K2_SETUP3 == 2
+        if (L0 + G < nlev) setup(L0 + G, par ^ 1);
+#endif
         const int nd = (L0 > 0 && !(P.ablate & 2)) ? s_ndef[par ^ 1] : 0, nc = (P.ablate & 2) ? 0 : s_ncand[0];
         for (int p = warp; p < nd + nc; p += NW) {
           int lc, h;
