@@ -262,78 +262,86 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
         const int bx0 = max(0, -RX0), bxs = min(P.k2o.raws - 1, P.W - 1 - RX0) - bx0;
         const int by0 = max(0, -RY0), bys = min(P.k2o.raws - 1, P.H - 1 - RY0) - by0;
         bool ovf = false;
-        for (int i0 = warp * 32; i0 < nact; i0 += NT) {
-          const int i = i0 + lane;
-          unsigned lm = 0;   // levels of the step inside the ray's interval
-          int xr = 0, yr = 0;
-          double dx = 0.0, dy = 0.0;
-          if (i < nact) {
-            uint32_t rr, xy;
-            double2 d;
-            const int e = act[i];
-            if (e < rcap) {
-              d = sd[e];
-              xy = sxy[e];
-              rr = rr_s[e];
-            } else {   // beyond the resident capacity: from global memory
-              xy = __ldg(P.ray_xy + gbase + e);
-              d = __ldg(P.ray_d + gbase + e);
-              rr = __ldg(P.ray_r + gbase + e);
+        // the votes of GL levels (GL = G, or 1 for a last step with a single level: no masked
+        // work for the absent levels)
+        auto run_votes = [&](auto GLc) {
+          constexpr int GL = decltype(GLc)::value;
+          for (int i0 = warp * 32; i0 < nact; i0 += NT) {
+            const int i = i0 + lane;
+            unsigned lm = 0;   // levels of the step inside the ray's interval
+            int xr = 0, yr = 0;
+            double dx = 0.0, dy = 0.0;
+            if (i < nact) {
+              uint32_t rr, xy;
+              double2 d;
+              const int e = act[i];
+              if (e < rcap) {
+                d = sd[e];
+                xy = sxy[e];
+                rr = rr_s[e];
+              } else {   // beyond the resident capacity: from global memory
+                xy = __ldg(P.ray_xy + gbase + e);
+                d = __ldg(P.ray_d + gbase + e);
+                rr = __ldg(P.ray_r + gbase + e);
+              }
+              const int ga = max((int)(rr & 0xFFFFu) - L0, 0), gb = min((int)(rr >> 16) - L0, G - 1);
+              lm = gb >= ga ? (2u << gb) - (1u << ga) : 0u;
+              dx = d.x;
+              dy = d.y;
+              xr = (int)(xy & 0xFFFFu) - RX0;
+              yr = (int)(xy >> 16) - RY0;
             }
-            const int ga = max((int)(rr & 0xFFFFu) - L0, 0), gb = min((int)(rr >> 16) - L0, G - 1);
-            lm = gb >= ga ? (2u << gb) - (1u << ga) : 0u;
-            dx = d.x;
-            dy = d.y;
-            xr = (int)(xy & 0xFFFFu) - RX0;
-            yr = (int)(xy >> 16) - RY0;
-          }
-          // targets of the G levels, branch-free: a vote counts if its level is in the ray's
-          // interval and its cell lies in the raw buffer and in the frame (cells outside a
-          // level's box, tile + K_r + 1, are never read by that level's windows; the clear
-          // resets them)
-          uint32_t addr[G], sh[G], old[G];
-          const uint32_t pb = raw_base + (uint32_t)(CB * (yr * rawp + xr));   // the ray's own cell (bytes)
-          const int ux = xr - bx0, uy = yr - by0;
-#pragma unroll
-          for (int g = 0; g < G; ++g) {
-            const double rd = rb0 + (double)g;
-            const int ox = round_half_away_i(__dmul_rn(rd, dx));
-            const int oy = round_half_away_i(__dmul_rn(rd, dy));
-            const bool ok = ((lm >> g) & 1u) & ((unsigned)(ux + ox) <= (unsigned)bxs) &
-                            ((unsigned)(uy + oy) <= (unsigned)bys);
-            const uint32_t bc = pb + (uint32_t)(g * lvlc * CB) + (uint32_t)(CB * (oy * rawp + ox));   // byte address
-            // masked votes: shift 32 (shl/shr clamp to 0) on the lane's dummy word
-            sh[g] = ok ? (bc & 3u) * 8u : 32u;
-            addr[g] = ok ? (bc & ~3u) : dummy;
-          }
-#pragma unroll
-          for (int g = 0; g < G; ++g) old[g] = atom_add_shared(addr[g], shl_clamp(1u, sh[g]));
-          uint32_t omax = 0;
-#pragma unroll
-          for (int g = 0; g < G; ++g) {
-            const uint32_t oc = shr_clamp(old[g], sh[g]) & CMASK;   // 0 for masked votes
-            omax = max(omax, oc);
-            if (oc == T_raw) {   // this vote lifted the counter past T_raw (T_raw >= 1)
-              const int cell = (int)((addr[g] - raw_base - (uint32_t)(g * lvlc * CB)) >> (CB - 1)) + (int)(sh[g] / BITS);
-              const int cy = (int)__umulhi((uint32_t)cell, P.k2o.rawp_magic), cx = cell - cy * rawp;
-              const int ix = cx - (hal - 1), iy = cy - (hal - 1);
-              if ((unsigned)ix >= (unsigned)(T + 2) || (unsigned)iy >= (unsigned)(T + 2)) continue;   // not in the ring
-              const int li = L0 + g;
-              const int h = atomicAdd(&hcnt[li], 1);
-              if (h < hot_cap) {
-                hcell[slot_of[g] * hot_cap + h] = (uint16_t)((iy << 8) | ix);
-                if (CB == 2) {   // (byte counters take their S tasks straight from the level lists)
-                  const int slot = tK[li] <= SMALL_K ? atomicAdd(&s_ntask[0], 1)
-                                                     : G * hot_cap - 1 - atomicAdd(&s_ntask[1], 1);
-                  tasks[slot] = (uint16_t)((g << 12) | h);
+            // targets of the G levels, branch-free: a vote counts if its level is in the ray's
+            // interval and its cell lies in the raw buffer and in the frame (cells outside a
+            // level's box, tile + K_r + 1, are never read by that level's windows; the clear
+            // resets them)
+            uint32_t addr[GL], sh[GL], old[GL];
+            const uint32_t pb = raw_base + (uint32_t)(CB * (yr * rawp + xr));   // the ray's own cell (bytes)
+            const int ux = xr - bx0, uy = yr - by0;
+  #pragma unroll
+            for (int g = 0; g < GL; ++g) {
+              const double rd = rb0 + (double)g;
+              const int ox = round_half_away_i(__dmul_rn(rd, dx));
+              const int oy = round_half_away_i(__dmul_rn(rd, dy));
+              const bool ok = ((lm >> g) & 1u) & ((unsigned)(ux + ox) <= (unsigned)bxs) &
+                              ((unsigned)(uy + oy) <= (unsigned)bys);
+              const uint32_t bc = pb + (uint32_t)(g * lvlc * CB) + (uint32_t)(CB * (oy * rawp + ox));   // byte address
+              // masked votes: shift 32 (shl/shr clamp to 0) on the lane's dummy word
+              sh[g] = ok ? (bc & 3u) * 8u : 32u;
+              addr[g] = ok ? (bc & ~3u) : dummy;
+            }
+  #pragma unroll
+            for (int g = 0; g < GL; ++g) old[g] = atom_add_shared(addr[g], shl_clamp(1u, sh[g]));
+            uint32_t omax = 0;
+  #pragma unroll
+            for (int g = 0; g < GL; ++g) {
+              const uint32_t oc = shr_clamp(old[g], sh[g]) & CMASK;   // 0 for masked votes
+              omax = max(omax, oc);
+              if (oc == T_raw) {   // this vote lifted the counter past T_raw (T_raw >= 1)
+                const int cell = (int)((addr[g] - raw_base - (uint32_t)(g * lvlc * CB)) >> (CB - 1)) + (int)(sh[g] / BITS);
+                const int cy = (int)__umulhi((uint32_t)cell, P.k2o.rawp_magic), cx = cell - cy * rawp;
+                const int ix = cx - (hal - 1), iy = cy - (hal - 1);
+                if ((unsigned)ix >= (unsigned)(T + 2) || (unsigned)iy >= (unsigned)(T + 2)) continue;   // not in the ring
+                const int li = L0 + g;
+                const int h = atomicAdd(&hcnt[li], 1);
+                if (h < hot_cap) {
+                  hcell[slot_of[g] * hot_cap + h] = (uint16_t)((iy << 8) | ix);
+                  if (CB == 2) {   // (byte counters take their S tasks straight from the level lists)
+                    const int slot = tK[li] <= SMALL_K ? atomicAdd(&s_ntask[0], 1)
+                                                       : G * hot_cap - 1 - atomicAdd(&s_ntask[1], 1);
+                    tasks[slot] = (uint16_t)((g << 12) | h);
+                  }
+                } else {
+                  atomicOr(s_flags, OVF_HOTSPOTS);
                 }
-              } else {
-                atomicOr(s_flags, OVF_HOTSPOTS);
               }
             }
+            if (CB == 1) ovf |= omax >= (uint32_t)P.u8_limit;
           }
-          if (CB == 1) ovf |= omax >= (uint32_t)P.u8_limit;
-        }
+        };
+        const int nl = min(G, nlev - L0);
+        if (nl == 1 && G > 1) run_votes(std::integral_constant<int, 1>{});
+        else run_votes(std::integral_constant<int, G>{});
         if (CB == 1 && __any_sync(FULL, ovf) && lane == 0) *s_ovf = 1;
       }
       __syncthreads();
@@ -535,7 +543,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
         {   // clear the step's level buffers
           uint4* r4 = reinterpret_cast<uint4*>(raw32);
           constexpr int U = 4;
-          const int n16 = (CB * G * lvlc) / 16;
+          const int n16 = (CB * min(G, nlev - L0) * lvlc) / 16;   // the levels the step used
           int i = tid;
           for (; i + (U - 1) * NT < n16; i += U * NT) {
 #pragma unroll

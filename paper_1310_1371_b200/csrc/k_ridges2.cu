@@ -42,7 +42,7 @@ struct K1SSmem {                       // dynamic shared memory of k_ridges2
   double2 sD[RB + 2][KS_COLS];         // rho ring (x = NOT_CAND: no candidate)
   double sK[RB + 2][KS_COLS];          // kappa ring
   double sG[RB][KS_COLS];              // G rows
-  int sI[RB][KS_COLS];                 // input rows (as int)
+  int sI[KS_COLS][RB];                 // input rows (as int), a column's RB rows adjacent
   unsigned sBal[2][RB][KS_COLS / 32];  // ridge ballots of a step's rows, by parity
   int sCur[KS_NB];                     // ridges so far in the current row of each bin
 };
@@ -119,7 +119,7 @@ k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, in
     if (compute) {
 #pragma unroll
       for (int r = 0; r < RB; ++r) {
-        sI[r][tid] = (int)pf[r];
+        sI[tid][r] = (int)pf[r];
         const int yy = min(max(yi0 + RB + r, 0), H - 1);
         pf[r] = reinterpret_cast<const PixT*>(frame + (int64_t)yy * pitch)[xc];
       }
@@ -161,16 +161,28 @@ k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, in
     }
     if (!compute) break;
     // 2. row passes R(yi) (int32 exact) -> column window; G(yg) (fp64 exact), RB rows
+    int accr[RB];   // R of the RB rows: one (vector) load per tap serves all of them
+#pragma unroll
+    for (int r = 0; r < RB; ++r) accr[r] = 0;
+    if (doR) {
+#pragma unroll
+      for (int j = 0; j < NTAP; ++j) {
+        const int* col = sI[tid - KS + j];
+        if constexpr (RB == 2) {
+          const int2 v = *reinterpret_cast<const int2*>(col);
+          accr[0] += q[j] * v.x;
+          accr[1] += q[j] * v.y;
+        } else {
+#pragma unroll
+          for (int r = 0; r < RB; ++r) accr[r] += q[j] * col[r];
+        }
+      }
+    }
 #pragma unroll
     for (int r = 0; r < RB; ++r) {
-      int acc = 0;
-      if (doR) {
-#pragma unroll
-        for (int j = 0; j < NTAP; ++j) acc += q[j] * sI[r][tid - KS + j];
-      }
 #pragma unroll
       for (int j = 0; j < NTAP - 1; ++j) wR[j] = wR[j + 1];
-      wR[NTAP - 1] = (uint32_t)acc;
+      wR[NTAP - 1] = (uint32_t)accr[r];
       // G = sum q_j R_j < 2^53 in 64-bit integers (symmetric taps), then exactly to fp64
       unsigned long long g = (unsigned long long)(uint32_t)q[KS] * wR[KS];
 #pragma unroll
