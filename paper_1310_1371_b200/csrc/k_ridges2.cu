@@ -172,6 +172,12 @@ k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, in
           const int2 v = *reinterpret_cast<const int2*>(col);
           accr[0] += q[j] * v.x;
           accr[1] += q[j] * v.y;
+        } else if constexpr (RB == 4) {
+          const int4 v = *reinterpret_cast<const int4*>(col);
+          accr[0] += q[j] * v.x;
+          accr[1] += q[j] * v.y;
+          accr[2] += q[j] * v.z;
+          accr[3] += q[j] * v.w;
         } else {
 #pragma unroll
           for (int r = 0; r < RB; ++r) accr[r] += q[j] * col[r];
