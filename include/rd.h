@@ -141,6 +141,19 @@ rd_status rd_query_overflow(rd_detector* det, int32_t n_frames, int32_t* h_flags
  * hotspots, peaks).  Synchronous copy. */
 rd_status rd_get_stats(rd_detector* det, int32_t n_frames, rd_frame_stats* h_stats);
 
+/* Classification (A9) of frame `frame` of the last rd_detect
+ * call: for each of the frame's rings, in the order rd_detect returned them, the ridge
+ * pixels in its annulus (r-w)_+^2 <= (x-cx)^2 + (y-cy)^2 <= (r+w)^2 (non-exclusive: a pixel
+ * may support several rings), packed x | y << 16, ordered by ridge bin (bin rows, bin
+ * columns) and row-major within a bin.  Computed on the GPU on request (not part of
+ * rd_detect).  h_offsets[0..min(offsets_cap, n_rings + 1)) receives the CSR offsets
+ * (ring i owns members [h_offsets[i], h_offsets[i+1])), h_members the first min(cap,
+ * total) members, *n_total the total (call again with a larger cap if needed; NULL
+ * buffers with cap 0 query the sizes).  Synchronous.  RD_ERR_CAPACITY if the frame
+ * overflowed (its ring count was -1); RD_ERR_STATE if there was no such frame. */
+rd_status rd_ring_members(rd_detector* det, int32_t frame, int32_t* h_offsets, int32_t offsets_cap,
+                          uint32_t* h_members, int64_t cap, int64_t* n_total);
+
 /* Debug: ridge list of frame `frame` of the last call, in tile order (32x32 tiles,
  * row-major within a tile).  Writes min(n, cap) records, sets *n. */
 rd_status rd_dump_ridges(rd_detector* det, int32_t frame, rd_ridge* h_out, int64_t cap, int64_t* n);

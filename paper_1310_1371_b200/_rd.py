@@ -39,7 +39,7 @@ assert RING_DTYPE.itemsize == 64
 
 EXPORTS = ("rd_abi_version", "rd_status_string", "rd_last_error", "rd_config_init", "rd_create", "rd_destroy",
            "rd_detect", "rd_detect_host", "rd_sync", "rd_query_overflow", "rd_get_stats", "rd_dump_ridges",
-           "rd_dump_hotspots", "rd_eigen", "rd_set_timing", "rd_kernel_times", "rd_phase_cycles")
+           "rd_dump_hotspots", "rd_eigen", "rd_set_timing", "rd_kernel_times", "rd_phase_cycles", "rd_ring_members")
 
 
 class RDError(RuntimeError):
@@ -79,6 +79,7 @@ def lib():
         L.rd_set_timing.argtypes = [vp, i32]
         L.rd_kernel_times.argtypes = [vp, vp, C.POINTER(i32)]
         L.rd_phase_cycles.argtypes = [vp, i32, vp]
+        L.rd_ring_members.argtypes = [vp, i32, vp, i32, vp, i64, C.POINTER(i64)]
         for n in EXPORTS:
             if n not in ("rd_abi_version", "rd_status_string", "rd_last_error"):
                 getattr(L, n).restype = C.c_int

@@ -138,6 +138,78 @@ __global__ void __launch_bounds__(K3_THREADS) k_fit(Params P, Ring* __restrict__
   }
 }
 
+// Classification output (A9): the ridge pixels of every ring of
+// frame f, rings in the canonical order of K3's output.  One CTA; a warp per ring scans the
+// ridge bins its annulus overlaps in the same order and with the same exact test as K3.
+// write == 0: offsets[p + 1] = member count of ring p (offsets[0] = 0, prefix summed here);
+// write == 1: members (x | y << 16) of ring p at offsets[p] .., in bin order (bin rows, bin
+// columns, row-major within a bin).  The frame must not have overflowed (K3 wrote -1).
+__global__ void __launch_bounds__(K3_THREADS) k_members(Params P, int f, int write, int* offsets,
+                                                         uint32_t* members) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  Peak* sp = reinterpret_cast<Peak*>(smem);                    // [ring_cap]
+  int* order = reinterpret_cast<int*>(sp + P.ring_cap);         // [ring_cap]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int npk = min(P.peak_count[f], P.ring_cap);
+  for (int i = tid; i < npk; i += K3_THREADS) sp[i] = P.peaks[(int64_t)f * P.ring_cap + i];
+  __syncthreads();
+  for (int i = tid; i < npk; i += K3_THREADS) {   // canonical (r, cy, cx) order, as K3
+    const Peak a = sp[i];
+    int rank = 0;
+    for (int j = 0; j < npk; ++j) {
+      const Peak b = sp[j];
+      rank += (b.r < a.r) || (b.r == a.r && (b.y < a.y || (b.y == a.y && b.x < a.x)));
+    }
+    order[rank] = i;
+  }
+  __syncthreads();
+  const int64_t fbins = (int64_t)f * P.nbx * P.nby;
+  for (int p = warp; p < npk; p += K3_THREADS / 32) {
+    const Peak pk = sp[order[p]];
+    const int w = P.lvlAnn[pk.r - P.r_lo];
+    const long long lo = max(pk.r - w, 0), hi = (long long)pk.r + w;
+    const long long lo2 = lo * lo, hi2 = hi * hi;
+    const int bx0 = max((pk.x - (int)hi) / T1, 0), bx1 = min((pk.x + (int)hi) / T1, P.nbx - 1);
+    const int by0 = max((pk.y - (int)hi) / T1, 0), by1 = min((pk.y + (int)hi) / T1, P.nby - 1);
+    int n = write ? offsets[p] : 0;
+    for (int by = by0; by <= by1; ++by)
+      for (int bx = bx0; bx <= bx1; ++bx) {
+        const int64_t b = fbins + by * P.nbx + bx;
+        const int cnt = P.bin_count[b];
+        const uint32_t* xy = P.bin_xy + b * P.ridge_cap;
+        for (int k0 = 0; k0 < cnt; k0 += 32) {
+          const int k = k0 + lane;
+          uint32_t v = 0;
+          bool in = false;
+          if (k < cnt) {
+            v = xy[k];
+            const long long u = (long long)(v & 0xFFFFu) - pk.x, vv = (long long)(v >> 16) - pk.y;
+            const long long z = u * u + vv * vv;
+            in = z >= lo2 && z <= hi2;
+          }
+          const unsigned bal = __ballot_sync(0xffffffffu, in);
+          if (write && in) members[n + __popc(bal & ((1u << lane) - 1u))] = v;
+          n += __popc(bal);
+        }
+      }
+    if (!write && lane == 0) offsets[p + 1] = n;
+  }
+  if (!write) {
+    __syncthreads();
+    if (tid == 0) {
+      offsets[0] = 0;
+      for (int p = 0; p < npk; ++p) offsets[p + 1] += offsets[p];
+    }
+  }
+}
+
+cudaError_t launch_members(const Params& P, int f, int write, int* offsets, uint32_t* members, cudaStream_t st) {
+  const size_t sm = (size_t)P.ring_cap * (sizeof(Peak) + sizeof(int));
+  cudaFuncSetAttribute(k_members, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_members<<<1, K3_THREADS, sm, st>>>(P, f, write, offsets, members);
+  return cudaGetLastError();
+}
+
 size_t k_fit_smem(const Params& P) { return (size_t)P.ring_cap * (sizeof(Peak) + sizeof(int)); }
 
 cudaError_t launch_fit(int n_frames, const Params& P, void* rings, int* counts, cudaStream_t st) {

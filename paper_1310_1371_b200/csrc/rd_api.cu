@@ -27,6 +27,7 @@ cudaError_t launch_hough2(int n_frames, const Params& P, bool wide, int G, int n
 size_t k_fit_smem(const Params& P);
 cudaError_t launch_fit(int n_frames, const Params& P, void* rings, int* counts, cudaStream_t st);
 cudaError_t launch_rays(int n_frames, const Params& P, cudaStream_t st);
+cudaError_t launch_members(const Params& P, int f, int write, int* offsets, uint32_t* members, cudaStream_t st);
 constexpr int RD_NEV = 5;   // timing events per rd_detect: K1 | K1.5 | K2 | K3
 }  // namespace rd
 
@@ -728,6 +729,42 @@ rd_status rd_get_stats(rd_detector* det, int32_t n, rd_frame_stats* h) {
   CK(cudaSetDevice(det->device));
   CK(cudaEventSynchronize(det->ev_last));
   CK(cudaMemcpy(h, det->P.stats, sizeof(Stats) * n, cudaMemcpyDeviceToHost));
+  return RD_OK;
+}
+
+rd_status rd_ring_members(rd_detector* det, int32_t frame, int32_t* h_offsets, int32_t offsets_cap,
+                          uint32_t* h_members, int64_t cap, int64_t* n_total) {
+  if (!det || !n_total || frame < 0 || frame >= det->max_batch || offsets_cap < 0 || cap < 0 ||
+      (offsets_cap > 0 && !h_offsets) || (cap > 0 && !h_members))
+    return RD_ERR_PARAM;
+  if (!det->have_last || frame >= det->last_n) return RD_ERR_STATE;
+  CK(cudaSetDevice(det->device));
+  CK(cudaEventSynchronize(det->ev_last));
+  const Params& P = det->P;
+  int flags = 0, npk = 0;
+  CK(cudaMemcpy(&flags, P.flags + frame, sizeof(int), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&npk, P.peak_count + frame, sizeof(int), cudaMemcpyDeviceToHost));
+  if (flags != 0 || npk > P.ring_cap) return RD_ERR_CAPACITY;   // the frame has no valid ring list
+  int* d_off = nullptr;
+  uint32_t* d_mem = nullptr;
+  rd_status result = RD_OK;
+  std::vector<int> off(npk + 1, 0);
+  cudaError_t e = cudaMalloc(&d_off, sizeof(int) * (npk + 1));
+  if (e == cudaSuccess) e = launch_members(P, frame, 0, d_off, nullptr, 0);
+  if (e == cudaSuccess) e = cudaMemcpy(off.data(), d_off, sizeof(int) * (npk + 1), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && off[npk] > 0) {
+    e = cudaMalloc(&d_mem, sizeof(uint32_t) * off[npk]);
+    if (e == cudaSuccess) e = launch_members(P, frame, 1, d_off, d_mem, 0);
+    if (e == cudaSuccess && cap > 0)
+      e = cudaMemcpy(h_members, d_mem, sizeof(uint32_t) * std::min<int64_t>(cap, off[npk]), cudaMemcpyDeviceToHost);
+  }
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) result = cuda_fail(e, "rd_ring_members");
+  cudaFree(d_off);
+  cudaFree(d_mem);
+  if (result != RD_OK) return result;
+  for (int i = 0; i < std::min(offsets_cap, npk + 1); ++i) h_offsets[i] = off[i];
+  *n_total = off[npk];
   return RD_OK;
 }
 

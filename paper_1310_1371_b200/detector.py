@@ -121,6 +121,19 @@ class Detector:
               "rd_dump_ridges")
         return out
 
+    def ring_members(self, frame: int) -> list[np.ndarray]:
+        """Classification of frame `frame` of the last detect(): per ring (output order), the
+        ridge pixels in its annulus as an (m, 2) int32 array of (x, y), in ridge-bin order."""
+        n = C.c_int64()
+        cnt = int(self.stats(frame + 1)["peaks"][frame])
+        off = np.zeros(cnt + 1, np.int32)
+        check(lib().rd_ring_members(self._h, frame, off.ctypes.data, cnt + 1, None, 0, C.byref(n)), "rd_ring_members")
+        mem = np.zeros(max(n.value, 1), np.uint32)
+        check(lib().rd_ring_members(self._h, frame, off.ctypes.data, cnt + 1, mem.ctypes.data, n.value, C.byref(n)),
+              "rd_ring_members")
+        xy = np.stack([mem[: n.value] & 0xFFFF, mem[: n.value] >> 16], axis=1).astype(np.int32)
+        return [xy[off[i]:off[i + 1]] for i in range(cnt)]
+
     def dump_hotspots(self, frame: int) -> np.ndarray:
         n = C.c_int64()
         check(lib().rd_dump_hotspots(self._h, frame, None, 0, C.byref(n)), "rd_dump_hotspots")

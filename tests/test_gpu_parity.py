@@ -269,6 +269,35 @@ def test_detect_host_many_chunks_two_slots(rdmod, force_redo, monkeypatch):
         assert hr[i, : hc[i]].tobytes() == ref[i].tobytes()
 
 
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_ring_members_match_annulus_definition(rdmod, cfg):
+    """rd_ring_members (A9): every ring's members are exactly the oracle's ridge pixels in
+    its annulus (r-w)_+^2 <= d^2 <= (r+w)^2, as many as the
+    ring's inliers, in ridge-bin order (bin row, bin column, row-major inside a bin)."""
+    params = synth.preset(cfg)
+    frames = synth.batch(cfg, 0, 7, 2)
+    det = _det(rdmod, params, max_batch=2)
+    rings, counts = det.detect(torch.from_numpy(frames).cuda())
+    det.sync()
+    out = det.rings_to_numpy(rings, counts)
+    p = oracle.params(**params)
+    for i in range(2):
+        R = oracle.ridges(p, frames[i])
+        rx, ry = R["x"].astype(np.int64), R["y"].astype(np.int64)
+        mem = det.ring_members(i)
+        assert len(mem) == len(out[i]) > 0
+        for ring, m in zip(out[i], mem):
+            r = int(ring["r"])
+            w = oracle.annulus_halfwidth(p, r)
+            lo, hi = max(r - w, 0), r + w
+            d2 = (rx - int(ring["cx"])) ** 2 + (ry - int(ring["cy"])) ** 2
+            sel = (d2 >= lo * lo) & (d2 <= hi * hi)
+            assert len(m) == int(ring["inliers"]) == int(sel.sum())
+            assert {(int(a), int(b)) for a, b in zip(rx[sel], ry[sel])} == {(int(a), int(b)) for a, b in m}
+            key = [(int(y) // 32, int(x) // 32, int(y), int(x)) for x, y in m]
+            assert key == sorted(key)
+
+
 def test_full_batch_cfg4_dense(rdmod):
     """cfg4 at BASELINE size (512 frames of 1024x1024, 200 rings): sampled frames vs the
     oracle; every frame valid (no capacity overflow with the dense-config capacities)."""
