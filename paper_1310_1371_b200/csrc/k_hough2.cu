@@ -89,12 +89,13 @@ size_t k_hough2_layout(Params& P, int G, int nt, int cb) {
   K2Layout& L = P.k2o;
   const int NSLOT = G + 2;
   (void)nt;
-  const int T = P.k2t, hot_cap = P.hot_cap, nlev = P.n_levels;
+  const int hot_cap = P.hot_cap, nlev = P.n_levels;
   L.cb = cb;
-  L.raws = T + 2 * P.hal;
+  L.raws = P.k2ty + 2 * P.hal;   // rows
+  L.rawc = P.k2t + 2 * P.hal;    // columns
   // row pitch of an odd number of 32-bit words: the rows of a window fall in distinct banks
   const int cpw = 4 / cb;   // cells per word
-  L.rawp = ((L.raws + cpw - 1) / cpw) | 1;
+  L.rawp = ((L.rawc + cpw - 1) / cpw) | 1;
   L.rawp *= cpw;
   L.lvlc = (L.raws * L.rawp + 15) & ~15;   // 16-byte aligned level buffers (bulk clears)
   size_t o = 0;
@@ -161,7 +162,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
   int* s_ovf = cnt + 13;    // a byte counter passed 255
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int T = P.k2t, hal = P.hal, hot_cap = P.hot_cap;
+  const int TX = P.k2t, TY = P.k2ty, hal = P.hal, hot_cap = P.hot_cap;
   const int rawp = P.k2o.rawp, lvlc = P.k2o.lvlc, rcap = P.k2_rcap, ecap = P.entry_cap;
   const int ntiles = P.ntx * P.nty;
   const uint32_t T_raw = (uint32_t)P.T_raw;
@@ -207,7 +208,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
     const int fw = item / ntiles, tile = item - fw * ntiles;
     const int f = redo_pass ? P.redo_list[1 + fw] : fw;
     const int tyi = tile / P.ntx, txi = tile - tyi * P.ntx;
-    const int X0 = txi * T, Y0 = tyi * T;
+    const int X0 = txi * TX, Y0 = tyi * TY;
     const int RX0 = X0 - hal, RY0 = Y0 - hal;   // raw buffer origin (frame coordinates)
     const int64_t tl = (int64_t)f * ntiles + tile;
     const int ne = min(P.ray_count[tl], P.entry_cap);
@@ -259,7 +260,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
         for (int g = 0; g < G; ++g) slot_of[g] = (L0 + g) % NSLOT;
         const uint32_t raw_base = smem_u32(raw32);
         const uint32_t dummy = smem_u32(dummy_w) + 4u * lane;   // masked votes add 0 to a private word
-        const int bx0 = max(0, -RX0), bxs = min(P.k2o.raws - 1, P.W - 1 - RX0) - bx0;
+        const int bx0 = max(0, -RX0), bxs = min(P.k2o.rawc - 1, P.W - 1 - RX0) - bx0;
         const int by0 = max(0, -RY0), bys = min(P.k2o.raws - 1, P.H - 1 - RY0) - by0;
         bool ovf = false;
         // the votes of GL levels (GL = G, or 1 for a last step with a single level: no masked
@@ -321,7 +322,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
                 const int cell = (int)((addr[g] - raw_base - (uint32_t)(g * lvlc * CB)) >> (CB - 1)) + (int)(sh[g] / BITS);
                 const int cy = (int)__umulhi((uint32_t)cell, P.k2o.rawp_magic), cx = cell - cy * rawp;
                 const int ix = cx - (hal - 1), iy = cy - (hal - 1);
-                if ((unsigned)ix >= (unsigned)(T + 2) || (unsigned)iy >= (unsigned)(T + 2)) continue;   // not in the ring
+                if ((unsigned)ix >= (unsigned)(TX + 2) || (unsigned)iy >= (unsigned)(TY + 2)) continue;   // not in the ring
                 const int li = L0 + g;
                 const int h = atomicAdd(&hcnt[li], 1);
                 if (h < hot_cap) {
@@ -420,7 +421,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
             if (valid && hl == 0) {
               const uint16_t rv = rawc[g * lvlc + (iy - 1 + hal) * rawp + (ix - 1 + hal)];
               hS[sl * hot_cap + h] = (S << 8) | rv;   // S < 2^46, raw < 256
-              if (ix >= 1 && ix <= T && iy >= 1 && iy <= T) {   // interior hotspot
+              if (ix >= 1 && ix <= TX && iy >= 1 && iy <= TY) {   // interior hotspot
                 ++my_hot;
                 if (P.debug) {
                   const int kd = atomicAdd(&P.dbg_count[f], 1);
@@ -509,7 +510,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
             hS[sl * hot_cap + h] = S;
             const uint16_t rv = *ctr;
             hraw[sl * hot_cap + h] = rv;
-            if (ix >= 1 && ix <= T && iy >= 1 && iy <= T) {   // interior hotspot
+            if (ix >= 1 && ix <= TX && iy >= 1 && iy <= TY) {   // interior hotspot
               ++my_hot;
               if (P.debug) {
                 const int kd = atomicAdd(&P.dbg_count[f], 1);

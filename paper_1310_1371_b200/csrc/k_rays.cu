@@ -51,20 +51,20 @@ __device__ __forceinline__ void half_ge(float a, float b, float& lo, float& hi) 
 __global__ void __launch_bounds__(256, RD_K15_MINB) k_rays(Params P) {
   const int f = blockIdx.y;
   const int by = blockIdx.x;
-  const int T = P.k2t, hal = P.hal, W = P.W, H = P.H;
+  const int TX = P.k2t, TY = P.k2ty, hal = P.hal, W = P.W, H = P.H;
   const int rlo = P.r_lo, rhi = P.r_hi;
   const float m = P.k_slope, c = P.k_icpt;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t tile0 = (int64_t)f * P.ntx * P.nty;
   // tiles any ray of a bin can reach: |offset| <= r_hi, halo <= hal
   const int reach = rhi + hal + 1;
-  const int wy0 = max((by * T1 - reach) / T, 0), wy1 = min((by * T1 + T1 - 1 + reach) / T, P.nty - 1);
+  const int wy0 = max((by * T1 - reach) / TY, 0), wy1 = min((by * T1 + T1 - 1 + reach) / TY, P.nty - 1);
   int my_votes = 0;
   for (int bx = warp; bx < P.nbx; bx += blockDim.x >> 5) {
     const int64_t fb = (int64_t)f * P.nbx * P.nby + by * P.nbx + bx;
     const int cnt = P.bin_count[fb];
     if (cnt == 0) continue;
-    const int wx0 = max((bx * T1 - reach) / T, 0), wx1 = min((bx * T1 + T1 - 1 + reach) / T, P.ntx - 1);
+    const int wx0 = max((bx * T1 - reach) / TX, 0), wx1 = min((bx * T1 + T1 - 1 + reach) / TX, P.ntx - 1);
     for (int j0 = 0; j0 < 2 * cnt; j0 += 32) {
       const int j = j0 + lane;
       const bool valid = j < 2 * cnt;
@@ -101,20 +101,20 @@ __global__ void __launch_bounds__(256, RD_K15_MINB) k_rays(Params P) {
         unsigned kbal = 0, hits = 0;
 #pragma unroll
         for (int ky = 0; ky < 3; ++ky) {
-          const int ty = wy0 + ky, Y0 = ty * T;
+          const int ty = wy0 + ky, Y0 = ty * TY;
           float ylo = flo, yhi = fhi;
           half_ge(fv + m, (float)Y0 - 1.5f - c - fy, ylo, yhi);
-          half_ge(m - fv, fy - (float)(Y0 + T) - 0.5f - c, ylo, yhi);
-          const bool yhit = valid && ty <= wy1 && sy1 >= Y0 && sy0 <= Y0 + T - 1 && yhi >= ylo - 2.f;
+          half_ge(m - fv, fy - (float)(Y0 + TY) - 0.5f - c, ylo, yhi);
+          const bool yhit = valid && ty <= wy1 && sy1 >= Y0 && sy0 <= Y0 + TY - 1 && yhi >= ylo - 2.f;
 #pragma unroll
           for (int kx = 0; kx < 3; ++kx) {
-            const int k = 3 * ky + kx, tx = wx0 + kx, X0 = tx * T;
-            bool hit = yhit && tx <= wx1 && sx1 >= X0 && sx0 <= X0 + T - 1;
+            const int k = 3 * ky + kx, tx = wx0 + kx, X0 = tx * TX;
+            bool hit = yhit && tx <= wx1 && sx1 >= X0 && sx0 <= X0 + TX - 1;
             int ra = 0, rb = -1;
             if (hit) {
               float lo = ylo, hi = yhi;
               half_ge(fu + m, (float)X0 - 1.5f - c - fx, lo, hi);
-              half_ge(m - fu, fx - (float)(X0 + T) - 0.5f - c, lo, hi);
+              half_ge(m - fu, fx - (float)(X0 + TX) - 0.5f - c, lo, hi);
               ra = max((int)floorf(lo) - 1, rlo);
               rb = min((int)ceilf(hi) + 1, rhi);
               hit = hi >= lo - 2.f && ra <= rb;
@@ -146,20 +146,20 @@ __global__ void __launch_bounds__(256, RD_K15_MINB) k_rays(Params P) {
         continue;
       }
       for (int ty = wy0; ty <= wy1; ++ty) {
-        const int Y0 = ty * T;
+        const int Y0 = ty * TY;
         float ylo = flo, yhi = fhi;
         half_ge(fv + m, (float)Y0 - 1.5f - c - fy, ylo, yhi);
-        half_ge(m - fv, fy - (float)(Y0 + T) - 0.5f - c, ylo, yhi);
-        const bool yhit = valid && sy1 >= Y0 && sy0 <= Y0 + T - 1 && yhi >= ylo - 2.f;
+        half_ge(m - fv, fy - (float)(Y0 + TY) - 0.5f - c, ylo, yhi);
+        const bool yhit = valid && sy1 >= Y0 && sy0 <= Y0 + TY - 1 && yhi >= ylo - 2.f;
         if (!__any_sync(0xffffffffu, yhit)) continue;
         for (int tx = wx0; tx <= wx1; ++tx) {
-          const int X0 = tx * T;
-          bool hit = yhit && sx1 >= X0 && sx0 <= X0 + T - 1;
+          const int X0 = tx * TX;
+          bool hit = yhit && sx1 >= X0 && sx0 <= X0 + TX - 1;
           int ra = 0, rb = -1;
           if (hit) {
             float lo = ylo, hi = yhi;
             half_ge(fu + m, (float)X0 - 1.5f - c - fx, lo, hi);
-            half_ge(m - fu, fx - (float)(X0 + T) - 0.5f - c, lo, hi);
+            half_ge(m - fu, fx - (float)(X0 + TX) - 0.5f - c, lo, hi);
             ra = max((int)floorf(lo) - 1, rlo);
             rb = min((int)ceilf(hi) + 1, rhi);
             hit = hi >= lo - 2.f && ra <= rb;

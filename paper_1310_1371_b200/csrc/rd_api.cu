@@ -277,7 +277,33 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
     // The 16-bit redo pass must use the main pass's tile side (K1.5 routes rays per tile).
     // RD_K2_SHAPE2="G,threads,ctas" or "T,G,threads,ctas" puts a shape first;
     // RD_K2_CB=2 forces 16-bit counters.
-    auto pick = [&](Params& Q, int cb, int& G, int& nt, int& minb, int forceT) {
+    // Tiles: for a shape's side T, the rectangular tiling of the frame (nx x ny tiles of
+    // ceil(W/nx) x ceil(H/ny)) whose raw buffers are no larger than T's square one and that
+    // minimises buffer cells (votes, clears) plus a per-tile cost: cfg3 gets 8 x 8 tiles of
+    // 128 x 86 instead of 10 x 7 of 104 x 104 (the last row and column only partly used).
+    auto tiling = [&](int T, int& tx, int& ty) {
+      const long long hh = 2LL * P.hal;
+      double slack = 1.03;   // raw buffers up to 3 % larger than T's square (fewer resident rays)
+      if (const char* env = getenv("RD_K2_TSLACK")) slack = atof(env);
+      const double budget = slack * (double)((T + hh) * (T + hh));
+      double best = 1e300;
+      tx = ty = T;
+      for (int nx = 1; nx <= c.width; ++nx) {
+        const int TX = (c.width + nx - 1) / nx;
+        if (TX > 254) continue;
+        if (TX < 16) break;
+        for (int ny = 1; ny <= c.height; ++ny) {
+          const int TY = (c.height + ny - 1) / ny;
+          if (TY > 254) continue;
+          if (TY < 16) break;
+          if ((double)((TX + hh) * (TY + hh)) > budget) continue;
+          const double cost = (double)nx * ny * ((double)(TX + hh) * (TY + hh) + 2000.0);
+          if (cost < best) best = cost, tx = TX, ty = TY;
+          break;   // larger ny only adds tiles
+        }
+      }
+    };
+    auto pick = [&](Params& Q, int cb, int& G, int& nt, int& minb, int forceT, int forceTY) {
       std::vector<Shape> sh = cb == 1 ? std::vector<Shape>{{104, 4, 512, 2}, {96, 4, 512, 2}, {64, 4, 256, 3}, {64, 4, 384, 2},
                                                            {64, 8, 512, 1}}
                                       : std::vector<Shape>{{64, 4, 384, 2}, {64, 4, 512, 2}, {64, 8, 512, 1},
@@ -293,7 +319,14 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
       for (const Shape& s : sh) {
         if (!k_hough2_has_shape(cb, s.G, s.nt, s.minb)) continue;
         if (cb == 1 && Q.wstride - 1 > 15) break;   // byte-counter windows: 2K + 1 <= 31 rows per half-warp
-        Q.k2t = forceT ? forceT : s.T;
+        if (forceT) {
+          Q.k2t = forceT;
+          Q.k2ty = forceTY;
+        } else if (getenv("RD_K2_SQUARE")) {   // square tiles of side T (A/B)
+          Q.k2t = Q.k2ty = s.T;
+        } else {
+          tiling(s.T, Q.k2t, Q.k2ty);
+        }
         const size_t limit = s.minb == 1 ? smax : std::min(smax, sm_sm / s.minb - 1024);
           Q.k2_rcap = 256;
         if (k_hough2_layout(Q, s.G, s.nt, cb) > limit) continue;
@@ -314,12 +347,13 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
     };
     det->k2_cb = 1;
     if (const char* env = getenv("RD_K2_CB")) det->k2_cb = atoi(env) == 2 ? 2 : 1;
-    if (det->k2_cb == 1) pick(P, 1, det->G, det->k2_threads, det->k2_minb, 0);
+    if (det->k2_cb == 1) pick(P, 1, det->G, det->k2_threads, det->k2_minb, 0, 0);
     det->P16 = P;
-    pick(det->P16, 2, det->G16, det->k2_threads16, det->k2_minb16, det->G ? P.k2t : 0);
+    pick(det->P16, 2, det->G16, det->k2_threads16, det->k2_minb16, det->G ? P.k2t : 0, det->G ? P.k2ty : 0);
     if (det->G == 0 && det->G16 != 0) {   // 16-bit counters as the only pass
       det->k2_cb = 2;
       P.k2t = det->P16.k2t;
+      P.k2ty = det->P16.k2ty;
       P.k2_rcap = det->P16.k2_rcap;
       P.k2o = det->P16.k2o;
       det->G = det->G16;
@@ -331,7 +365,7 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   if (det->G == 0) {   // no persistent shape fits (large halo or capacities): one CTA per tile
     det->k2_impl = 1;
     for (const Shape& s : shapes) {
-      P.k2t = s.T;
+      P.k2t = P.k2ty = s.T;
       const size_t need = k_hough_smem(P, s.G);
       const size_t limit = s.minb == 1 ? smax : std::min(smax, sm_sm / s.minb - 1024);
       if (need <= limit) {
@@ -343,14 +377,14 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
     }
   }
   if (getenv("RD_K2_VERBOSE"))
-    fprintf(stderr, "rd: K2 impl %d cb %d G %d threads %d ctas/SM %d smem %d rcap %d | redo G %d threads %d "
-            "ctas/SM %d smem %d rcap %d\n", det->k2_impl, det->k2_cb, det->G, det->k2_threads, det->k2_minb,
+    fprintf(stderr, "rd: K2 tiles %dx%d impl %d cb %d G %d threads %d ctas/SM %d smem %d rcap %d | redo G %d threads %d "
+            "ctas/SM %d smem %d rcap %d\n", P.k2t, P.k2ty, det->k2_impl, det->k2_cb, det->G, det->k2_threads, det->k2_minb,
             det->k2_impl == 2 ? P.k2o.total : (int)k_hough_smem(P, det->G), P.k2_rcap, det->G16,
             det->k2_threads16, det->k2_minb16, det->P16.k2o.total, det->P16.k2_rcap);
   P.ntx = (c.width + P.k2t - 1) / P.k2t;
-  P.nty = (c.height + P.k2t - 1) / P.k2t;
+  P.nty = (c.height + P.k2ty - 1) / P.k2ty;
   {   // K1.5 tests a bin's rays against a window of at most 64 Hough tiles
-    const int reach = P.r_hi + P.hal + 1, wspan = (2 * reach + T1) / P.k2t + 2;
+    const int reach = P.r_hi + P.hal + 1, wspan = (2 * reach + T1) / std::min(P.k2t, P.k2ty) + 2;
     if (wspan * wspan > 64) {
       delete det;
       snprintf(g_err, sizeof g_err, "search radius %d too large for the %d-px Hough tiles", c.r_max, P.k2t);
@@ -449,6 +483,7 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   {   // the redo pass: same buffers, its own layout, shape and the redo list
     Params Q = P;
     Q.k2t = det->P16.k2t;
+    Q.k2ty = det->P16.k2ty;
     Q.k2_rcap = det->P16.k2_rcap;
     Q.k2o = det->P16.k2o;
     e = cudaMalloc(&det->d_redo_list, sizeof(int) * 2 * (B + 1));   // one list per slot (frame_view)
@@ -523,6 +558,7 @@ static void frame_view(const rd_detector* det, int f0, int slot, Params& V, Para
   V.k2_work = P.k2_work + 2 * slot;   // [main, redo] work counters of the slot
   V16 = V;
   V16.k2t = det->P16.k2t;
+  V16.k2ty = det->P16.k2ty;
   V16.k2_rcap = det->P16.k2_rcap;
   V16.k2o = det->P16.k2o;
   V16.redo_list = det->P16.redo_list + (int64_t)slot * (det->max_batch + 1);

@@ -31,7 +31,8 @@ struct Stats {         // per-frame counters (same layout as rd_frame_stats)
 
 // Shared-memory layout of the persistent Hough kernel (byte offsets; host-computed)
 struct K2Layout {
-  int cb, raws, rawp, lvlc;   // counter bytes, raw side, row pitch (cells), cells per level
+  int cb, raws, rawp, lvlc;   // counter bytes, raw rows, row pitch (cells), cells per level
+  int rawc;                   // raw columns (tile width + 2 halo); raws = tile height + 2 halo
   int raw, hS, sd, rr, xy, hcell, hraw, task, cand, cdef, act, hcnt, w, k, tn, dummy, total;
   uint32_t rawp_magic;        // ceil(2^32 / rawp): cell / rawp = umulhi(cell, magic) for cells < 2^16
 };
@@ -64,7 +65,8 @@ struct Params {
   uint32_t* bin_xy;             // [F][bins][ridge_cap] x | y<<16
   double2* bin_d;               // [F][bins][ridge_cap] (dx, dy)
   // Hough tiles (K2)
-  int k2t;                      // Hough tile side (T x T accumulator cells per CTA)
+  int k2t;                      // Hough tile width (k2t x k2ty accumulator cells per CTA)
+  int k2ty;                     // Hough tile height (the persistent K2 balances the tiling; else = k2t)
   int ntx, nty;                 // Hough tiles per frame
   int entry_cap, hot_cap;
   int* ray_count;               // [F][tiles] voting rays routed to each Hough tile (K1.5)
