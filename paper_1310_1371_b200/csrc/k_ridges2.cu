@@ -3,8 +3,8 @@
 // the 32x32 bins.
 //
 // Rows A1-A4 of DESIGN.md §1 ("Directed ridge detection"; SI steps 1-2,
-// PAPER.md:919-931).  A CTA owns a vertical strip of KS_COLS = 256 frame columns (224
-// output columns = 7 ridge bins, 16 halo columns on each side) and a segment of rows; thread
+// PAPER.md:919-931).  A CTA owns a vertical strip of KS_COLS = 384 frame columns (352
+// output columns = 11 ridge bins, 16 halo columns on each side) and a segment of rows; thread
 // t owns column X0 - 16 + t and the CTA walks down the rows, RB input rows per step:
 //   R = q (x) I along x      from the input rows in shared memory         (int32, exact)
 //   G = q (x) R along y      2K_s+1 R values in a register window          (fp64, exact)
@@ -25,12 +25,15 @@
 namespace rd {
 
 namespace {
-constexpr int KS_COLS = 256;        // strip columns = threads per CTA
+#ifndef RD_K1_COLS
+#define RD_K1_COLS 384   // 352 output columns = 11 bins (cfg3: 3 strips); 256 and 320 measured slower
+#endif
+constexpr int KS_COLS = RD_K1_COLS; // strip columns = threads per CTA (32 + a multiple of 32)
 constexpr int KS_HALO = 16;         // halo columns on each side (>= K_s + 3)
 constexpr int KS_OUT = KS_COLS - 2 * KS_HALO;   // 224 output columns = 7 bins
 constexpr int KS_NB = KS_OUT / 32;  // bins per strip
 #ifndef RD_K1_MINB
-#define RD_K1_MINB 3
+#define RD_K1_MINB 2   // 2 CTAs of 384 threads at 80 registers
 #endif
 #ifndef RD_K1_RB
 #define RD_K1_RB 2
