@@ -78,6 +78,8 @@ struct rd_detector {
   int* d_counts_stage[NSTAGE] = {};
   cudaStream_t s_comp = nullptr, s_h2d = nullptr, s_d2h = nullptr;
   cudaStream_t s_comp2 = nullptr;   // chunks alternate between s_comp and s_comp2 (their tails overlap)
+  cudaStream_t s_half[2] = {nullptr, nullptr};   // rd_detect: the two halves of a large batch
+  cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
   int n_slots = 1;                  // frame regions of the internal buffers used by concurrent chunks
   cudaEvent_t ev_h2d[NSTAGE], ev_done[NSTAGE], ev_d2h[NSTAGE];
   cudaEvent_t ev_last = nullptr;
@@ -529,6 +531,11 @@ rd_status rd_destroy(rd_detector* det) {
     }
   }
   if (det->ev_last) cudaEventDestroy(det->ev_last);
+  for (int i = 0; i < 2; ++i) {
+    if (det->s_half[i]) cudaStreamDestroy(det->s_half[i]);
+    if (det->ev_join[i]) cudaEventDestroy(det->ev_join[i]);
+  }
+  if (det->ev_fork) cudaEventDestroy(det->ev_fork);
   for (cudaEvent_t e : det->tev) cudaEventDestroy(e);
   delete det;
   return RD_OK;
@@ -629,7 +636,35 @@ rd_status rd_detect(rd_detector* det, const void* d_frames, int64_t pitch, int64
   rd_status s = check_frames(det, d_frames, pitch, fstride, n);
   if (s != RD_OK) return s;
   CK(cudaSetDevice(det->device));
-  return detect_impl(det, d_frames, pitch, fstride, n, d_rings, d_counts, (cudaStream_t)stream);
+  cudaStream_t st = (cudaStream_t)stream;
+  // A large batch runs as two halves on two internal streams (disjoint frame views of the
+  // internal buffers), joined back into the caller's stream: each kernel's last partial
+  // wave overlaps the other half's kernels.  Per-kernel timing keeps one stream.
+  if (n >= 128 && !det->timing && !getenv("RD_NO_SPLIT")) {
+    if (!det->s_half[0]) {
+      for (int i = 0; i < 2; ++i) {
+        CK(cudaStreamCreateWithFlags(&det->s_half[i], cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&det->ev_join[i], cudaEventDisableTiming));
+      }
+      CK(cudaEventCreateWithFlags(&det->ev_fork, cudaEventDisableTiming));
+    }
+    const int h = n / 2;
+    CK(cudaEventRecord(det->ev_fork, st));
+    for (int i = 0; i < 2; ++i) CK(cudaStreamWaitEvent(det->s_half[i], det->ev_fork, 0));
+    s = detect_impl(det, d_frames, pitch, fstride, h, d_rings, d_counts, det->s_half[0], 0, 0);
+    if (s != RD_OK) return s;
+    s = detect_impl(det, (const char*)d_frames + (size_t)h * fstride, pitch, fstride, n - h,
+                    d_rings + (size_t)h * det->P.ring_cap, d_counts + h, det->s_half[1], h, 1);
+    if (s != RD_OK) return s;
+    for (int i = 0; i < 2; ++i) {
+      CK(cudaEventRecord(det->ev_join[i], det->s_half[i]));
+      CK(cudaStreamWaitEvent(st, det->ev_join[i], 0));
+    }
+    CK(cudaEventRecord(det->ev_last, st));
+    det->last_n = n;
+    return RD_OK;
+  }
+  return detect_impl(det, d_frames, pitch, fstride, n, d_rings, d_counts, st);
 }
 
 static rd_status ensure_host_path(rd_detector* det) {
