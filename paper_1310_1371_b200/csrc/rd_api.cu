@@ -6,6 +6,7 @@
 #include <cstring>
 #include <algorithm>
 #include <cstdlib>
+#include <tuple>
 #include <vector>
 
 #include "rd.h"
@@ -283,27 +284,29 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
     // ceil(W/nx) x ceil(H/ny)) whose raw buffers are no larger than T's square one and that
     // minimises buffer cells (votes, clears) plus a per-tile cost: cfg3 gets 8 x 8 tiles of
     // 128 x 86 instead of 10 x 7 of 104 x 104 (the last row and column only partly used).
-    auto tiling = [&](int T, int& tx, int& ty) {
+    auto tilings = [&](int T) {
       const long long hh = 2LL * P.hal;
-      double slack = 1.03;   // raw buffers up to 3 % larger than T's square (fewer resident rays)
+      double slack = 1.2;   // raw buffers up to 20 % larger than T's square (fewer resident rays)
       if (const char* env = getenv("RD_K2_TSLACK")) slack = atof(env);
       const double budget = slack * (double)((T + hh) * (T + hh));
-      double best = 1e300;
-      tx = ty = T;
+      std::vector<std::tuple<double, int, int>> cand;
       for (int nx = 1; nx <= c.width; ++nx) {
         const int TX = (c.width + nx - 1) / nx;
         if (TX > 254) continue;
-        if (TX < 16) break;
+        if (TX < std::max(16, T / 2)) break;   // no slivers (K1.5 windows grow as 1 / side)
         for (int ny = 1; ny <= c.height; ++ny) {
           const int TY = (c.height + ny - 1) / ny;
           if (TY > 254) continue;
-          if (TY < 16) break;
+          if (TY < std::max(16, T / 2)) break;
           if ((double)((TX + hh) * (TY + hh)) > budget) continue;
-          const double cost = (double)nx * ny * ((double)(TX + hh) * (TY + hh) + 2000.0);
-          if (cost < best) best = cost, tx = TX, ty = TY;
+          // buffer cells (votes, clears) plus a per-tile cost of 8000 cells (17 barrier-separated
+          // steps, the ray load): fitted to cfg3's measured 64, 63, 60, 56, 54-tile tilings
+          cand.emplace_back((double)nx * ny * ((double)(TX + hh) * (TY + hh) + 8000.0), TX, TY);
           break;   // larger ny only adds tiles
         }
       }
+      std::sort(cand.begin(), cand.end());
+      return cand;
     };
     auto pick = [&](Params& Q, int cb, int& G, int& nt, int& minb, int forceT, int forceTY) {
       std::vector<Shape> sh = cb == 1 ? std::vector<Shape>{{104, 4, 512, 2}, {96, 4, 512, 2}, {64, 4, 256, 3}, {64, 4, 384, 2},
@@ -326,11 +329,24 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
           Q.k2ty = forceTY;
         } else if (getenv("RD_K2_SQUARE")) {   // square tiles of side T (A/B)
           Q.k2t = Q.k2ty = s.T;
-        } else {
-          tiling(s.T, Q.k2t, Q.k2ty);
+        } else if (getenv("RD_K2_TILE") &&   // "TX,TY" (A/B)
+                   sscanf(getenv("RD_K2_TILE"), "%d,%d", &Q.k2t, &Q.k2ty) == 2 && Q.k2t >= 16 &&
+                   Q.k2t <= 254 && Q.k2ty >= 16 && Q.k2ty <= 254) {
+        } else {   // the cheapest tiling whose layout fits this shape with 256 resident rays
+          Q.k2t = Q.k2ty = s.T;
+          Q.k2_rcap = 256;
+          const size_t lim = s.minb == 1 ? smax : std::min(smax, sm_sm / s.minb - 1024);
+          for (const auto& t : tilings(s.T)) {
+            Q.k2t = std::get<1>(t);
+            Q.k2ty = std::get<2>(t);
+            Params Q16 = Q;   // the 16-bit redo pass must fit the same tiles (one CTA per SM)
+            const bool redo_fits = cb == 2 || k_hough2_layout(Q16, 4, 512, 2) <= smax;
+            if (redo_fits && k_hough2_layout(Q, s.G, s.nt, cb) <= lim) break;
+            Q.k2t = Q.k2ty = s.T;
+          }
         }
         const size_t limit = s.minb == 1 ? smax : std::min(smax, sm_sm / s.minb - 1024);
-          Q.k2_rcap = 256;
+        Q.k2_rcap = 256;
         if (k_hough2_layout(Q, s.G, s.nt, cb) > limit) continue;
         while (Q.k2_rcap < Q.entry_cap) {   // as many resident rays as fit
           Q.k2_rcap += 64;
