@@ -63,7 +63,8 @@ typedef struct rd_config {
   int32_t max_rings_per_frame;    /* output capacity per frame (default 1024) */
   int32_t max_ridges_per_tile;    /* ridges per 32x32 tile (default 512) */
   int32_t max_entries_per_tile;   /* voting rays per Hough tile (default 3072; tiles are 96x96 or 64x64) */
-  int32_t max_hotspots_per_level; /* hotspots per Hough tile per level (default 224) */
+  int32_t max_hotspots_per_level; /* hotspots per Hough tile per level (0 = automatic: 160 for ridges,
+                                     256 for edges; cfg3 ridges need < 128) */
   int32_t debug;                  /* 1: keep hotspot records for rd_dump_hotspots */
   /* ABI 2: feature selection ("replaced by directed edges ... replacing the
    * Hessian by the Gradient ... the gradient magnitude ... a local maximum along the gradient

@@ -131,7 +131,7 @@ rd_status rd_config_init(rd_config* c, int32_t width, int32_t height, int32_t pi
   c->max_rings_per_frame = 1024;
   c->max_ridges_per_tile = 512;
   c->max_entries_per_tile = 3072;
-  c->max_hotspots_per_level = 224;
+  c->max_hotspots_per_level = 0;   // automatic (rd_create)
   c->debug = 0;
   return RD_OK;
 }
@@ -166,7 +166,9 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   if (!c.max_rings_per_frame) c.max_rings_per_frame = 1024;
   if (!c.max_ridges_per_tile) c.max_ridges_per_tile = 512;
   if (!c.max_entries_per_tile) c.max_entries_per_tile = 3072;
-  if (!c.max_hotspots_per_level) c.max_hotspots_per_level = 224;
+  // automatic: cfg3 ridges need < 128 per level per Hough tile; directed edges vote about
+  // twice as much (one frame of the 600-frame robustness corpus needs > 160)
+  if (!c.max_hotspots_per_level) c.max_hotspots_per_level = c.feature == RD_FEATURE_EDGE ? 256 : 160;
   if (c.max_ridges_per_tile > T1 * T1) c.max_ridges_per_tile = T1 * T1;
   if (c.max_hotspots_per_level > 4095) return RD_ERR_PARAM;   // 12-bit hotspot index in K2 task lists
   if (c.max_entries_per_tile > k_hough_max_entries()) c.max_entries_per_tile = k_hough_max_entries();
@@ -286,7 +288,7 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
     // 128 x 86 instead of 10 x 7 of 104 x 104 (the last row and column only partly used).
     auto tilings = [&](int T) {
       const long long hh = 2LL * P.hal;
-      double slack = 1.2;   // raw buffers up to 20 % larger than T's square (fewer resident rays)
+      double slack = 1.3;   // raw buffers up to 30 % larger than T's square (fewer resident rays)
       if (const char* env = getenv("RD_K2_TSLACK")) slack = atof(env);
       const double budget = slack * (double)((T + hh) * (T + hh));
       std::vector<std::tuple<double, int, int>> cand;
