@@ -298,6 +298,26 @@ def test_ring_members_match_annulus_definition(rdmod, cfg):
             assert key == sorted(key)
 
 
+@pytest.mark.parametrize("env", [("RD_K2_SQUARE", "1"), ("RD_K2_TILE", "86,77"), ("RD_K2_TILE", "200,60")])
+def test_rings_independent_of_hough_tiling(rdmod, env, monkeypatch):
+    """The Hough tiling (square, rectangular, thin) changes how K1.5 routes rays and K2
+    sweeps tiles, never the result: every frame's ring list is byte-identical to the default
+    tiling's."""
+    params = synth.preset(3)
+    frames = torch.from_numpy(synth.batch(3, 0, 60, 6)).cuda()
+    det = _det(rdmod, params, max_batch=6)
+    rings, counts = det.detect(frames)
+    det.sync()
+    ref = det.rings_to_numpy(rings, counts)
+    monkeypatch.setenv(*env)
+    det2 = _det(rdmod, params, max_batch=6)
+    rings2, counts2 = det2.detect(frames)
+    det2.sync()
+    out = det2.rings_to_numpy(rings2, counts2)
+    for a, b in zip(ref, out):
+        assert len(a) > 20 and a.tobytes() == b.tobytes()
+
+
 def test_full_batch_cfg4_dense(rdmod):
     """cfg4 at BASELINE size (512 frames of 1024x1024, 200 rings): sampled frames vs the
     oracle; every frame valid (no capacity overflow with the dense-config capacities)."""
