@@ -79,8 +79,9 @@ struct rd_detector {
   int* d_counts_stage[NSTAGE] = {};
   cudaStream_t s_comp = nullptr, s_h2d = nullptr, s_d2h = nullptr;
   cudaStream_t s_comp2 = nullptr;   // chunks alternate between s_comp and s_comp2 (their tails overlap)
-  cudaStream_t s_half[2] = {nullptr, nullptr};   // rd_detect: the two halves of a large batch
-  cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
+  static constexpr int NPART = 4;    // frame-view slots: rd_detect parts / host-path chunks
+  cudaStream_t s_half[NPART] = {};   // rd_detect: the parts of a large batch
+  cudaEvent_t ev_fork = nullptr, ev_join[NPART] = {};
   int n_slots = 1;                  // frame regions of the internal buffers used by concurrent chunks
   cudaEvent_t ev_h2d[NSTAGE], ev_done[NSTAGE], ev_d2h[NSTAGE];
   cudaEvent_t ev_last = nullptr;
@@ -454,7 +455,7 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   ALLOC(det->d_ray_d, sizeof(double2) * B * ntl * P.entry_cap);
   ALLOC(det->d_ray_xy, sizeof(uint32_t) * B * ntl * P.entry_cap);
   ALLOC(det->d_ray_r, sizeof(uint32_t) * B * ntl * P.entry_cap);
-  det->counters_bytes = sizeof(Stats) * B + sizeof(int) * 3 * B + sizeof(int) * B * ntl + 16 + sizeof(int) * B;
+  det->counters_bytes = sizeof(Stats) * B + sizeof(int) * 3 * B + sizeof(int) * B * ntl + 8 * rd_detector::NPART + sizeof(int) * B;
   ALLOC(det->d_counters, det->counters_bytes);
   if (c.debug) ALLOC(det->d_dbg, sizeof(HotRec) * B * P.dbg_cap);
   // tables
@@ -489,7 +490,7 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   P.dbg_count = P.flags + B;
   P.ray_count = P.dbg_count + B;
   P.k2_work = P.ray_count + B * ntl;
-  P.redo = P.k2_work + 4;
+  P.redo = P.k2_work + 2 * rd_detector::NPART;
   P.redo_list = nullptr;
   P.force_redo = getenv("RD_K2_FORCE_REDO") ? 1 : 0;
   P.u8_limit = 255;
@@ -506,7 +507,7 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
     Q.k2ty = det->P16.k2ty;
     Q.k2_rcap = det->P16.k2_rcap;
     Q.k2o = det->P16.k2o;
-    e = cudaMalloc(&det->d_redo_list, sizeof(int) * 2 * (B + 1));   // one list per slot (frame_view)
+    e = cudaMalloc(&det->d_redo_list, sizeof(int) * rd_detector::NPART * (B + 1));   // one list per slot
     if (e != cudaSuccess) { rd_destroy(det); return cuda_fail(e, "cudaMalloc redo_list"); }
     Q.redo_list = (int*)det->d_redo_list;
     det->P16 = Q;
@@ -549,7 +550,7 @@ rd_status rd_destroy(rd_detector* det) {
     }
   }
   if (det->ev_last) cudaEventDestroy(det->ev_last);
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < rd_detector::NPART; ++i) {
     if (det->s_half[i]) cudaStreamDestroy(det->s_half[i]);
     if (det->ev_join[i]) cudaEventDestroy(det->ev_join[i]);
   }
@@ -586,7 +587,7 @@ static void frame_view(const rd_detector* det, int f0, int slot, Params& V, Para
   V16.k2ty = det->P16.k2ty;
   V16.k2_rcap = det->P16.k2_rcap;
   V16.k2o = det->P16.k2o;
-  V16.redo_list = det->P16.redo_list + (int64_t)slot * (det->max_batch + 1);
+  V16.redo_list = det->P16.redo_list + (int64_t)slot * (det->max_batch + 1);   // slot < NPART
 }
 
 static rd_status detect_impl(rd_detector* det, const void* d_frames, int64_t pitch, int64_t fstride, int n,
@@ -658,23 +659,24 @@ rd_status rd_detect(rd_detector* det, const void* d_frames, int64_t pitch, int64
   // A large batch runs as two halves on two internal streams (disjoint frame views of the
   // internal buffers), joined back into the caller's stream: each kernel's last partial
   // wave overlaps the other half's kernels.  Per-kernel timing keeps one stream.
-  if (n >= 128 && !det->timing && !getenv("RD_NO_SPLIT")) {
+  int parts = n >= 128 ? 2 : 1;
+  if (const char* env = getenv("RD_SPLIT")) parts = std::max(1, std::min(rd_detector::NPART, atoi(env)));
+  if (det->timing || n < 2 * parts) parts = 1;
+  if (parts > 1) {
     if (!det->s_half[0]) {
-      for (int i = 0; i < 2; ++i) {
+      for (int i = 0; i < rd_detector::NPART; ++i) {
         CK(cudaStreamCreateWithFlags(&det->s_half[i], cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&det->ev_join[i], cudaEventDisableTiming));
       }
       CK(cudaEventCreateWithFlags(&det->ev_fork, cudaEventDisableTiming));
     }
-    const int h = n / 2;
     CK(cudaEventRecord(det->ev_fork, st));
-    for (int i = 0; i < 2; ++i) CK(cudaStreamWaitEvent(det->s_half[i], det->ev_fork, 0));
-    s = detect_impl(det, d_frames, pitch, fstride, h, d_rings, d_counts, det->s_half[0], 0, 0);
-    if (s != RD_OK) return s;
-    s = detect_impl(det, (const char*)d_frames + (size_t)h * fstride, pitch, fstride, n - h,
-                    d_rings + (size_t)h * det->P.ring_cap, d_counts + h, det->s_half[1], h, 1);
-    if (s != RD_OK) return s;
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < parts; ++i) {
+      const int f0 = (int)((int64_t)n * i / parts), f1 = (int)((int64_t)n * (i + 1) / parts);
+      CK(cudaStreamWaitEvent(det->s_half[i], det->ev_fork, 0));
+      s = detect_impl(det, (const char*)d_frames + (size_t)f0 * fstride, pitch, fstride, f1 - f0,
+                      d_rings + (size_t)f0 * det->P.ring_cap, d_counts + f0, det->s_half[i], f0, i);
+      if (s != RD_OK) return s;
       CK(cudaEventRecord(det->ev_join[i], det->s_half[i]));
       CK(cudaStreamWaitEvent(st, det->ev_join[i], 0));
     }
