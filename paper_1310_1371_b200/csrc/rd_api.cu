@@ -78,7 +78,7 @@ struct rd_detector {
   void* d_rings_stage[NSTAGE] = {};
   int* d_counts_stage[NSTAGE] = {};
   cudaStream_t s_comp = nullptr, s_h2d = nullptr, s_d2h = nullptr;
-  cudaStream_t s_comp2 = nullptr;   // chunks alternate between s_comp and s_comp2 (their tails overlap)
+  cudaStream_t s_hc[4] = {};        // host path: chunk k computes on s_hc[k % n_slots] (tails overlap)
   static constexpr int NPART = 4;    // frame-view slots: rd_detect parts / host-path chunks
   cudaStream_t s_half[NPART] = {};   // rd_detect: the parts of a large batch
   cudaEvent_t ev_fork = nullptr, ev_join[NPART] = {};
@@ -540,7 +540,8 @@ rd_status rd_destroy(rd_detector* det) {
   }
   if (det->s_comp) {
     cudaStreamDestroy(det->s_comp);
-    if (det->s_comp2) cudaStreamDestroy(det->s_comp2);
+    for (int i = 1; i < 4; ++i)
+      if (det->s_hc[i]) cudaStreamDestroy(det->s_hc[i]);
     cudaStreamDestroy(det->s_h2d);
     cudaStreamDestroy(det->s_d2h);
     for (int i = 0; i < rd_detector::NSTAGE; ++i) {
@@ -690,7 +691,9 @@ rd_status rd_detect(rd_detector* det, const void* d_frames, int64_t pitch, int64
 static rd_status ensure_host_path(rd_detector* det) {
   if (det->s_comp) return RD_OK;
   // two chunks in flight use disjoint halves of the internal buffers (frame_view)
-  det->n_slots = det->max_batch >= 2 ? 2 : 1;
+  int slots = 2;
+  if (const char* env = getenv("RD_HOST_SLOTS")) slots = std::max(1, std::min(4, atoi(env)));
+  det->n_slots = std::max(1, std::min(slots, det->max_batch));
   const int room = det->max_batch / det->n_slots;
   det->chunk = std::min(room, 48);
   if (const char* env = getenv("RD_HOST_CHUNK")) det->chunk = std::max(1, std::min(room, atoi(env)));
@@ -704,7 +707,8 @@ static rd_status ensure_host_path(rd_detector* det) {
     CK(cudaEventCreateWithFlags(&det->ev_d2h[i], cudaEventDisableTiming));
   }
   CK(cudaStreamCreateWithFlags(&det->s_comp, cudaStreamNonBlocking));
-  CK(cudaStreamCreateWithFlags(&det->s_comp2, cudaStreamNonBlocking));
+  det->s_hc[0] = det->s_comp;
+  for (int i = 1; i < det->n_slots; ++i) CK(cudaStreamCreateWithFlags(&det->s_hc[i], cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&det->s_h2d, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&det->s_d2h, cudaStreamNonBlocking));
   return RD_OK;
@@ -744,8 +748,8 @@ rd_status rd_detect_host(rd_detector* det, const void* h_frames, int64_t pitch, 
     const int f0 = cstart[k], m = cstart[k + 1] - f0;
     // buffer slot and stream b: chunk k overlaps chunk k - 1 (other slot) and follows chunk k - 2
     // on the same stream; stage q holds its frames and rings
-    const int b = det->n_slots == 2 ? (k & 1) : 0, q = k % rd_detector::NSTAGE;
-    cudaStream_t sc = b ? det->s_comp2 : det->s_comp;
+    const int b = k % det->n_slots, q = k % rd_detector::NSTAGE;
+    cudaStream_t sc = det->s_hc[b];
     // H2D of chunk k may overwrite stage q only after the stage's previous chunk finished computing
     if (k >= rd_detector::NSTAGE) CK(cudaStreamWaitEvent(det->s_h2d, det->ev_done[q], 0));
     mark(det->s_h2d);
@@ -778,7 +782,7 @@ rd_status rd_detect_host(rd_detector* det, const void* h_frames, int64_t pitch, 
   }
   CK(cudaStreamSynchronize(det->s_d2h));
   CK(cudaStreamSynchronize(det->s_comp));
-  CK(cudaStreamSynchronize(det->s_comp2));
+  for (int i = 1; i < det->n_slots; ++i) CK(cudaStreamSynchronize(det->s_hc[i]));
   if (trace) {   // per chunk: h2d start/end, compute start/end, d2h end (ms from the first copy)
     for (size_t i = 0; i + 5 <= tev.size(); i += 5) {
       float t[5];
