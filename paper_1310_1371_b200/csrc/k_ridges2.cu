@@ -19,6 +19,7 @@
 // clamped at load time.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "rd_internal.cuh"
 
@@ -300,12 +301,17 @@ static cudaError_t launch_s(const void* frames, int64_t pitch, int64_t fstride, 
   for (int nseg = 1; nseg <= std::min(bin_rows, 8); ++nseg) {
     const int sr = (bin_rows + nseg - 1) / nseg * T1;            // rows per segment
     const int ns = (P.H + sr - 1) / sr;
-    const double ctas = (double)strips * ns * n_frames, waves = ctas / slots;
+    // concurrent parts of a batch share the SMs: each sees its share of the CTA slots
+    const double ctas = (double)strips * ns * n_frames, waves = ctas / (slots / (double)std::max(1, P.parts));
     const double eff = waves / std::ceil(waves) * (double)P.H / (P.H + ns * (3.0 * KS + 6.0));
     if (eff > best + 1e-9) {
       best = eff;
       seg = sr;
     }
+  }
+  if (const char* env = getenv("RD_K1_NSEG")) {   // A/B: a fixed number of row segments
+    const int ns = std::max(1, std::min(bin_rows, atoi(env)));
+    seg = (bin_rows + ns - 1) / ns * T1;
   }
   dim3 grid(strips, (P.H + seg - 1) / seg, n_frames);
   k_ridges2<PixT, KS, RB, EDGE><<<grid, KS_COLS, sm, st>>>((const uint8_t*)frames, pitch, fstride, seg, P);

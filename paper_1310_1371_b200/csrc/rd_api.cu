@@ -592,9 +592,11 @@ static void frame_view(const rd_detector* det, int f0, int slot, Params& V, Para
 }
 
 static rd_status detect_impl(rd_detector* det, const void* d_frames, int64_t pitch, int64_t fstride, int n,
-                             void* d_rings, int* d_counts, cudaStream_t st, int f0 = 0, int slot = 0) {
+                             void* d_rings, int* d_counts, cudaStream_t st, int f0 = 0, int slot = 0,
+                             int parts = 1) {
   Params P, P16;
   frame_view(det, f0, slot, P, P16);
+  P.parts = P16.parts = parts;
   cudaEvent_t* ev = nullptr;
   if (det->timing) {
     size_t need = RD_NEV * (size_t)(det->n_timed + 1);
@@ -676,7 +678,7 @@ rd_status rd_detect(rd_detector* det, const void* d_frames, int64_t pitch, int64
       const int f0 = (int)((int64_t)n * i / parts), f1 = (int)((int64_t)n * (i + 1) / parts);
       CK(cudaStreamWaitEvent(det->s_half[i], det->ev_fork, 0));
       s = detect_impl(det, (const char*)d_frames + (size_t)f0 * fstride, pitch, fstride, f1 - f0,
-                      d_rings + (size_t)f0 * det->P.ring_cap, d_counts + f0, det->s_half[i], f0, i);
+                      d_rings + (size_t)f0 * det->P.ring_cap, d_counts + f0, det->s_half[i], f0, i, parts);
       if (s != RD_OK) return s;
       CK(cudaEventRecord(det->ev_join[i], det->s_half[i]));
       CK(cudaStreamWaitEvent(st, det->ev_join[i], 0));

@@ -67,6 +67,7 @@ struct Params {
   // Hough tiles (K2)
   int k2t;                      // Hough tile width (k2t x k2ty accumulator cells per CTA)
   int k2ty;                     // Hough tile height (the persistent K2 balances the tiling; else = k2t)
+  int parts;                    // concurrent launches sharing the GPU (rd_detect's batch parts)
   int ntx, nty;                 // Hough tiles per frame
   int entry_cap, hot_cap;
   int* ray_count;               // [F][tiles] voting rays routed to each Hough tile (K1.5)
