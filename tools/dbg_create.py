@@ -1,3 +1,4 @@
+"""Create a detector for the dense cfg4 capacities and print rd_create's error, if any (RD_K2_VERBOSE=1 shows the K2 shape)."""
 import os, sys
 sys.path.insert(0, os.getcwd())
 import synth, paper_1310_1371_b200 as rd
