@@ -36,7 +36,8 @@ STATS_DTYPE = np.dtype([("ridges", "i8"), ("votes", "i8"), ("hotspots", "i8"), (
 def lib():
     global _LIB
     if _LIB is None:
-        path = os.path.join(_HERE, "liboracle.so")
+        # ORACLE_LIB_PATH: a mutated build (tools/mutate_oracle.py checks that the pins catch it)
+        path = os.environ.get("ORACLE_LIB_PATH") or os.path.join(_HERE, "liboracle.so")
         if not os.path.exists(path):
             from tools.build import build_oracle
             build_oracle()
