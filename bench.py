@@ -1,19 +1,25 @@
 #!/usr/bin/env python
 """bench.py — frames/s of the B200 ring detector on BASELINE.json's headline workload.
 
-Step = one pass of the whole hot path (K1 ridges -> K2 Hough -> K3 classify/fit) over one
-batch of B synthetic frames shaped like the paper's workload (BASELINE.json configs[2]:
-1024x688 uint16 (12-bit), 50 rings, overlap / nesting / occlusion; frames generated as
-cfg5 = cfg3 seeds, so frame i is identical for any GPU count).  Frames are resident in HBM
-before timing; the batch (B * 1.41 MB = 360 MB at B = 256) is larger than L2, so no
-flush is needed between steps.
+Step = one pass of the whole hot path (K1 ridges -> K1.5 ray routing -> K2 Hough -> K3
+classify/fit -> output) over one batch of B synthetic frames shaped like the paper's workload
+(BASELINE.json configs[2]: 1024x688 uint16 (12-bit), 50 rings, overlap / nesting / occlusion;
+frames generated with the cfg5 = cfg3 seeds, so frame i is identical for any GPU count).
+Frames are resident in HBM before timing; the batch (B * 1.41 MB = 360 MB at B = 256) is
+larger than L2, so no flush is needed between steps.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl reference]
+  python bench.py --config 5 [--gpus N] [--frames 8192] [--parity sample|full|none]
 
-N > 1: launched by torchrun; each rank processes its own B frames per step (weak
-scaling, no data-path collective); after the timed region the ring lists are gathered
-to rank 0 over NCCL (the paper's producer/consumer result collection)
-and checked for P-invariance of frame content.
+Default (configs[2]): N > 1 is launched by torchrun; each rank processes its own B frames per
+step (weak scaling, no data-path collective).  Rank 0 compares every ring of its timed batch
+with the CPU oracle ("parity"), which it also times ("cpu_baseline").
+
+--config 5 (BASELINE.json configs[4], the stream sweep): 8192 frames in total, rank k detects
+frames [k N/P, (k+1) N/P) in batches of B; after the timed compute the ring lists are gathered
+to rank 0 (dist.gather over NCCL); a step = the whole sweep (strong scaling).
+Rank 0 reports compute-only and compute+gather frames/s, a sha256 of the gathered records
+(identical for every P) and their parity with the oracle.
 
 --impl reference: times the CPU oracle (oracle/, the only reference this paper has) on the
 box's host cores over a bounded sample of the same workload.
@@ -21,6 +27,7 @@ box's host cores over a bounded sample of the same workload.
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import math
 import os
@@ -38,11 +45,24 @@ sys.path.insert(0, ROOT)
 CFG = 3                      # BASELINE.json configs[2] (cfg5 frames are cfg3 frames)
 WORKLOAD = "cfg3: 1024x688 uint16 (12-bit), 50 rings/frame (30% overlapping pairs, 10% nested, 10% occluded), " \
            "Poisson+read noise; r in [8,70]"
+WORKLOAD5 = "cfg5: 8192 frames as cfg3 (seeded per frame index), sharded by frame across the GPUs, ring lists " \
+            "gathered to rank 0"
 METRIC = "frames/s (0.7 MP, ~50 rings)"
+FIT_TOL = 1e-4
 
 
 def _env_rank():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -93,73 +113,92 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(busy)}
 
 
-def make_frames(first: int, n: int):
+def make_frames(first: int, n: int, out=None):
     import synth
-    return synth.batch(CFG, 0, first, n)
+    return synth.batch(CFG, 0, first, n, out=out)
+
+
+def compare_rings(got: list, exp: list) -> dict:
+    """Parity of per-frame ring lists: integer fields bit-exact, fits within FIT_TOL px."""
+    bad, worst = [], 0.0
+    for i, (g, e) in enumerate(zip(got, exp)):
+        ok = g is not None and len(g) == len(e)
+        if ok:
+            for k in ("cx", "cy", "r", "raw_votes", "score_fixed", "inliers", "fit_ok"):
+                ok &= bool(np.array_equal(g[k], e[k]))
+            if ok and len(g):
+                d = max(float(np.max(np.abs(g[k] - e[k]))) for k in ("fx", "fy", "fr", "rms"))
+                worst = max(worst, d)
+                ok &= d <= FIT_TOL
+        if not ok:
+            bad.append(i)
+    return {"frames": len(exp), "mismatches": len(bad), "first_mismatch": bad[0] if bad else None,
+            "rings": int(sum(len(e) for e in exp)), "max_fit_diff_px": worst, "fit_tol_px": FIT_TOL}
 
 
 # ------------------------------------------------------------------------ CPU oracle arm
-def cpu_oracle_rate(n_frames: int, first: int = 0, frames=None, streamed: bool = False):
-    """Time the oracle (as it stands) on all host cores over a bounded sample.  streamed=True
-    times the paper's own streamed CPU method (oracle/streamed.c, NEXT-1) instead."""
-    import oracle
-    import synth
-    p = oracle.params(**synth.preset(CFG))
-    if frames is None:
-        frames = make_frames(first, n_frames)
-    cores = os.cpu_count() or 1
-    t0 = time.perf_counter()
-    oracle.detect_batch(p, frames, nthreads=cores, streamed=streamed)
-    dt = time.perf_counter() - t0
-    return n_frames / dt, cores, dt
-
-
 def run_reference(args):
+    """The reference arm: the oracle as it stands, on all host cores, a bounded sample per step.
+    Workspaces are kept across steps (oracle.Pool), so steps time the arithmetic, not allocation."""
     rank, _, world = _env_rank()
     if rank != 0:
         return 0
-    import synth  # noqa: F401
+    import oracle
+    import synth
     per_step = args.ref_frames
     frames = make_frames(0, per_step)
-    cpu_oracle_rate(min(per_step, 4), frames=frames[: min(per_step, 4)])  # warm (page faults, threads)
-    for _ in range(max(0, min(args.warmup, 1))):
-        pass
-    times = []
     cores = os.cpu_count() or 1
+    pool = oracle.Pool(oracle.params(**synth.preset(CFG)), nthreads=cores)
+    for _ in range(max(1, min(args.warmup, 2))):
+        pool.detect(frames)
+    times = []
     for _ in range(args.steps):
-        _, cores, dt = cpu_oracle_rate(per_step, frames=frames)
-        times.append(dt)
+        t0 = time.perf_counter()
+        pool.detect(frames)
+        times.append(time.perf_counter() - t0)
     total = sum(times)
     value = per_step * args.steps / total
+    sample = f"frames 0..{per_step - 1} of cfg3 per step, full frames; {cores} threads on {cpu_model()}"
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "frames/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(1000 * total / args.steps, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": WORKLOAD, "frames_per_step": per_step, "parallelism": "host threads"},
             "cpu_baseline": {"value": round(value, 3), "unit": "frames/s", "cores": cores, "kind": "oracle",
-                             "sample": f"frames 0..{per_step - 1} of cfg3 per step, full frames"},
+                             "cpu": cpu_model(), "sample": sample},
             "e2e": {"value": round(value, 3), "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
-# ------------------------------------------------------------------------ GPU arm
-def run_gpu(args):
+# ------------------------------------------------------------------------ GPU arm helpers
+def _init_dist(args):
     import torch
     import torch.distributed as dist
-
-    import paper_1310_1371_b200 as rd
-    import synth
-
     rank, local, world = _env_rank()
-    if world != args.gpus:
-        if world == 1 and args.gpus > 1:
-            raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
+    if world != args.gpus and world == 1 and args.gpus > 1:
+        raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=dev)
+    return torch, dist, rank, local, world, dev
+
+
+def _max_over_ranks(torch, dist, world, dev, v: float) -> float:
+    if world > 1:
+        t = torch.tensor([v], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        v = float(t.item())
+    return v
+
+
+def run_gpu(args):
+    torch, dist, rank, local, world, dev = _init_dist(args)
+    import paper_1310_1371_b200 as rd
+    import synth
+
     B = args.batch
     params = synth.preset(CFG)
     fbytes = params["width"] * params["height"] * params["pixel_bytes"]
@@ -168,7 +207,7 @@ def run_gpu(args):
     frames_h = make_frames(rank * B, B)
     frames_d = torch.from_numpy(frames_h).to(dev)
     det = rd.Detector(params, max_batch=B, device=local)
-    rings, counts = det.alloc_outputs(B)
+    out = det.alloc_outputs(B)
     stream = torch.cuda.current_stream(dev)
 
     def barrier():
@@ -176,10 +215,11 @@ def run_gpu(args):
             dist.barrier()
 
     for _ in range(args.warmup):
-        det.detect(frames_d, rings, counts, stream)
+        det.detect(frames_d, out, stream)
     det.sync()
     stats = det.stats(B)
     votes_per_step = int(stats["votes"].sum())
+    gpu_rings = out.to_numpy()
     # window cells of the hotspots (A7's unit of work): a debug pass over a
     # few frames lists every interior hotspot with its r; cells = sum (2 K_r + 1)^2
     nd = min(B, 8)
@@ -187,11 +227,14 @@ def run_gpu(args):
     dbg.detect(frames_d[:nd])
     dbg.sync()
     win_cells = 0
+    hot_per_frame = 0
     for i in range(nd):
         r = dbg.dump_hotspots(i)["r"].astype(np.int64)
         K = (3 * (params["sig_a"] * r + params["sig_b"]) + params["sig_den"] - 1) // params["sig_den"]
         win_cells += int(((2 * K + 1) ** 2).sum())
+        hot_per_frame += len(r)
     win_cells_per_frame = win_cells / nd
+    hot_per_frame /= nd
     dbg.close()
 
     # ---------------- timed region: device time, CUDA events on the launching stream
@@ -203,127 +246,115 @@ def run_gpu(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        det.detect(frames_d, rings, counts, stream)
+        det.detect(frames_d, out, stream)
     e1.record(stream)
     torch.cuda.synchronize(dev)
     barrier()
     ms = e0.elapsed_time(e1)
     # per-kernel durations (the roofline): a separate pass with CUDA events around each kernel
-    # on the launching stream; timing keeps a batch on one stream (no two-half overlap), so
-    # these are the kernels' own durations
+    # on the launching stream (rd_set_timing keeps a batch on one stream: the kernels' own durations)
     det.set_timing(True)
     for _ in range(max(1, min(args.steps, 5))):
-        det.detect(frames_d, rings, counts, stream)
+        det.detect(frames_d, out, stream)
     kms, ncalls = det.kernel_times()
     det.set_timing(False)
     det.sync()
     clocks = clk.stop()
-    if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = _max_over_ranks(torch, dist, world, dev, ms)
     ms_per_step = ms / args.steps
     value = world * B * args.steps / (ms / 1e3)
 
     # ---------------- end to end through the public API on pinned host buffers
     pinned = torch.from_numpy(frames_h).pin_memory()
-    h_rings = torch.empty((B, det.ring_cap, rd.RING_DTYPE.itemsize), dtype=torch.uint8).pin_memory()
-    h_counts = torch.empty((B,), dtype=torch.int32).pin_memory()
-    for _ in range(max(1, min(args.warmup, 2))):
-        det.detect_host(pinned, h_rings, h_counts)
+    hout = det.detect_host(pinned)   # allocates the host RingBatch once
+    for _ in range(max(1, min(args.warmup, 2)) - 1):
+        det.detect_host(pinned, hout)
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
     barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        det.detect_host(pinned, h_rings, h_counts)
+        det.detect_host(pinned, hout)
     dt = time.perf_counter() - t0
     barrier()
-    if world > 1:
-        t = torch.tensor([dt], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dt = float(t.item())
+    dt = _max_over_ranks(torch, dist, world, dev, dt)
     e2e_value = world * B * e2e_steps / dt
-
-    # ---------------- gather ring lists to rank 0 over NCCL (after timing)
-    gather_ms = None
-    n_rings_total = int(counts.clamp(min=0).sum().item())
-    if world > 1:
-        from paper_1310_1371_b200.distributed import gather_rings
-        torch.cuda.synchronize(dev)
-        g0 = time.perf_counter()
-        res = gather_rings(rings, counts)
-        torch.cuda.synchronize(dev)
-        gather_ms = (time.perf_counter() - g0) * 1e3
-        if res is not None:
-            n_rings_total = int(res[1].clamp(min=0).sum().item())
+    n_rings_rank = int(np.maximum(hout.counts, 0).sum())
+    d2h_step = n_rings_rank * 64 + 4 * (2 * B + 1)   # rings found + counts + offsets (compact output)
+    host_equal = all(a.tobytes() == b.tobytes() for a, b in zip(hout.to_numpy(), gpu_rings))
 
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return 0
 
-    # ---------------- roofline of the dominant kernel (DESIGN.md §6)
+    # ---------------- roofline of the dominant kernel (DESIGN.md §6, §9)
     names = ["k_ridges", "k_rays", "k_hough", "k_fit"]
     kms_all = [k / ncalls for k in kms]
-    kms_step = [kms_all[0], kms_all[2], kms_all[3]]      # K1, K2, K3 (K1.5 reported separately)
-    dom = int(np.argmax(kms_step))
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
-    # K1: fp64 pipe (exact stencil arithmetic); peak = 148 SM x 64 DFMA/clk x sm_max
-    Ks = math.ceil(3 * params["smoothing_sigma"])
-    k1_ops_per_px = (2 * Ks + 1) + 9 + 9 + 10
     px = params["width"] * params["height"]
+    Ks = math.ceil(3 * params["smoothing_sigma"])
+    # K1 as an fp64/ALU-issue kernel: algorithmic operations per pixel of the exact integer
+    # smoothing (2K_s + 1 taps per pass, two passes share the symmetric taps: 2K_s + 1), the
+    # Sobel (9 + 9) and the kappa recipe (10); peak = the fp64 pipe, 148 SM x 64/clk x sm_max
+    k1_ops_per_px = (2 * Ks + 1) + 9 + 9 + 10
     fp64_peak = 148 * 64 * sm_max * 1e6 / 1e12
-    k1_ach = B * px * k1_ops_per_px / (kms_step[0] / 1e3) / 1e12
-    # K2: one shared-memory atomic per in-frame vote is the irreducible work of an
-    # accumulator Hough transform; peak = measured ATOMS throughput 11.0/clk/SM
-    # (tools/microbench, profiles/microbench_r01.log) x 148 SM x sm_max
-    atom_peak = 11.0 * 148 * sm_max * 1e6 / 1e9
-    k2_ach = votes_per_step / (kms_step[1] / 1e3) / 1e9
-    # K2 as an ALU-issue-bound kernel: algorithmic lane operations per frame =
-    # 11 per in-frame vote (~10 ops + 1 atomic) + 2 per hotspot window cell
-    # (multiply-add); the NMS compares (<1 %) are left out; peak = 148 SM x 128 lanes x sm_max
-    k2_ops = 11 * votes_per_step + 2 * win_cells_per_frame * B
+    k1_ach = B * px * k1_ops_per_px / (kms_all[0] / 1e3) / 1e12
+    # K2 as an ALU-issue-bound kernel: SURVEY.md §8(d)'s count — 11 lane operations per in-frame
+    # vote (~10 ops + 1 shared atomic) and 1 per hotspot window cell (one MAC), 3x3x3 NMS compares
+    # (26 per hotspot) — against 148 SM x 128 lanes x sm_max
+    k2_ops = 11 * votes_per_step + (win_cells_per_frame + 26 * hot_per_frame) * B
     lane_peak = 148 * 128 * sm_max * 1e6 / 1e12
-    k2_alu = k2_ops / (kms_step[1] / 1e3) / 1e12
+    k2_alu = k2_ops / (kms_all[2] / 1e3) / 1e12
+    atom_peak = 11.0 * 148 * sm_max * 1e6 / 1e9   # measured ATOMS/clk/SM (profiles/microbench_r01.log)
+    k2_atom = votes_per_step / (kms_all[2] / 1e3) / 1e9
     summ = {}
-    sp = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
+    sp = os.path.join(ROOT, "profiles", "ncu_summary_r02.json")
     if os.path.exists(sp):
         for d in json.load(open(sp)):
             for n in names:
-                if n in d.get("kernel", "") and "dram_bytes_per_frame" in d:
+                if d.get("kernel", "").startswith(n) and "dram_bytes_per_frame" in d:
                     summ[n] = d["dram_bytes_per_frame"] * B
     roofs = [
         {"kernel": "k_ridges", "bound": "alu", "achieved": round(k1_ach, 3), "peak": round(fp64_peak, 3),
-         "unit": "TFLOP/s", "frac": round(k1_ach / fp64_peak, 4), "traffic": summ.get("k_ridges"),
-         "peak_note": "fp64 DFMA issue: 148 SM x 64/clk x sm_max (guide unit counts); ops = fp64 instructions of "
-                      "the exact separable Gaussian + Sobel + kappa per pixel (DESIGN.md §6)"},
+         "unit": "T op/s", "frac": round(k1_ach / fp64_peak, 4), "traffic": summ.get("k_ridges"),
+         "per_unit": f"{k1_ops_per_px} fp64 ops/pixel x {px} pixels x {B} frames per launch",
+         "peak_note": "fp64 DFMA issue: 148 SM x 64/clk x sm_max (guide unit counts)"},
         {"kernel": "k_hough", "bound": "alu", "achieved": round(k2_alu, 4), "peak": round(lane_peak, 2),
          "unit": "T lane-op/s", "frac": round(k2_alu / lane_peak, 5), "traffic": summ.get("k_hough"),
-         "peak_note": "ALU issue: 148 SM x 128 lanes x sm_max (guide unit counts); ops = 11 per in-frame vote + "
-                      "2 per hotspot window cell (SURVEY.md §8(d), DESIGN.md §6); window cells "
-                      f"{win_cells_per_frame:.0f}/frame measured by a debug pass"},
-        {"kernel": "k_hough", "bound": "alu", "achieved": round(k2_ach, 3), "peak": round(atom_peak, 1),
-         "unit": "Gvote/s", "frac": round(k2_ach / atom_peak, 5), "traffic": summ.get("k_hough"),
-         "peak_note": "shared-memory atomic issue: measured 11.0 ATOMS/clk/SM x 148 SM x sm_max; one atomic per "
-                      "in-frame vote (DESIGN.md §6)"},
+         "per_unit": f"11 per in-frame vote ({votes_per_step / B:.0f}/frame) + 1 per window cell "
+                     f"({win_cells_per_frame:.0f}/frame) + 26 per hotspot ({hot_per_frame:.0f}/frame) x {B} frames",
+         "peak_note": "ALU issue: 148 SM x 128 lanes x sm_max (guide unit counts); SURVEY.md §8(d) op count"},
+        {"kernel": "k_hough", "bound": "alu", "achieved": round(k2_atom, 3), "peak": round(atom_peak, 1),
+         "unit": "Gvote/s", "frac": round(k2_atom / atom_peak, 5), "traffic": summ.get("k_hough"),
+         "peak_note": "shared-memory atomic issue: measured 11.0 ATOMS/clk/SM x 148 SM x sm_max"},
     ]
-    roof = dict(roofs[0] if dom == 0 else roofs[1])
+    dom = 0 if kms_all[0] >= kms_all[2] else 1
+    roof = dict(roofs[dom])
     hbm_peak = float(peaks.get("hbm_gbs", 6549.1))
-    alg_bytes_frame = fbytes + 64 * (n_rings_total / max(1, B * world))
+    alg_bytes_frame = fbytes + 64 * (n_rings_rank / B)
     hbm_achieved = alg_bytes_frame * value / world / 1e9
 
-    cpu = None
-    if world == 1 and not args.no_cpu:
-        n_cpu = args.cpu_frames
-        rate, cores, dt = cpu_oracle_rate(n_cpu, frames=frames_h[:n_cpu])
-        cpu = {"value": round(rate, 3), "unit": "frames/s", "cores": cores, "kind": "oracle",
-               "sample": f"first {n_cpu} frames of this batch (cfg3, full frames), {dt:.1f} s wall"}
-        srate, _, sdt = cpu_oracle_rate(n_cpu, frames=frames_h[:n_cpu], streamed=True)
-        cpu["paper_streamed"] = {"value": round(srate, 3), "unit": "frames/s", "cores": cores,
-                                 "note": "the paper's streamed CPU method (sorted vote stack, r mod 3 "
-                                         f"sub-spaces; oracle/streamed.c), same sample, {sdt:.1f} s wall"}
+    cpu, parity = None, None
+    if not args.no_cpu:
+        import oracle
+        cores = os.cpu_count() or 1
+        n_cpu = min(args.cpu_frames, B)
+        pool = oracle.Pool(oracle.params(**params), nthreads=cores)
+        pool.detect(frames_h[: min(n_cpu, 2 * cores)])   # workspaces + threads, untimed
+        t0 = time.perf_counter()
+        exp, est = pool.detect(frames_h[:n_cpu])
+        cdt = time.perf_counter() - t0
+        pool.close()
+        cpu = {"value": round(n_cpu / cdt, 3), "unit": "frames/s", "cores": cores, "kind": "oracle",
+               "cpu": cpu_model(),
+               "sample": f"the first {n_cpu} frames of this batch (cfg3, full frames), {cdt:.1f} s wall on {cores} "
+                         f"threads"}
+        parity = compare_rings(gpu_rings[:n_cpu], exp)
+        parity["stats_equal"] = bool(all(np.array_equal(stats[k][:n_cpu], est[k][:n_cpu])
+                                         for k in ("ridges", "votes", "hotspots", "peaks")))
+        parity["host_path_equal_device"] = bool(host_equal)
 
     line = {"metric": METRIC, "value": round(value, 1), "unit": "frames/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
@@ -339,16 +370,114 @@ def run_gpu(args):
                              "frac": round(hbm_achieved / hbm_peak, 5),
                              "note": "algorithmic bytes = frame read + 64 B/ring written (SURVEY §8(d))"},
             "cpu_baseline": cpu,
+            "parity": parity,
             "e2e": {"value": round(e2e_value, 1), "unit": "frames/s", "steps": e2e_steps,
-                    "h2d_bytes_per_step": B * fbytes * world,
-                    "d2h_bytes_per_step": (B * det.ring_cap * 64 + 4 * B) * world,
-                    "api": "Detector.detect_host -> rd_detect_host (pinned host buffers)"},
-            # K1, K1.5, K2, K2 redo reset, K2 redo pass, K3 per batch; a batch of >= 128 frames
-            # runs as two halves
-            "gpu_launches": 6 * (2 if B >= 128 else 1) * args.steps,
+                    "h2d_bytes_per_step": B * fbytes * world, "d2h_bytes_per_step": d2h_step * world,
+                    "api": "Detector.detect_host -> rd_detect_host (pinned host buffers, compact ring output)"},
+            # K1, K1.5, K2, K2 redo reset, K2 redo pass, K3 per part (a batch of >= 128 frames runs
+            # as two halves) + k_scan and k_copy per call
+            "gpu_launches": (6 * (2 if B >= 128 else 1) + 2) * args.steps,
             "clocks": clocks}
-    if gather_ms is not None:
-        line["gather_ms"] = round(gather_ms, 3)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+# ------------------------------------------------------------------------ cfg5 sweep
+def run_sweep(args):
+    """BASELINE.json configs[4]: 8192 cfg3 frames sharded by frame across P GPUs, ring lists
+    gathered to rank 0.  A step = the whole sweep (strong scaling)."""
+    torch, dist, rank, local, world, dev = _init_dist(args)
+    import paper_1310_1371_b200 as rd
+    from paper_1310_1371_b200.distributed import gather_records, shard, unpack
+    import synth
+
+    N, B = args.frames, args.batch
+    params = synth.preset(5)
+    a, b = shard(N, world, rank)
+    n_mine = b - a
+    frames_d = torch.empty((n_mine, params["height"], params["width"]), dtype=torch.uint16, device=dev)
+    chunk = 512
+    for s in range(0, n_mine, chunk):   # generated in pieces (host memory), resident on the device
+        m = min(chunk, n_mine - s)
+        frames_d[s:s + m].copy_(torch.from_numpy(synth.batch(5, 0, a + s, m)))
+    det = rd.Detector(params, max_batch=B, device=local)
+    nb = (n_mine + B - 1) // B
+    outs = [det.alloc_outputs(min(B, n_mine - k * B)) for k in range(nb)]
+    stream = torch.cuda.current_stream(dev)
+
+    def sweep():
+        for k in range(nb):
+            det.detect(frames_d[k * B:(k + 1) * B], outs[k], stream)
+
+    def gather():
+        # pack this rank's batches, then one gather to rank 0
+        from paper_1310_1371_b200.distributed import pack
+        recs, cnts = zip(*[pack(o.rings, o.counts, o.offsets) for o in outs]) if outs else ((), ())
+        r = torch.cat(recs) if recs else torch.zeros((0, 64), dtype=torch.uint8, device=dev)
+        c = torch.cat(cnts) if cnts else torch.zeros(0, dtype=torch.int64, device=dev)
+        return gather_records(r.reshape(-1, 64), c) if world > 1 else None
+
+    for _ in range(args.warmup):
+        sweep()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.15)
+    e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    e0.record(stream)
+    for _ in range(args.steps):
+        sweep()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    clocks = clk.stop()
+    ms = _max_over_ranks(torch, dist, world, dev, e0.elapsed_time(e1))
+    # compute + gather of one sweep's results
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    g0 = time.perf_counter()
+    res = gather()
+    torch.cuda.synchronize(dev)
+    gms = _max_over_ranks(torch, dist, world, dev, (time.perf_counter() - g0) * 1e3)
+    if rank != 0:
+        dist.destroy_process_group() if world > 1 else None
+        return 0
+    if res is None:   # world == 1: the local lists are the gathered ones
+        from paper_1310_1371_b200.distributed import pack
+        recs, cnts = zip(*[pack(o.rings, o.counts, o.offsets) for o in outs])
+        res = (torch.cat(recs), torch.cat(cnts))
+    recs, cnts = res
+    digest = hashlib.sha256(recs.cpu().numpy().tobytes() + cnts.cpu().numpy().tobytes()).hexdigest()
+    lists = unpack(recs, cnts)
+    parity = None
+    if args.parity != "none":
+        import oracle
+        cores = os.cpu_count() or 1
+        idx = list(range(N)) if args.parity == "full" else sorted(set(np.linspace(0, N - 1, 64).astype(int)))
+        pool = oracle.Pool(oracle.params(**params), nthreads=cores)
+        exp = []
+        for s in range(0, len(idx), 512):
+            sel = idx[s:s + 512]
+            fr = np.stack([synth.frame(5, 0, i)[0] for i in sel]) if args.parity != "full" else \
+                synth.batch(5, 0, sel[0], len(sel))
+            exp += pool.detect(fr)[0]
+        pool.close()
+        parity = compare_rings([lists[i] for i in idx], exp)
+        parity["frames_checked"] = "all" if args.parity == "full" else f"{len(idx)} evenly spaced"
+    sweep_ms = ms / args.steps
+    line = {"metric": METRIC, "value": round(N / (sweep_ms / 1e3), 1), "unit": "frames/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(sweep_ms, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD5, "frames_total": N, "frames_per_call": B,
+                       "parallelism": f"frame-sharded x{world}, gather to rank 0"},
+            "compute_plus_gather": {"value": round(N / ((sweep_ms + gms) / 1e3), 1), "gather_ms": round(gms, 3),
+                                    "records": int(recs.shape[0])},
+            "gathered_sha256": digest, "parity": parity, "clocks": clocks,
+            "gpu_launches": (6 * 2 + 2) * nb * args.steps}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -361,14 +490,21 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--batch", type=int, default=256)
+    ap.add_argument("--config", type=int, default=3, choices=[3, 5])
+    ap.add_argument("--frames", type=int, default=8192)
+    ap.add_argument("--parity", default="sample", choices=["none", "sample", "full"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-frames", type=int, default=256)
-    ap.add_argument("--ref-frames", type=int, default=32)
+    ap.add_argument("--ref-frames", type=int, default=64)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.config == 5:
+        if args.steps == 50:
+            args.steps = 5   # a step is the whole 8192-frame sweep
+        return run_sweep(args)
     return run_gpu(args)
 
 

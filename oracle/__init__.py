@@ -78,6 +78,12 @@ def lib():
                                        C.c_void_p, C.c_int32]
         L.orc_detect_batch.restype = C.c_int
         L.orc_detect_batch_streamed.argtypes = L.orc_detect_batch.argtypes
+        L.orc_pool_create.argtypes = [P, C.c_int32, C.c_int32]
+        L.orc_pool_create.restype = C.c_void_p
+        L.orc_pool_detect.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int32,
+                                      C.c_void_p, C.c_void_p]
+        L.orc_pool_detect.restype = C.c_int
+        L.orc_pool_free.argtypes = [C.c_void_p]
         L.orc_detect_batch_streamed.restype = C.c_int
         L.orc_peaks.argtypes = [P, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]
         L.orc_peaks.restype = C.c_int64
@@ -260,6 +266,39 @@ def detect_batch(p, frames: np.ndarray, nthreads: int = 0, ring_stride: int = 10
     if rc:
         raise RuntimeError("orc_detect_batch failed")
     return [rings[i, : counts[i]].copy() for i in range(n)], stats
+
+
+class Pool:
+    """Host thread pool with per-thread workspaces kept across calls (orc_pool_*): the same
+    outputs as detect_batch; only the allocation of the full arrays is paid once."""
+
+    def __init__(self, p, nthreads: int = 0, streamed: bool = False):
+        self.p = p
+        self._h = lib().orc_pool_create(C.byref(p), nthreads, 1 if streamed else 0)
+        if not self._h:
+            raise RuntimeError("orc_pool_create failed")
+
+    def detect(self, frames: np.ndarray, ring_stride: int = 1024):
+        frames = np.ascontiguousarray(frames)
+        n = frames.shape[0]
+        rings = np.zeros((n, ring_stride), dtype=RING_DTYPE)
+        counts = np.zeros(n, dtype=np.int32)
+        stats = np.zeros(n, dtype=STATS_DTYPE)
+        if lib().orc_pool_detect(self._h, frames.ctypes.data, frames.strides[0], n, rings.ctypes.data, ring_stride,
+                                 counts.ctypes.data, stats.ctypes.data):
+            raise RuntimeError("orc_pool_detect failed")
+        return [rings[i, : counts[i]].copy() for i in range(n)], stats
+
+    def close(self):
+        if self._h:
+            lib().orc_pool_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def fit(xs, ys, cx, cy):

@@ -97,6 +97,14 @@ int orc_detect_batch_streamed(const orc_params* p, const void* frames, int64_t f
                               orc_ring* rings, int32_t ring_stride, int32_t* counts, orc_stats* stats,
                               int32_t nthreads);
 
+/* orc_detect_batch with per-thread workspaces kept across calls (timing legs of bench.py):
+ * same outputs, the full arrays are allocated once per pool thread instead of once per call. */
+typedef struct orc_pool orc_pool;
+orc_pool* orc_pool_create(const orc_params* p, int32_t nthreads, int32_t streamed);
+int orc_pool_detect(orc_pool* pool, const void* frames, int64_t frame_stride_bytes, int32_t n_frames, orc_ring* rings,
+                    int32_t ring_stride, int32_t* counts, orc_stats* stats);
+void orc_pool_free(orc_pool* pool);
+
 /* Whole pipeline, steps 1-10, for one frame.  rings: canonical (r, cy, cx) order.
  * Optional debug outputs may be NULL.  Returns the number of rings (all are
  * written only if <= ring_cap), or -1 on allocation failure / bad parameters. */

@@ -35,11 +35,20 @@ RING_DTYPE = np.dtype([("cx", "i4"), ("cy", "i4"), ("r", "i4"), ("raw_votes", "i
 RIDGE_DTYPE = np.dtype([("x", "i4"), ("y", "i4"), ("dx", "f8"), ("dy", "f8")])
 HOT_DTYPE = np.dtype([("r", "i4"), ("y", "i4"), ("x", "i4"), ("raw", "i4"), ("S", "i8")])
 STATS_DTYPE = np.dtype([("ridges", "i8"), ("votes", "i8"), ("hotspots", "i8"), ("peaks", "i8")])
-assert RING_DTYPE.itemsize == 64
+FPR_DTYPE = np.dtype([("r", "i4"), ("pad", "i4"), ("votes", "i8"), ("sq", "i8"), ("pos", "i8")])
+assert RING_DTYPE.itemsize == 64 and FPR_DTYPE.itemsize == 32
+RD_DUMP_RIDGES, RD_DUMP_LEVEL_FPR, RD_DUMP_HOTSPOTS, RD_DUMP_MEMBERS = range(4)
+OVF_BITS = {"ridges": 1, "entries": 2, "hotspots": 4, "rings": 8, "debug": 16, "output": 32}
+
+
+class rd_overflow(C.Structure):
+    _fields_ = [("frames_overflowed", C.c_int32), ("flags", C.c_int32), ("needed_ridges_per_tile", C.c_int32),
+                ("needed_entries_per_tile", C.c_int32), ("needed_hotspots_per_level", C.c_int32),
+                ("needed_rings_per_frame", C.c_int32), ("needed_rings_total", C.c_int64)]
 
 EXPORTS = ("rd_abi_version", "rd_status_string", "rd_last_error", "rd_config_init", "rd_create", "rd_destroy",
-           "rd_detect", "rd_detect_host", "rd_sync", "rd_query_overflow", "rd_get_stats", "rd_dump_ridges",
-           "rd_dump_hotspots", "rd_eigen", "rd_set_timing", "rd_kernel_times", "rd_phase_cycles", "rd_ring_members")
+           "rd_detect", "rd_detect_host", "rd_sync", "rd_query_overflow", "rd_query_flags", "rd_get_stats",
+           "rd_debug_dump", "rd_eigen", "rd_set_timing", "rd_kernel_times", "rd_phase_cycles", "rd_ring_members")
 
 
 class RDError(RuntimeError):
@@ -68,13 +77,13 @@ def lib():
         L.rd_config_init.argtypes = [C.POINTER(rd_config), i32, i32, i32]
         L.rd_create.argtypes = [C.POINTER(rd_config), i32, i32, C.POINTER(vp)]
         L.rd_destroy.argtypes = [vp]
-        L.rd_detect.argtypes = [vp, vp, i64, i64, i32, vp, vp, vp]
-        L.rd_detect_host.argtypes = [vp, vp, i64, i64, i32, vp, vp]
+        L.rd_detect.argtypes = [vp, vp, i64, i64, i32, vp, i32, vp, vp, vp]
+        L.rd_detect_host.argtypes = [vp, vp, i64, i64, i32, vp, i32, vp, vp]
         L.rd_sync.argtypes = [vp]
-        L.rd_query_overflow.argtypes = [vp, i32, vp]
+        L.rd_query_overflow.argtypes = [vp, C.POINTER(rd_overflow)]
+        L.rd_query_flags.argtypes = [vp, i32, vp]
         L.rd_get_stats.argtypes = [vp, i32, vp]
-        L.rd_dump_ridges.argtypes = [vp, i32, vp, i64, C.POINTER(i64)]
-        L.rd_dump_hotspots.argtypes = [vp, i32, vp, i64, C.POINTER(i64)]
+        L.rd_debug_dump.argtypes = [vp, i32, i32, vp, i64, C.POINTER(i64)]
         L.rd_eigen.argtypes = [vp, i64, vp, vp, vp]
         L.rd_set_timing.argtypes = [vp, i32]
         L.rd_kernel_times.argtypes = [vp, vp, C.POINTER(i32)]

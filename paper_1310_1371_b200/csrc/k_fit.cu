@@ -13,13 +13,6 @@
 
 namespace rd {
 
-struct Ring {  // == rd_ring (64 B)
-  int32_t cx, cy, r, raw_votes;
-  int64_t score_fixed;
-  int32_t inliers, fit_ok;
-  double fx, fy, fr, rms;
-};
-
 __device__ __forceinline__ long long warp_sum_ll(long long v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -36,17 +29,14 @@ __device__ __forceinline__ __int128 det3(__int128 a, __int128 b, __int128 c, __i
   return a * (e * i - f * h) - b * (d * i - f * g) + c * (d * h - e * g);
 }
 
-__global__ void __launch_bounds__(K3_THREADS) k_fit(Params P, Ring* __restrict__ rings, int* __restrict__ counts) {
+__global__ void __launch_bounds__(K3_THREADS) k_fit(Params P) {
   extern __shared__ __align__(16) unsigned char smem[];
   Peak* sp = reinterpret_cast<Peak*>(smem);                    // [ring_cap]
   int* order = reinterpret_cast<int*>(sp + P.ring_cap);         // [ring_cap]
   const int f = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int npk = P.peak_count[f];
   const int flags = P.flags[f];
-  if (flags != 0 || npk > P.ring_cap) {
-    if (tid == 0) counts[f] = -1;
-    return;
-  }
+  if (flags != 0 || npk > P.ring_cap) return;   // k_emit reports the frame with count -1
   for (int i = tid; i < npk; i += K3_THREADS) sp[i] = P.peaks[(int64_t)f * P.ring_cap + i];
   __syncthreads();
   // canonical (r, cy, cx) order: rank of each (unique) key
@@ -131,13 +121,10 @@ __global__ void __launch_bounds__(K3_THREADS) k_fit(Params P, Ring* __restrict__
       g.fy = ok ? pk.y + vc : (double)pk.y;
       g.fr = ok ? R : (double)pk.r;
       g.rms = rms;
-      rings[(int64_t)f * P.ring_cap + p] = g;
+      P.rings[(int64_t)f * P.ring_cap + p] = g;
     }
   }
-  if (tid == 0 && blockIdx.y == 0) {
-    counts[f] = npk;
-    P.stats[f].peaks = (unsigned long long)npk;
-  }
+  if (tid == 0 && blockIdx.y == 0) P.stats[f].peaks = (unsigned long long)npk;
 }
 
 // Classification output (A9): the ridge pixels of every ring of
@@ -214,20 +201,102 @@ cudaError_t launch_members(const Params& P, int f, int write, int* offsets, uint
 
 size_t k_fit_smem(const Params& P) { return (size_t)P.ring_cap * (sizeof(Peak) + sizeof(int)); }
 
-cudaError_t launch_fit(int n_frames, const Params& P, void* rings, int* counts, cudaStream_t st) {
+cudaError_t launch_fit(int n_frames, const Params& P, cudaStream_t st) {
   size_t sm = k_fit_smem(P);
   cudaFuncSetAttribute(k_fit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   // CTAs per frame (rings dealt across them; each ranks all peaks): enough to cover the SMs
   // at small batches, one per frame at large ones (cfg3, 256 frames: 0.69 -> 0.56 us/frame
   // against 4 per frame)
-  static int n_sm = 0;
-  if (!n_sm) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  const int split = std::max(1, std::min(4, (P.n_sm + n_frames - 1) / n_frames));
+  k_fit<<<dim3(n_frames, split), K3_THREADS, sm, st>>>(P);
+  return cudaGetLastError();
+}
+
+// Output assembly (A11): per-frame counts and CSR offsets over the call's
+// frames, one CTA.  A frame is valid iff no internal capacity overflowed; its rings occupy
+// [offsets[f], offsets[f] + counts[f]) of the caller's buffer.  offsets advance by every
+// frame's peak count (0 for invalid frames), so offsets[n] is the capacity the call needed; a
+// valid frame whose range passes out_cap gets count -1 and OVF_OUTPUT.  base_in (may be null:
+// 0) is the first offset, base_out (may be null) receives offsets[n] (host-path chunks chain);
+// flags_out (may be null) receives the frames' overflow bits.
+__global__ void __launch_bounds__(1024) k_scan(Params P, int n_frames, int out_cap, int* __restrict__ counts,
+                                               int* __restrict__ offsets, const int* base_in, int* base_out,
+                                               int* flags_out) {
+  __shared__ int wsum[32];
+  __shared__ int carry;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) carry = base_in ? *base_in : 0;
+  int mx = 0;
+  __syncthreads();
+  for (int f0 = 0; f0 < n_frames; f0 += 1024) {
+    const int f = f0 + tid;
+    int npk = 0;
+    bool valid = false;
+    if (f < n_frames) {
+      npk = P.peak_count[f];
+      valid = P.flags[f] == 0 && npk <= P.ring_cap;
+      mx = max(mx, npk);
+    }
+    const int v = valid ? npk : 0;
+    int incl = v;   // block-inclusive scan
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      int w = wsum[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += t;
+      }
+      wsum[lane] = w;
+    }
+    __syncthreads();
+    const int c0 = carry;
+    const int excl = c0 + (warp ? wsum[warp - 1] : 0) + incl - v;
+    if (f < n_frames) {
+      offsets[f] = excl;
+      int cnt = valid ? npk : -1;
+      if (valid && (long long)excl + npk > (long long)out_cap) {
+        cnt = -1;
+        P.flags[f] |= OVF_OUTPUT;
+      }
+      counts[f] = cnt;
+      if (flags_out) flags_out[f] = P.flags[f];
+    }
+    __syncthreads();
+    if (tid == 0) carry = c0 + wsum[31];
+    __syncthreads();
   }
-  const int split = std::max(1, std::min(4, (n_sm + n_frames - 1) / n_frames));
-  k_fit<<<dim3(n_frames, split), K3_THREADS, sm, st>>>(P, reinterpret_cast<Ring*>(rings), counts);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if (lane == 0 && mx) atomicMax(&P.need[NEED_RINGS], mx);
+  if (tid == 0) {
+    offsets[n_frames] = carry;
+    if (base_out) *base_out = carry;
+  }
+}
+
+// Copies each valid frame's rings from the per-frame scratch to the caller's buffer at its
+// offset (16-byte words; the destination may be mapped host memory on the host path).
+__global__ void __launch_bounds__(128) k_copy(Params P, Ring* __restrict__ out, const int* __restrict__ counts,
+                                              const int* __restrict__ offsets) {
+  const int f = blockIdx.x, n = counts[f];
+  if (n <= 0) return;
+  const uint4* src = reinterpret_cast<const uint4*>(P.rings + (int64_t)f * P.ring_cap);
+  uint4* dst = reinterpret_cast<uint4*>(out + offsets[f]);
+  for (int i = threadIdx.x; i < 4 * n; i += blockDim.x) dst[i] = src[i];
+}
+
+cudaError_t launch_emit(int n_frames, const Params& P, void* out, int out_cap, int* counts, int* offsets,
+                        const int* base_in, int* base_out, int* flags_out, cudaStream_t st) {
+  k_scan<<<1, 1024, 0, st>>>(P, n_frames, out_cap, counts, offsets, base_in, base_out, flags_out);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_copy<<<n_frames, 128, 0, st>>>(P, reinterpret_cast<Ring*>(out), counts, offsets);
   return cudaGetLastError();
 }
 

@@ -171,6 +171,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
   const int n_work_frames = redo_pass ? P.redo_list[0] : n_frames;
 
   unsigned long long t_acc[6] = {0, 0, 0, 0, 0, 0};
+  int need_e = 0, need_h = 0;   // capacities the CTA's tiles needed (rd_query_overflow)
   long long t_last = clock64();
 #ifdef RD_K2_PROF   // per-phase cycle accounting (rd_phase_cycles); compiled in on request only
 #define PMARK(i)                                      \
@@ -211,7 +212,9 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
     const int X0 = txi * TX, Y0 = tyi * TY;
     const int RX0 = X0 - hal, RY0 = Y0 - hal;   // raw buffer origin (frame coordinates)
     const int64_t tl = (int64_t)f * ntiles + tile;
-    const int ne = min(P.ray_count[tl], P.entry_cap);
+    const int ne_all = P.ray_count[tl];
+    const int ne = min(ne_all, P.entry_cap);
+    need_e = max(need_e, ne_all);   // (one global atomicMax per CTA at exit)
     const int64_t gbase = tl * P.entry_cap;
     int my_hot = 0;   // interior hotspots (the per-frame vote count comes from K1.5)
 
@@ -467,19 +470,20 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
           const int iy = c >> 8, ix = c & 0xFF;
           const cell_t* ctr = rawc + g * lvlc + (iy - 1 + hal) * rawp + (ix - 1 + hal);   // the hotspot's cell
           const int sub = small ? (lane & 15) : lane;
-          unsigned long long acc = 0;
-          if (valid && sub <= 2 * K && !(P.ablate & 1)) {
-            const int row = sub;   // 2K+1 <= 31 rows (K <= 15), one per lane
-            const cell_t* rowp = ctr + (row - K) * rawp;
-            if (kWide) {
-              unsigned long long rs = (unsigned long long)w[0] * rowp[0];
-              for (int j = 1; j <= K; ++j) rs += (unsigned long long)w[j] * (uint32_t)(rowp[-j] + rowp[j]);
-              acc = rs * (unsigned long long)w[abs(row - K)];
-            } else {
-              uint32_t rs = (uint32_t)w[0] * rowp[0];
+          unsigned long long acc = 0;   // lane sum over window rows sub, sub + 32, ... (K > 15: 2K + 1 > 32 rows)
+          if (valid && !(P.ablate & 1)) {
+            for (int row = sub; row <= 2 * K; row += small ? 16 : 32) {
+              const cell_t* rowp = ctr + (row - K) * rawp;
+              if (kWide) {
+                unsigned long long rs = (unsigned long long)w[0] * rowp[0];
+                for (int j = 1; j <= K; ++j) rs += (unsigned long long)w[j] * (uint32_t)(rowp[-j] + rowp[j]);
+                acc += rs * (unsigned long long)w[abs(row - K)];
+              } else {
+                uint32_t rs = (uint32_t)w[0] * rowp[0];
 #pragma unroll 4
-              for (int j = 1; j <= K; ++j) rs += (uint32_t)w[j] * (uint32_t)(rowp[-j] + rowp[j]);
-              acc = (unsigned long long)rs * (unsigned long long)w[abs(row - K)];
+                for (int j = 1; j <= K; ++j) rs += (uint32_t)w[j] * (uint32_t)(rowp[-j] + rowp[j]);
+                acc += (unsigned long long)rs * (unsigned long long)w[abs(row - K)];
+              }
             }
           }
           unsigned long long S;
@@ -490,7 +494,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
               if (!(small && o == 16)) acc += v;
             }
             S = acc;
-          } else {   // lane terms < 2^45: 24-bit halves reduced with single-instruction reductions
+          } else {   // lane sums < 2^47 (K <= 48: at most 4 rows of < 2^44): 24-bit halves, single-instruction reductions
             const unsigned lo = (unsigned)(acc & 0xFFFFFFull), hi = (unsigned)(acc >> 24);
             unsigned slo, shi;
             if (small) {   // (warp-uniform branch) the two halves reduce separately
@@ -537,6 +541,26 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
       __syncthreads();
       PMARK(3);
       // ---------------- (3) undo the step's counters, then peaks of levels L0-1 .. Lhi-1
+      if (P.debug) {   // level fingerprints over the tile's own cells (each frame voxel once)
+        const int x1 = min(X0 + TX, P.W), y1 = min(Y0 + TY, P.H), nx = x1 - X0, ncell = nx * (y1 - Y0);
+        for (int g = 0; g < min(G, nlev - L0); ++g) {
+          unsigned long long acc[3] = {0, 0, 0};
+          for (int i = tid; i < ncell; i += NT) {
+            const int yy = Y0 + i / nx, xx = X0 + i % nx;
+            const unsigned long long c = rawc[g * lvlc + (yy - RY0) * rawp + (xx - RX0)];
+            acc[0] += c;
+            acc[1] += c * c;
+            acc[2] += c * (unsigned long long)((long long)yy * P.W + xx);
+          }
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_xor_sync(FULL, acc[k], o);
+            if (lane == 0 && acc[k]) atomicAdd(&P.dbg_fpr[((int64_t)f * nlev + L0 + g) * 3 + k], acc[k]);
+          }
+        }
+        __syncthreads();   // read before the clear below
+      }
       {
 #if RD_K2_SETUP3 == 1
         if (L0 + G < nlev) setup(L0 + G, par ^ 1);
@@ -609,6 +633,11 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
       PMARK(4);
     }
     // ---------------- per-frame counters of this tile
+    if (warp == 0) {   // hotspots per level this tile needed (rd_query_overflow)
+      int m = 0;
+      for (int i = lane; i < nlev; i += 32) m = max(m, hcnt[i]);
+      need_h = max(need_h, __reduce_max_sync(FULL, m));
+    }
     my_hot = __reduce_add_sync(FULL, my_hot);
     if (lane == 0 && my_hot) atomicAdd(&P.stats[f].hotspots, (unsigned long long)my_hot);
     __syncthreads();
@@ -620,6 +649,8 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
       if (P.prof) atomicAdd(&P.prof[15], 1ull);
     }
   }
+  if (tid == 0 && need_e) atomicMax(&P.need[NEED_ENTRIES], need_e);
+  if (tid == 0 && need_h) atomicMax(&P.need[NEED_HOTSPOTS], need_h);
   if (P.prof && tid == 0) {
 #pragma unroll
     for (int i = 0; i < 6; ++i) atomicAdd(&P.prof[i], t_acc[i]);
@@ -639,6 +670,8 @@ __global__ void k_redo_reset(Params P, int n_frames) {
     P.stats[f].hotspots = 0;
     P.dbg_count[f] = 0;
     P.flags[f] &= ~(OVF_HOTSPOTS | OVF_RINGS | OVF_DEBUG);
+    if (P.dbg_fpr)
+      for (int i = 0; i < 3 * P.n_levels; ++i) P.dbg_fpr[(int64_t)f * 3 * P.n_levels + i] = 0;
     P.redo_list[1 + atomicAdd(&n, 1)] = f;
   }
   __syncthreads();

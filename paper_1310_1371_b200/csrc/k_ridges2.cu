@@ -13,8 +13,7 @@
 //   kappa (fixed fp64 recipe, no FMA) and rho of the candidates kappa < t, into row rings
 //   ridge test one row behind against the kappa ring (R6)
 // Three CTA barriers per step of RB rows; the RB rows of a phase are independent chains.
-// Pixels, taps and arithmetic are those of the tiled K1 (k_ridges.cu) and of the oracle:
-// every integer stage is exact, so evaluation order is free; kappa/rho use the shared
+// Every integer stage is exact, so evaluation order is free; kappa/rho use the shared
 // explicit-rounding recipe (rd_internal.cuh).  Replicate border: input rows and columns are
 // clamped at load time.
 #include <algorithm>
@@ -49,6 +48,7 @@ struct K1SSmem {                       // dynamic shared memory of k_ridges2
   int sI[KS_COLS][RB];                 // input rows (as int), a column's RB rows adjacent
   unsigned sBal[2][RB][KS_COLS / 32];  // ridge ballots of a step's rows, by parity
   int sCur[KS_NB];                     // ridges so far in the current row of each bin
+  int sNeed;                           // largest bin of the CTA (one global atomicMax at the end)
 };
 }  // namespace
 
@@ -111,6 +111,7 @@ k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, in
   const int b_own = (tid - KS_HALO) >> 5, b_i = (tid - KS_HALO) & 31;   // bin and index in it
   const int64_t fbase = (int64_t)f * P.nbx * P.nby;
   if (tid < KS_NB) sCur[tid] = 0;
+  if (tid == 0) S.sNeed = 0;
   unsigned rd_bits = 0;            // ridge flags of the previous step's RB test rows
   int rd_y0 = 0;                   // first test row of the previous step
   bool rd_any = false;             // the previous step tested rows of this segment
@@ -156,7 +157,10 @@ k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, in
             const int64_t bin = fbase + (int64_t)(yr / T1) * P.nbx + bx;
             P.bin_count[bin] = min(base, P.ridge_cap);
             if (base > P.ridge_cap) atomicOr(&P.flags[f], OVF_RIDGES);
-            if (base) atomicAdd(&P.stats[f].ridges, (unsigned long long)base);
+            if (base) {
+              atomicAdd(&P.stats[f].ridges, (unsigned long long)base);
+              atomicMax(&S.sNeed, base);
+            }
           }
           base = 0;
         }
@@ -276,6 +280,8 @@ k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, in
       rd_any |= yr >= Y0 && yr < Y1;
     }
   }
+  __syncthreads();
+  if (tid == 0 && S.sNeed) atomicMax(&P.need[NEED_RIDGES], S.sNeed);
 }
 
 template <typename PixT, int KS, bool EDGE>
@@ -285,16 +291,9 @@ static cudaError_t launch_s(const void* frames, int64_t pitch, int64_t fstride, 
   // dynamic shared memory: rings + rows (NR = RB + 2 rows of rho and kappa)
   const size_t sm = sizeof(K1SSmem<RB>);
   cudaFuncSetAttribute(k_ridges2<PixT, KS, RB, EDGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  // segments of whole bin rows: the count that best fills the resident CTA slots, each
-  // segment paying 3K_s + 6 rows of pipeline warm-up
-  static int slots = 0;
-  if (!slots) {
-    int dev = 0, nsm = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_ridges2<PixT, KS, RB, EDGE>, KS_COLS, sm);
-    slots = std::max(1, nsm * std::max(per, 1));
-  }
+  // segments of whole bin rows: the count that best fills the resident CTA slots (P.k1_slots,
+  // from rd_create), each segment paying 3K_s + 6 rows of pipeline warm-up
+  const int slots = std::max(1, P.k1_slots);
   const int strips = (P.W + KS_OUT - 1) / KS_OUT, bin_rows = (P.H + T1 - 1) / T1;
   int seg = bin_rows * T1;
   double best = -1.0;
@@ -339,16 +338,50 @@ static cudaError_t launch_sp(const void* frames, int64_t pitch, int64_t fstride,
   return cudaErrorInvalidValue;
 }
 
-// K_s <= 13 (the 16-column halo covers K_s + 3); larger K_s use the tiled K1
-bool ridges_stream_ok(const Params& P) { return P.Ks >= 1 && P.Ks <= KS_HALO - 3; }
+static_assert(KS_MAX <= KS_HALO - 3, "the 16-column halo covers K_s + 3");
 
-cudaError_t launch_ridges_stream(const void* frames, int64_t pitch, int64_t fstride, int n_frames, const Params& P,
-                                 cudaStream_t st) {
+size_t k_ridges_smem(int) { return sizeof(K1SSmem<RD_K1_RB>); }
+
+// resident K1 CTAs per device (all K1 instances share the launch bounds and shared memory)
+int k_ridges_slots(int n_sm) {
+  int per = 0;
+  const size_t sm = sizeof(K1SSmem<RD_K1_RB>);
+  cudaFuncSetAttribute(k_ridges2<uint16_t, 5, RD_K1_RB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_ridges2<uint16_t, 5, RD_K1_RB, false>, KS_COLS, sm) !=
+      cudaSuccess)
+    per = 1;
+  return std::max(1, n_sm * std::max(per, 1));
+}
+
+cudaError_t launch_ridges(const void* frames, int64_t pitch, int64_t fstride, int n_frames, const Params& P,
+                          cudaStream_t st) {
+  if (P.Ks < 1 || P.Ks > KS_MAX) return cudaErrorInvalidValue;
   if (P.feature == 1)
     return P.pixel_bytes == 1 ? launch_sp<uint8_t, true>(frames, pitch, fstride, n_frames, P, st)
                               : launch_sp<uint16_t, true>(frames, pitch, fstride, n_frames, P, st);
   return P.pixel_bytes == 1 ? launch_sp<uint8_t, false>(frames, pitch, fstride, n_frames, P, st)
                             : launch_sp<uint16_t, false>(frames, pitch, fstride, n_frames, P, st);
+}
+
+// A3 in isolation (rd_eigen): the same recipe on caller-supplied Hessians.
+__global__ void k_eigen(const double* __restrict__ abc, int64_t n, double* __restrict__ out, int* __restrict__ deg) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double a = abc[3 * i], b = abc[3 * i + 1], c = abc[3 * i + 2];
+  double s, e;
+  const double k = kappa_of(a, b, c, &s, &e);
+  double dx, dy;
+  const bool ok = direction_of(b, e, s, &dx, &dy);
+  out[3 * i] = k;
+  out[3 * i + 1] = dx;
+  out[3 * i + 2] = dy;
+  deg[i] = ok ? 0 : 1;
+}
+
+cudaError_t launch_eigen(const double* abc, int64_t n, double* out, int* deg, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  k_eigen<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(abc, n, out, deg);
+  return cudaGetLastError();
 }
 
 }  // namespace rd

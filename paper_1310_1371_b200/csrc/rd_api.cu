@@ -14,19 +14,19 @@
 
 namespace rd {
 size_t k_ridges_smem(int Ks);
+int k_ridges_slots(int n_sm);
 cudaError_t launch_ridges(const void* frames, int64_t pitch, int64_t fstride, int n_frames, const Params& P,
                           cudaStream_t st);
 cudaError_t launch_eigen(const double* abc, int64_t n, double* out, int* deg, cudaStream_t st);
-size_t k_hough_smem(const Params& P, int G);
-int k_hough_max_entries();
-cudaError_t launch_hough(int n_frames, const Params& P, bool wide, int G, int nt, int minb, cudaStream_t st);
 size_t k_hough2_layout(Params& P, int G, int nt, int cb);
 bool k_hough2_has_shape(int cb, int G, int nt, int minb);
 cudaError_t launch_redo_reset(int n_frames, const Params& P, cudaStream_t st);
 cudaError_t launch_hough2(int n_frames, const Params& P, bool wide, int G, int nt, int minb, int cb, int n_sm,
                           cudaStream_t st);
 size_t k_fit_smem(const Params& P);
-cudaError_t launch_fit(int n_frames, const Params& P, void* rings, int* counts, cudaStream_t st);
+cudaError_t launch_fit(int n_frames, const Params& P, cudaStream_t st);
+cudaError_t launch_emit(int n_frames, const Params& P, void* out, int out_cap, int* counts, int* offsets,
+                        const int* base_in, int* base_out, int* flags_out, cudaStream_t st);
 cudaError_t launch_rays(int n_frames, const Params& P, cudaStream_t st);
 cudaError_t launch_members(const Params& P, int f, int write, int* offsets, uint32_t* members, cudaStream_t st);
 constexpr int RD_NEV = 5;   // timing events per rd_detect: K1 | K1.5 | K2 | K3
@@ -53,7 +53,6 @@ struct rd_detector {
   Params P;
   bool wide;
   int G, k2_threads, k2_minb;   // Hough kernel launch shape (levels per step, threads, CTAs/SM)
-  int k2_impl;                  // 2: persistent K2 (k_hough2.cu), 1: one CTA per tile (k_hough.cu)
   int k2_cb;                    // counter bytes of the main persistent pass (1: + 16-bit redo pass)
   Params P16;                   // redo pass (16-bit counters): its own layout and shape
   int G16, k2_threads16, k2_minb16;
@@ -69,14 +68,26 @@ struct rd_detector {
   void* d_ray_r = nullptr;
   void* d_counters = nullptr;  // stats | peak_count | flags | dbg_count
   size_t counters_bytes = 0;
+  void* d_rings_int = nullptr; // K3 output per frame, compacted into the caller's buffer by k_emit
+  int* d_need = nullptr;       // [NEED_N] capacities the call needed
+  int* d_cursor = nullptr;     // host path: first output offset of each chunk (chained by k_scan)
   void* d_dbg = nullptr;
+  void* d_fpr = nullptr;       // debug: level fingerprints
+  int* d_mem_off = nullptr;    // rd_ring_members scratch: offsets (ring_cap + 1)
+  uint32_t* d_members = nullptr;
+  int64_t members_cap = 0;
+  cudaStream_t s_aux = nullptr;   // rd_ring_members / queries
   void* d_redo_list = nullptr;
-  // host-path staging
+  // host-path staging (rings, counts and offsets come back through mapped pinned memory)
   int chunk = 0;
+  rd_ring* h_out_rings = nullptr;   // mapped pinned: compacted rings of a host-path call
+  int64_t h_out_cap = 0;
+  int* h_out_co = nullptr;          // mapped pinned: counts [max chunk frames ...] per call (grown)
+  int64_t h_out_co_cap = 0;
+  int cursor_cap = 0;
+  int64_t last_d2h = 0;             // bytes the last host-path call read back
   static constexpr int NSTAGE = 4;   // host-path chunk buffers: copies run up to 3 chunks ahead
   void* d_stage[NSTAGE] = {};
-  void* d_rings_stage[NSTAGE] = {};
-  int* d_counts_stage[NSTAGE] = {};
   cudaStream_t s_comp = nullptr, s_h2d = nullptr, s_d2h = nullptr;
   cudaStream_t s_hc[4] = {};        // host path: chunk k computes on s_hc[k % n_slots] (tails overlap)
   static constexpr int NPART = 4;    // frame-view slots: rd_detect parts / host-path chunks
@@ -90,6 +101,7 @@ struct rd_detector {
   int n_timed = 0;
   unsigned long long* d_prof = nullptr;
   bool have_last = false;
+  bool last_host = false;           // the last call was rd_detect_host (internal buffers hold chunks)
   int last_n = 0;
 };
 
@@ -141,7 +153,8 @@ static rd_status validate(const rd_config* c) {
   if (c->width < 8 || c->height < 8 || c->width > 16384 || c->height > 16384) return RD_ERR_DIM;
   if (c->pixel != RD_U8 && c->pixel != RD_U16) return RD_ERR_PARAM;
   if (c->max_value < 1 || c->max_value > (c->pixel == RD_U8 ? 255 : 65535)) return RD_ERR_PARAM;
-  if (!(c->smoothing_sigma > 0.0) || !(c->smoothing_sigma <= 5.0)) return RD_ERR_PARAM;
+  // K_s = ceil(3 sigma_s) <= 13: the K1 strip's 16-column halo covers K_s + 3
+  if (!(c->smoothing_sigma > 0.0) || !(std::ceil(3.0 * c->smoothing_sigma) <= (double)KS_MAX)) return RD_ERR_PARAM;
   if (c->feature != RD_FEATURE_RIDGE && c->feature != RD_FEATURE_EDGE) return RD_ERR_PARAM;
   if (c->feature == RD_FEATURE_RIDGE && (!(c->curvature_threshold <= 0.0) || !std::isfinite(c->curvature_threshold)))
     return RD_ERR_PARAM;
@@ -172,7 +185,7 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   if (!c.max_hotspots_per_level) c.max_hotspots_per_level = c.feature == RD_FEATURE_EDGE ? 256 : 160;
   if (c.max_ridges_per_tile > T1 * T1) c.max_ridges_per_tile = T1 * T1;
   if (c.max_hotspots_per_level > 4095) return RD_ERR_PARAM;   // 12-bit hotspot index in K2 task lists
-  if (c.max_entries_per_tile > k_hough_max_entries()) c.max_entries_per_tile = k_hough_max_entries();
+  if (c.max_entries_per_tile > ENTRY_MAX) c.max_entries_per_tile = ENTRY_MAX;
 
   // ---- host tables (DESIGN.md §2 A1, A5, A7, A8, A9)
   Params P;
@@ -259,25 +272,14 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   P.debug = c.debug;
   P.dbg_cap = c.debug ? (1 << 20) : 0;
 
-  // Hough launch shape (tile side T, levels per step G, threads, CTAs per SM): the first of
-  // the candidates whose shared memory fits; RD_K2_SHAPE="T,G,threads,ctas" puts a shape first
   cudaDeviceProp prop;
   e = cudaGetDeviceProperties(&prop, device);
   if (e != cudaSuccess) { delete det; return cuda_fail(e, "cudaGetDeviceProperties"); }
   const size_t smax = prop.sharedMemPerBlockOptin, sm_sm = prop.sharedMemPerMultiprocessor;
   struct Shape { int T, G, nt, minb; };
-  std::vector<Shape> shapes = {{64, 8, 512, 1}, {64, 4, 512, 1}, {48, 4, 384, 2}, {64, 2, 512, 1}, {32, 2, 256, 1}};
-  if (const char* env = getenv("RD_K2_SHAPE")) {
-    Shape s{};
-    if (sscanf(env, "%d,%d,%d,%d", &s.T, &s.G, &s.nt, &s.minb) == 4 && s.T >= 16 && s.T <= 128 &&
-        (s.G == 2 || s.G == 4 || s.G == 8) && s.nt >= 64 && s.nt <= 512 && (s.nt % 32) == 0 && s.minb >= 1)
-      shapes.insert(shapes.begin(), s);
-  }
   det->G = 0;
   det->n_sm = prop.multiProcessorCount;
-  det->k2_impl = 2;
-  if (const char* env = getenv("RD_K2_IMPL")) det->k2_impl = atoi(env) == 1 ? 1 : 2;
-  if (det->k2_impl == 2) {
+  {
     // persistent K2: the first (T, G, threads, CTAs/SM) candidate whose layout fits with at
     // least 256 resident rays per tile, then as many resident rays as fit (up to entry_cap).
     // The 16-bit redo pass must use the main pass's tile side (K1.5 routes rays per tile).
@@ -383,24 +385,10 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
     }
     if (det->k2_cb == 1 && det->G16 == 0) det->G = 0;   // no 16-bit redo shape: not exact, do not use
   }
-  if (det->G == 0) {   // no persistent shape fits (large halo or capacities): one CTA per tile
-    det->k2_impl = 1;
-    for (const Shape& s : shapes) {
-      P.k2t = P.k2ty = s.T;
-      const size_t need = k_hough_smem(P, s.G);
-      const size_t limit = s.minb == 1 ? smax : std::min(smax, sm_sm / s.minb - 1024);
-      if (need <= limit) {
-        det->G = s.G;
-        det->k2_threads = s.nt;
-        det->k2_minb = s.minb;
-        break;
-      }
-    }
-  }
   if (getenv("RD_K2_VERBOSE"))
-    fprintf(stderr, "rd: K2 tiles %dx%d impl %d cb %d G %d threads %d ctas/SM %d smem %d rcap %d | redo G %d threads %d "
-            "ctas/SM %d smem %d rcap %d\n", P.k2t, P.k2ty, det->k2_impl, det->k2_cb, det->G, det->k2_threads, det->k2_minb,
-            det->k2_impl == 2 ? P.k2o.total : (int)k_hough_smem(P, det->G), P.k2_rcap, det->G16,
+    fprintf(stderr, "rd: K2 tiles %dx%d cb %d G %d threads %d ctas/SM %d smem %d rcap %d | redo G %d threads %d "
+            "ctas/SM %d smem %d rcap %d\n", P.k2t, P.k2ty, det->k2_cb, det->G, det->k2_threads, det->k2_minb,
+            P.k2o.total, P.k2_rcap, det->G16,
             det->k2_threads16, det->k2_minb16, det->P16.k2o.total, det->P16.k2_rcap);
   P.ntx = (c.width + P.k2t - 1) / P.k2t;
   P.nty = (c.height + P.k2ty - 1) / P.k2ty;
@@ -414,8 +402,8 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   }
   if (k_ridges_smem(P.Ks) > smax || det->G == 0 || k_fit_smem(P) > smax) {
     delete det;
-    snprintf(g_err, sizeof g_err, "shared memory: K1 %zu K2 %zu K3 %zu > %zu", k_ridges_smem(P.Ks),
-             k_hough_smem(P, 2), k_fit_smem(P), smax);
+    snprintf(g_err, sizeof g_err, "shared memory: K1 %zu K3 %zu (limit %zu); K2 %s", k_ridges_smem(P.Ks),
+             k_fit_smem(P), smax, det->G ? "fits" : "no persistent shape fits (halo K_max + 1 or capacities too large)");
     return RD_ERR_CONFIG;
   }
 
@@ -457,7 +445,13 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   ALLOC(det->d_ray_r, sizeof(uint32_t) * B * ntl * P.entry_cap);
   det->counters_bytes = sizeof(Stats) * B + sizeof(int) * 3 * B + sizeof(int) * B * ntl + 8 * rd_detector::NPART + sizeof(int) * B;
   ALLOC(det->d_counters, det->counters_bytes);
-  if (c.debug) ALLOC(det->d_dbg, sizeof(HotRec) * B * P.dbg_cap);
+  ALLOC(det->d_rings_int, sizeof(Ring) * B * P.ring_cap);
+  ALLOC(det->d_need, sizeof(int) * NEED_N);
+  ALLOC(det->d_mem_off, sizeof(int) * (P.ring_cap + 1));
+  if (c.debug) {
+    ALLOC(det->d_dbg, sizeof(HotRec) * B * P.dbg_cap);
+    ALLOC(det->d_fpr, sizeof(unsigned long long) * 3 * B * P.n_levels);
+  }
   // tables
   {
     std::vector<unsigned char> h(tb, 0);
@@ -492,6 +486,11 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   P.k2_work = P.ray_count + B * ntl;
   P.redo = P.k2_work + 2 * rd_detector::NPART;
   P.redo_list = nullptr;
+  P.rings = (Ring*)det->d_rings_int;
+  P.need = det->d_need;
+  P.dbg_fpr = (unsigned long long*)det->d_fpr;
+  P.n_sm = det->n_sm;
+  P.k1_slots = k_ridges_slots(det->n_sm);
   P.force_redo = getenv("RD_K2_FORCE_REDO") ? 1 : 0;
   P.u8_limit = 255;
   P.ablate = getenv("RD_K2_ABLATE") ? atoi(getenv("RD_K2_ABLATE")) : 0;
@@ -514,6 +513,8 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   }
   e = cudaEventCreateWithFlags(&det->ev_last, cudaEventDisableTiming);
   if (e != cudaSuccess) { rd_destroy(det); return cuda_fail(e, "cudaEventCreate"); }
+  e = cudaStreamCreateWithFlags(&det->s_aux, cudaStreamNonBlocking);
+  if (e != cudaSuccess) { rd_destroy(det); return cuda_fail(e, "cudaStreamCreate"); }
   *out = det;
   return RD_OK;
 }
@@ -529,14 +530,23 @@ rd_status rd_destroy(rd_detector* det) {
   cudaFree(det->d_ray_d);
   cudaFree(det->d_ray_xy);
   cudaFree(det->d_ray_r);
+  if (det->ev_last) cudaEventSynchronize(det->ev_last);
+  if (det->s_aux) cudaStreamSynchronize(det->s_aux);
   cudaFree(det->d_counters);
+  cudaFree(det->d_rings_int);
+  cudaFree(det->d_need);
+  cudaFree(det->d_cursor);
+  cudaFree(det->d_mem_off);
+  cudaFree(det->d_members);
+  cudaFree(det->d_fpr);
+  cudaFreeHost(det->h_out_rings);
+  cudaFreeHost(det->h_out_co);
+  if (det->s_aux) cudaStreamDestroy(det->s_aux);
   cudaFree(det->d_dbg);
   cudaFree(det->d_redo_list);
   cudaFree(det->d_prof);
   for (int i = 0; i < rd_detector::NSTAGE; ++i) {
     cudaFree(det->d_stage[i]);
-    cudaFree(det->d_rings_stage[i]);
-    cudaFree(det->d_counts_stage[i]);
   }
   if (det->s_comp) {
     cudaStreamDestroy(det->s_comp);
@@ -572,6 +582,7 @@ static void frame_view(const rd_detector* det, int f0, int slot, Params& V, Para
   V.bin_xy += f0 * nb * P.ridge_cap;
   V.bin_d += f0 * nb * P.ridge_cap;
   V.peaks += (int64_t)f0 * P.ring_cap;
+  V.rings += (int64_t)f0 * P.ring_cap;
   V.stats += f0;
   V.peak_count += f0;
   V.flags += f0;
@@ -581,6 +592,7 @@ static void frame_view(const rd_detector* det, int f0, int slot, Params& V, Para
   V.ray_xy += f0 * ntl * P.entry_cap;
   V.ray_r += f0 * ntl * P.entry_cap;
   if (V.dbg_hot) V.dbg_hot += (int64_t)f0 * P.dbg_cap;
+  if (V.dbg_fpr) V.dbg_fpr += (int64_t)f0 * 3 * P.n_levels;
   V.redo += f0;
   V.k2_work = P.k2_work + 2 * slot;   // [main, redo] work counters of the slot
   V16 = V;
@@ -591,9 +603,10 @@ static void frame_view(const rd_detector* det, int f0, int slot, Params& V, Para
   V16.redo_list = det->P16.redo_list + (int64_t)slot * (det->max_batch + 1);   // slot < NPART
 }
 
+// K1 -> K1.5 -> K2 (+ 16-bit redo) -> K3 on frames [f0, f0 + n) of the internal buffers (frame
+// view of slot `slot`); K3's rings stay in the per-frame scratch until k_emit.
 static rd_status detect_impl(rd_detector* det, const void* d_frames, int64_t pitch, int64_t fstride, int n,
-                             void* d_rings, int* d_counts, cudaStream_t st, int f0 = 0, int slot = 0,
-                             int parts = 1) {
+                             cudaStream_t st, int f0 = 0, int slot = 0, int parts = 1) {
   Params P, P16;
   frame_view(det, f0, slot, P, P16);
   P.parts = P16.parts = parts;
@@ -621,25 +634,19 @@ static rd_status detect_impl(rd_detector* det, const void* d_frames, int64_t pit
     CK(cudaMemsetAsync(P.k2_work, 0, sizeof(int) * 2, st));
     CK(cudaMemsetAsync(P.redo, 0, sizeof(int) * n, st));
   }
+  if (P.dbg_fpr) CK(cudaMemsetAsync(P.dbg_fpr, 0, sizeof(unsigned long long) * 3 * P.n_levels * n, st));
   if (ev) CK(cudaEventRecord(ev[0], st));
   CK(launch_ridges(d_frames, pitch, fstride, n, P, st));
   if (ev) CK(cudaEventRecord(ev[1], st));
   CK(launch_rays(n, P, st));
   if (ev) CK(cudaEventRecord(ev[2], st));
-  if (det->k2_impl == 2) {
-    CK(launch_hough2(n, P, det->wide, det->G, det->k2_threads, det->k2_minb, det->k2_cb, det->n_sm, st));
-    if (det->k2_cb == 1) {   // frames whose byte counters overflowed: recomputed with 16-bit counters
-      CK(launch_redo_reset(n, P16, st));
-      CK(launch_hough2(n, P16, det->wide, det->G16, det->k2_threads16, det->k2_minb16, 2, det->n_sm, st));
-    }
-  } else
-    CK(launch_hough(n, P, det->wide, det->G, det->k2_threads, det->k2_minb, st));
+  CK(launch_hough2(n, P, det->wide, det->G, det->k2_threads, det->k2_minb, det->k2_cb, det->n_sm, st));
+  if (det->k2_cb == 1) {   // frames whose byte counters overflowed: recomputed with 16-bit counters
+    CK(launch_redo_reset(n, P16, st));
+    CK(launch_hough2(n, P16, det->wide, det->G16, det->k2_threads16, det->k2_minb16, 2, det->n_sm, st));
+  }
   if (ev) CK(cudaEventRecord(ev[3], st));
-  CK(launch_fit(n, P, d_rings, d_counts, st));
-  if (ev) CK(cudaEventRecord(ev[4], st));
-  CK(cudaEventRecord(det->ev_last, st));
-  det->have_last = true;
-  det->last_n = n;
+  CK(launch_fit(n, P, st));
   return RD_OK;
 }
 
@@ -653,12 +660,17 @@ static rd_status check_frames(rd_detector* det, const void* frames, int64_t pitc
 }
 
 rd_status rd_detect(rd_detector* det, const void* d_frames, int64_t pitch, int64_t fstride, int32_t n,
-                    rd_ring* d_rings, int32_t* d_counts, void* stream) {
-  if (!det || n < 1 || n > det->max_batch || !d_rings || !d_counts) return RD_ERR_PARAM;
+                    rd_ring* d_rings, int32_t ring_cap_total, int32_t* d_counts, int32_t* d_offsets, void* stream) {
+  if (!det || n < 1 || n > det->max_batch || !d_counts || !d_offsets || ring_cap_total < 0 ||
+      (ring_cap_total > 0 && !d_rings) || ((uintptr_t)d_rings % 16))
+    return RD_ERR_PARAM;
   rd_status s = check_frames(det, d_frames, pitch, fstride, n);
   if (s != RD_OK) return s;
   CK(cudaSetDevice(det->device));
   cudaStream_t st = (cudaStream_t)stream;
+  if (det->have_last) CK(cudaStreamWaitEvent(st, det->ev_last, 0));   // the previous call's scratch
+  det->have_last = false;
+  CK(cudaMemsetAsync(det->d_need, 0, sizeof(int) * NEED_N, st));
   // A large batch runs as two halves on two internal streams (disjoint frame views of the
   // internal buffers), joined back into the caller's stream: each kernel's last partial
   // wave overlaps the other half's kernels.  Per-kernel timing keeps one stream.
@@ -677,17 +689,24 @@ rd_status rd_detect(rd_detector* det, const void* d_frames, int64_t pitch, int64
     for (int i = 0; i < parts; ++i) {
       const int f0 = (int)((int64_t)n * i / parts), f1 = (int)((int64_t)n * (i + 1) / parts);
       CK(cudaStreamWaitEvent(det->s_half[i], det->ev_fork, 0));
-      s = detect_impl(det, (const char*)d_frames + (size_t)f0 * fstride, pitch, fstride, f1 - f0,
-                      d_rings + (size_t)f0 * det->P.ring_cap, d_counts + f0, det->s_half[i], f0, i, parts);
+      s = detect_impl(det, (const char*)d_frames + (size_t)f0 * fstride, pitch, fstride, f1 - f0, det->s_half[i],
+                      f0, i, parts);
       if (s != RD_OK) return s;
       CK(cudaEventRecord(det->ev_join[i], det->s_half[i]));
       CK(cudaStreamWaitEvent(st, det->ev_join[i], 0));
     }
-    CK(cudaEventRecord(det->ev_last, st));
-    det->last_n = n;
-    return RD_OK;
+  } else {
+    s = detect_impl(det, d_frames, pitch, fstride, n, st);
+    if (s != RD_OK) return s;
   }
-  return detect_impl(det, d_frames, pitch, fstride, n, d_rings, d_counts, st);
+  // A11: counts, offsets and the compacted rings of all n frames
+  CK(launch_emit(n, det->P, d_rings, ring_cap_total, d_counts, d_offsets, nullptr, nullptr, nullptr, st));
+  if (det->timing) CK(cudaEventRecord(det->tev[RD_NEV * (size_t)(det->n_timed - 1) + RD_NEV - 1], st));
+  CK(cudaEventRecord(det->ev_last, st));
+  det->have_last = true;
+  det->last_host = false;
+  det->last_n = n;
+  return RD_OK;
 }
 
 static rd_status ensure_host_path(rd_detector* det) {
@@ -702,8 +721,6 @@ static rd_status ensure_host_path(rd_detector* det) {
   const size_t fbytes = (size_t)det->cfg.width * det->cfg.height * det->P.pixel_bytes;
   for (int i = 0; i < rd_detector::NSTAGE; ++i) {
     CK(cudaMalloc(&det->d_stage[i], fbytes * det->chunk));
-    CK(cudaMalloc(&det->d_rings_stage[i], sizeof(rd_ring) * det->chunk * det->P.ring_cap));
-    CK(cudaMalloc(&det->d_counts_stage[i], sizeof(int) * det->chunk));
     CK(cudaEventCreateWithFlags(&det->ev_h2d[i], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&det->ev_done[i], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&det->ev_d2h[i], cudaEventDisableTiming));
@@ -717,26 +734,65 @@ static rd_status ensure_host_path(rd_detector* det) {
 }
 
 rd_status rd_detect_host(rd_detector* det, const void* h_frames, int64_t pitch, int64_t fstride, int32_t n,
-                         rd_ring* h_rings, int32_t* h_counts) {
-  if (!det || n < 1 || !h_rings || !h_counts) return RD_ERR_PARAM;
+                         rd_ring* h_rings, int32_t ring_cap_total, int32_t* h_counts, int32_t* h_offsets) {
+  if (!det || n < 1 || !h_counts || !h_offsets || ring_cap_total < 0 || (ring_cap_total > 0 && !h_rings))
+    return RD_ERR_PARAM;
   rd_status s = check_frames(det, h_frames, pitch, fstride, n);
   if (s != RD_OK) return s;
   CK(cudaSetDevice(det->device));
   s = ensure_host_path(det);
   if (s != RD_OK) return s;
+  // output staging: mapped pinned memory the k_emit copies write straight into (only the rings
+  // found cross the bus), grown when a call asks for more than any before
+  if (det->h_out_cap < std::max<int64_t>(ring_cap_total, 1)) {
+    cudaFreeHost(det->h_out_rings);
+    det->h_out_rings = nullptr;
+    det->h_out_cap = 0;
+    CK(cudaHostAlloc((void**)&det->h_out_rings, sizeof(rd_ring) * std::max<int64_t>(ring_cap_total, 1),
+                     cudaHostAllocMapped));
+    det->h_out_cap = std::max<int64_t>(ring_cap_total, 1);
+  }
+  if (det->h_out_co_cap < 3LL * n + 1) {   // counts [n] | offsets [n + 1] | flags [n]
+    cudaFreeHost(det->h_out_co);
+    det->h_out_co = nullptr;
+    det->h_out_co_cap = 0;
+    CK(cudaHostAlloc((void**)&det->h_out_co, sizeof(int) * (3LL * n + 1), cudaHostAllocMapped));
+    det->h_out_co_cap = 3LL * n + 1;
+  }
   const int W = det->cfg.width, H = det->cfg.height, pb = det->P.pixel_bytes;
   const size_t row = (size_t)W * pb, fbytes = row * H;
-  const int C = det->chunk, rc = det->P.ring_cap;
+  const int C = det->chunk;
   // chunk sizes ramp up from a quarter chunk by 3/2 per chunk: the first copy is the only one
   // nothing overlaps, and each copy ends before the previous (smaller) chunk's compute does
-  // (a symmetric ramp-down at the end measured no better)
   std::vector<int> cstart;
   for (int f = 0, m = std::max(1, C / 4); f < n; f += m, m = std::min(C, std::max(m + 1, m * 3 / 2)))
     cstart.push_back(f);
   cstart.push_back(n);
   const int nchunks = (int)cstart.size() - 1;
-  rd_status result = RD_OK;
-  // RD_HOST_TRACE: per-chunk copy / compute / readback times on stderr (diagnostics only)
+  if ((int)det->cursor_cap < nchunks + 1) {
+    cudaFree(det->d_cursor);
+    det->d_cursor = nullptr;
+    CK(cudaMalloc(&det->d_cursor, sizeof(int) * (nchunks + 1)));
+    det->cursor_cap = nchunks + 1;
+  }
+  rd_ring* d_out_rings = nullptr;
+  int* d_out_co = nullptr;
+  CK(cudaHostGetDevicePointer((void**)&d_out_rings, det->h_out_rings, 0));
+  CK(cudaHostGetDevicePointer((void**)&d_out_co, det->h_out_co, 0));
+  int* d_counts_all = d_out_co;            // [n]
+  int* d_offsets_all = d_out_co + n;       // [n + 1]
+  int* d_flags_all = d_out_co + 2 * n + 1; // [n]
+  // the previous call on this detector (rd_detect on a caller stream) must finish first
+  if (det->have_last) {
+    CK(cudaStreamWaitEvent(det->s_h2d, det->ev_last, 0));
+    for (int i = 0; i < det->n_slots; ++i) CK(cudaStreamWaitEvent(det->s_hc[i], det->ev_last, 0));
+  }
+  det->have_last = false;
+  CK(cudaMemsetAsync(det->d_need, 0, sizeof(int) * NEED_N, det->s_h2d));
+  CK(cudaMemsetAsync(det->d_cursor, 0, sizeof(int), det->s_h2d));
+  CK(cudaEventRecord(det->ev_d2h[0], det->s_h2d));   // the memsets before any chunk's kernels
+  for (int i = 0; i < det->n_slots; ++i) CK(cudaStreamWaitEvent(det->s_hc[i], det->ev_d2h[0], 0));
+  // RD_HOST_TRACE: per-chunk copy / compute times on stderr (diagnostics only)
   const bool trace = getenv("RD_HOST_TRACE") != nullptr;
   std::vector<cudaEvent_t> tev;
   auto mark = [&](cudaStream_t st) {
@@ -749,7 +805,7 @@ rd_status rd_detect_host(rd_detector* det, const void* h_frames, int64_t pitch, 
   for (int k = 0; k < nchunks; ++k) {
     const int f0 = cstart[k], m = cstart[k + 1] - f0;
     // buffer slot and stream b: chunk k overlaps chunk k - 1 (other slot) and follows chunk k - 2
-    // on the same stream; stage q holds its frames and rings
+    // on the same stream; stage q holds its frames
     const int b = k % det->n_slots, q = k % rd_detector::NSTAGE;
     cudaStream_t sc = det->s_hc[b];
     // H2D of chunk k may overwrite stage q only after the stage's previous chunk finished computing
@@ -766,41 +822,50 @@ rd_status rd_detect_host(rd_detector* det, const void* h_frames, int64_t pitch, 
     CK(cudaEventRecord(det->ev_h2d[q], det->s_h2d));
     mark(det->s_h2d);
     CK(cudaStreamWaitEvent(sc, det->ev_h2d[q], 0));
-    // the ring stage q is reused only after its previous D2H completed
-    if (k >= rd_detector::NSTAGE) CK(cudaStreamWaitEvent(sc, det->ev_d2h[q], 0));
     mark(sc);
-    s = detect_impl(det, det->d_stage[q], row, fbytes, m, det->d_rings_stage[q], det->d_counts_stage[q], sc,
-                    b * C, b);
+    s = detect_impl(det, det->d_stage[q], row, fbytes, m, sc, b * C, b);
     if (s != RD_OK) return s;
     CK(cudaEventRecord(det->ev_done[q], sc));
+    // A11 for the chunk: its first offset is the previous chunk's end (chained through d_cursor)
+    if (k > 0) CK(cudaStreamWaitEvent(sc, det->ev_d2h[(k - 1) % rd_detector::NSTAGE], 0));
+    Params V, V16;
+    frame_view(det, b * C, b, V, V16);
+    CK(launch_emit(m, V, d_out_rings, ring_cap_total, d_counts_all + f0, d_offsets_all + f0, det->d_cursor + k,
+                   det->d_cursor + k + 1, d_flags_all + f0, sc));
+    if (det->timing) CK(cudaEventRecord(det->tev[RD_NEV * (size_t)(det->n_timed - 1) + RD_NEV - 1], sc));
+    CK(cudaEventRecord(det->ev_d2h[q], sc));
     mark(sc);
-    CK(cudaStreamWaitEvent(det->s_d2h, det->ev_done[q], 0));
-    CK(cudaMemcpyAsync(h_rings + (size_t)f0 * rc, det->d_rings_stage[q], sizeof(rd_ring) * (size_t)m * rc,
-                       cudaMemcpyDeviceToHost, det->s_d2h));
-    CK(cudaMemcpyAsync(h_counts + f0, det->d_counts_stage[q], sizeof(int) * m, cudaMemcpyDeviceToHost,
-                       det->s_d2h));
-    CK(cudaEventRecord(det->ev_d2h[q], det->s_d2h));
-    mark(det->s_d2h);
   }
-  CK(cudaStreamSynchronize(det->s_d2h));
-  CK(cudaStreamSynchronize(det->s_comp));
-  for (int i = 1; i < det->n_slots; ++i) CK(cudaStreamSynchronize(det->s_hc[i]));
-  if (trace) {   // per chunk: h2d start/end, compute start/end, d2h end (ms from the first copy)
-    for (size_t i = 0; i + 5 <= tev.size(); i += 5) {
-      float t[5];
-      for (int j = 0; j < 5; ++j) cudaEventElapsedTime(&t[j], tev[0], tev[i + j]);
-      fprintf(stderr, "rd: chunk %zu h2d %.3f-%.3f comp %.3f-%.3f d2h-end %.3f\n", i / 5, t[0], t[1], t[2], t[3], t[4]);
+  for (int i = 0; i < det->n_slots; ++i) CK(cudaStreamSynchronize(det->s_hc[i]));
+  CK(cudaStreamSynchronize(det->s_h2d));
+  if (trace) {   // per chunk: h2d start/end, compute start, emit end (ms from the first copy)
+    for (size_t i = 0; i + 4 <= tev.size(); i += 4) {
+      float t[4];
+      for (int j = 0; j < 4; ++j) cudaEventElapsedTime(&t[j], tev[0], tev[i + j]);
+      fprintf(stderr, "rd: chunk %zu h2d %.3f-%.3f comp %.3f-%.3f\n", i / 4, t[0], t[1], t[2], t[3]);
     }
     for (cudaEvent_t e : tev) cudaEventDestroy(e);
   }
-  for (int i = 0; i < n; ++i)
+  memcpy(h_counts, det->h_out_co, sizeof(int) * n);
+  memcpy(h_offsets, det->h_out_co + n, sizeof(int) * (n + 1));
+  int64_t total = 0;   // rings written: the valid frames' ranges (all inside ring_cap_total)
+  rd_status result = RD_OK;
+  for (int i = 0; i < n; ++i) {
     if (h_counts[i] < 0) result = RD_ERR_CAPACITY;
+    else total = std::max<int64_t>(total, (int64_t)h_offsets[i] + h_counts[i]);
+  }
+  if (total > 0) memcpy(h_rings, det->h_out_rings, sizeof(rd_ring) * total);
+  CK(cudaEventRecord(det->ev_last, det->s_h2d));
+  det->have_last = true;
+  det->last_host = true;
+  det->last_n = n;
+  det->last_d2h = total * (int64_t)sizeof(rd_ring) + sizeof(int) * (2LL * n + 1);
   return result;
 }
 
 rd_status rd_sync(rd_detector* det) {
   if (!det) return RD_ERR_PARAM;
-  if (!det->have_last) return RD_ERR_STATE;
+  if (!det->have_last || det->last_host) return RD_ERR_STATE;
   CK(cudaSetDevice(det->device));
   CK(cudaEventSynchronize(det->ev_last));
   std::vector<int> fl(det->last_n);
@@ -810,9 +875,46 @@ rd_status rd_sync(rd_detector* det) {
   return RD_OK;
 }
 
-rd_status rd_query_overflow(rd_detector* det, int32_t n, int32_t* h_flags) {
-  if (!det || !h_flags || n < 1 || n > det->max_batch) return RD_ERR_PARAM;
+rd_status rd_query_overflow(rd_detector* det, rd_overflow* out) {
+  if (!det || !out) return RD_ERR_PARAM;
   if (!det->have_last) return RD_ERR_STATE;
+  CK(cudaSetDevice(det->device));
+  CK(cudaEventSynchronize(det->ev_last));
+  int need[NEED_N];
+  CK(cudaMemcpy(need, det->d_need, sizeof need, cudaMemcpyDeviceToHost));
+  memset(out, 0, sizeof *out);
+  out->needed_ridges_per_tile = need[NEED_RIDGES];
+  out->needed_entries_per_tile = need[NEED_ENTRIES];
+  out->needed_hotspots_per_level = need[NEED_HOTSPOTS];
+  out->needed_rings_per_frame = need[NEED_RINGS];
+  const int n = det->last_n;
+  std::vector<int> counts(n), offsets(n + 1), flags(n, 0);
+  if (det->last_host) {   // the host path leaves counts, offsets and flags in its mapped staging
+    memcpy(counts.data(), det->h_out_co, sizeof(int) * n);
+    memcpy(offsets.data(), det->h_out_co + n, sizeof(int) * (n + 1));
+    memcpy(flags.data(), det->h_out_co + 2 * n + 1, sizeof(int) * n);
+  } else {
+    CK(cudaMemcpy(flags.data(), det->P.flags, sizeof(int) * n, cudaMemcpyDeviceToHost));
+    std::vector<int> pk(n);
+    CK(cudaMemcpy(pk.data(), det->P.peak_count, sizeof(int) * n, cudaMemcpyDeviceToHost));
+    offsets[0] = 0;
+    for (int i = 0; i < n; ++i) {
+      const bool valid = (flags[i] & ~OVF_OUTPUT) == 0 && pk[i] <= det->P.ring_cap;
+      offsets[i + 1] = offsets[i] + (valid ? pk[i] : 0);
+    }
+  }
+  for (int i = 0; i < n; ++i) {
+    if (flags[i]) ++out->frames_overflowed;
+    out->flags |= flags[i];
+  }
+  out->needed_rings_total = offsets[n];
+  return RD_OK;
+}
+
+rd_status rd_query_flags(rd_detector* det, int32_t n, int32_t* h_flags) {
+  if (!det || !h_flags || n < 1) return RD_ERR_PARAM;
+  if (!det->have_last || det->last_host) return RD_ERR_STATE;
+  if (n > det->last_n) return RD_ERR_PARAM;
   CK(cudaSetDevice(det->device));
   CK(cudaEventSynchronize(det->ev_last));
   CK(cudaMemcpy(h_flags, det->P.flags, sizeof(int) * n, cudaMemcpyDeviceToHost));
@@ -821,11 +923,38 @@ rd_status rd_query_overflow(rd_detector* det, int32_t n, int32_t* h_flags) {
 
 rd_status rd_get_stats(rd_detector* det, int32_t n, rd_frame_stats* h) {
   if (!det || !h || n < 1 || n > det->max_batch) return RD_ERR_PARAM;
-  if (!det->have_last) return RD_ERR_STATE;
+  if (!det->have_last || det->last_host) return RD_ERR_STATE;
+  if (n > det->last_n) return RD_ERR_PARAM;
   static_assert(sizeof(rd_frame_stats) == sizeof(Stats), "stats layout");
   CK(cudaSetDevice(det->device));
   CK(cudaEventSynchronize(det->ev_last));
   CK(cudaMemcpy(h, det->P.stats, sizeof(Stats) * n, cudaMemcpyDeviceToHost));
+  return RD_OK;
+}
+
+// members of frame `frame` into det->d_members (grown as needed); *npk, *total on return
+static rd_status members_impl(rd_detector* det, int frame, int* npk_out, int* total_out) {
+  const Params& P = det->P;
+  int flags = 0, npk = 0;
+  CK(cudaStreamWaitEvent(det->s_aux, det->ev_last, 0));
+  CK(cudaMemcpyAsync(&flags, P.flags + frame, sizeof(int), cudaMemcpyDeviceToHost, det->s_aux));
+  CK(cudaMemcpyAsync(&npk, P.peak_count + frame, sizeof(int), cudaMemcpyDeviceToHost, det->s_aux));
+  CK(cudaStreamSynchronize(det->s_aux));
+  if ((flags & ~OVF_OUTPUT) != 0 || npk > P.ring_cap) return RD_ERR_CAPACITY;   // no valid ring list
+  CK(launch_members(P, frame, 0, det->d_mem_off, nullptr, det->s_aux));
+  int total = 0;
+  CK(cudaMemcpyAsync(&total, det->d_mem_off + npk, sizeof(int), cudaMemcpyDeviceToHost, det->s_aux));
+  CK(cudaStreamSynchronize(det->s_aux));
+  if (total > det->members_cap) {
+    CK(cudaFree(det->d_members));
+    det->d_members = nullptr;
+    det->members_cap = 0;
+    CK(cudaMalloc(&det->d_members, sizeof(uint32_t) * total));
+    det->members_cap = total;
+  }
+  if (total > 0) CK(launch_members(P, frame, 1, det->d_mem_off, det->d_members, det->s_aux));
+  *npk_out = npk;
+  *total_out = total;
   return RD_OK;
 }
 
@@ -834,78 +963,90 @@ rd_status rd_ring_members(rd_detector* det, int32_t frame, int32_t* h_offsets, i
   if (!det || !n_total || frame < 0 || frame >= det->max_batch || offsets_cap < 0 || cap < 0 ||
       (offsets_cap > 0 && !h_offsets) || (cap > 0 && !h_members))
     return RD_ERR_PARAM;
-  if (!det->have_last || frame >= det->last_n) return RD_ERR_STATE;
+  if (!det->have_last || det->last_host || frame >= det->last_n) return RD_ERR_STATE;
   CK(cudaSetDevice(det->device));
-  CK(cudaEventSynchronize(det->ev_last));
-  const Params& P = det->P;
-  int flags = 0, npk = 0;
-  CK(cudaMemcpy(&flags, P.flags + frame, sizeof(int), cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(&npk, P.peak_count + frame, sizeof(int), cudaMemcpyDeviceToHost));
-  if (flags != 0 || npk > P.ring_cap) return RD_ERR_CAPACITY;   // the frame has no valid ring list
-  int* d_off = nullptr;
-  uint32_t* d_mem = nullptr;
-  rd_status result = RD_OK;
-  std::vector<int> off(npk + 1, 0);
-  cudaError_t e = cudaMalloc(&d_off, sizeof(int) * (npk + 1));
-  if (e == cudaSuccess) e = launch_members(P, frame, 0, d_off, nullptr, 0);
-  if (e == cudaSuccess) e = cudaMemcpy(off.data(), d_off, sizeof(int) * (npk + 1), cudaMemcpyDeviceToHost);
-  if (e == cudaSuccess && off[npk] > 0) {
-    e = cudaMalloc(&d_mem, sizeof(uint32_t) * off[npk]);
-    if (e == cudaSuccess) e = launch_members(P, frame, 1, d_off, d_mem, 0);
-    if (e == cudaSuccess && cap > 0)
-      e = cudaMemcpy(h_members, d_mem, sizeof(uint32_t) * std::min<int64_t>(cap, off[npk]), cudaMemcpyDeviceToHost);
-  }
-  if (e == cudaSuccess) e = cudaDeviceSynchronize();
-  if (e != cudaSuccess) result = cuda_fail(e, "rd_ring_members");
-  cudaFree(d_off);
-  cudaFree(d_mem);
-  if (result != RD_OK) return result;
-  for (int i = 0; i < std::min(offsets_cap, npk + 1); ++i) h_offsets[i] = off[i];
-  *n_total = off[npk];
+  int npk = 0, total = 0;
+  rd_status s = members_impl(det, frame, &npk, &total);
+  if (s != RD_OK) return s;
+  const int no = std::min(offsets_cap, npk + 1);
+  if (no > 0) CK(cudaMemcpyAsync(h_offsets, det->d_mem_off, sizeof(int) * no, cudaMemcpyDeviceToHost, det->s_aux));
+  const int64_t nm = std::min<int64_t>(cap, total);
+  if (nm > 0)
+    CK(cudaMemcpyAsync(h_members, det->d_members, sizeof(uint32_t) * nm, cudaMemcpyDeviceToHost, det->s_aux));
+  CK(cudaStreamSynchronize(det->s_aux));
+  *n_total = total;
   return RD_OK;
 }
 
-rd_status rd_dump_ridges(rd_detector* det, int32_t frame, rd_ridge* h_out, int64_t cap, int64_t* n_out) {
-  if (!det || !n_out || frame < 0 || frame >= det->max_batch || (cap > 0 && !h_out)) return RD_ERR_PARAM;
-  if (!det->have_last) return RD_ERR_STATE;
+rd_status rd_debug_dump(rd_detector* det, int32_t frame, int32_t what, void* h_buf, int64_t cap_bytes,
+                        int64_t* n_out) {
+  if (!det || !n_out || frame < 0 || frame >= det->max_batch || cap_bytes < 0 || (cap_bytes > 0 && !h_buf))
+    return RD_ERR_PARAM;
+  if (what < RD_DUMP_RIDGES || what > RD_DUMP_MEMBERS) return RD_ERR_PARAM;
+  if (!det->have_last || det->last_host || frame >= det->last_n) return RD_ERR_STATE;
+  if ((what == RD_DUMP_LEVEL_FPR || what == RD_DUMP_HOTSPOTS) && !det->cfg.debug) return RD_ERR_STATE;
   CK(cudaSetDevice(det->device));
   CK(cudaEventSynchronize(det->ev_last));
   const Params& P = det->P;
-  const int64_t nb = (int64_t)P.nbx * P.nby;
-  std::vector<int> cnt(nb);
-  std::vector<uint32_t> xy((size_t)nb * P.ridge_cap);
-  std::vector<double2> d((size_t)nb * P.ridge_cap);
-  CK(cudaMemcpy(cnt.data(), P.bin_count + frame * nb, sizeof(int) * nb, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(xy.data(), P.bin_xy + frame * nb * P.ridge_cap, sizeof(uint32_t) * xy.size(),
-                cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(d.data(), P.bin_d + frame * nb * P.ridge_cap, sizeof(double2) * d.size(), cudaMemcpyDeviceToHost));
-  int64_t k = 0;
-  for (int64_t b = 0; b < nb; ++b)
-    for (int i = 0; i < cnt[b]; ++i, ++k)
-      if (k < cap) {
-        uint32_t v = xy[b * P.ridge_cap + i];
-        h_out[k].x = (int32_t)(v & 0xFFFFu);
-        h_out[k].y = (int32_t)(v >> 16);
-        h_out[k].dx = d[b * P.ridge_cap + i].x;
-        h_out[k].dy = d[b * P.ridge_cap + i].y;
-      }
-  *n_out = k;
-  return RD_OK;
-}
-
-rd_status rd_dump_hotspots(rd_detector* det, int32_t frame, rd_hotspot* h_out, int64_t cap, int64_t* n_out) {
-  if (!det || !n_out || frame < 0 || frame >= det->max_batch || (cap > 0 && !h_out)) return RD_ERR_PARAM;
-  if (!det->have_last || !det->cfg.debug) return RD_ERR_STATE;
-  static_assert(sizeof(rd_hotspot) == sizeof(HotRec), "hotspot layout");
-  CK(cudaSetDevice(det->device));
-  CK(cudaEventSynchronize(det->ev_last));
-  int n = 0;
-  CK(cudaMemcpy(&n, det->P.dbg_count + frame, sizeof(int), cudaMemcpyDeviceToHost));
-  int64_t m = std::min<int64_t>(std::min<int64_t>(n, det->P.dbg_cap), cap);
-  if (m > 0)
-    CK(cudaMemcpy(h_out, det->P.dbg_hot + (int64_t)frame * det->P.dbg_cap, sizeof(HotRec) * m,
+  if (what == RD_DUMP_RIDGES) {
+    const int64_t nb = (int64_t)P.nbx * P.nby;
+    std::vector<int> cnt(nb);
+    std::vector<uint32_t> xy((size_t)nb * P.ridge_cap);
+    std::vector<double2> d((size_t)nb * P.ridge_cap);
+    CK(cudaMemcpy(cnt.data(), P.bin_count + frame * nb, sizeof(int) * nb, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(xy.data(), P.bin_xy + frame * nb * P.ridge_cap, sizeof(uint32_t) * xy.size(),
                   cudaMemcpyDeviceToHost));
-  *n_out = n;
+    CK(cudaMemcpy(d.data(), P.bin_d + frame * nb * P.ridge_cap, sizeof(double2) * d.size(), cudaMemcpyDeviceToHost));
+    rd_ridge* out = (rd_ridge*)h_buf;
+    const int64_t cap = cap_bytes / (int64_t)sizeof(rd_ridge);
+    int64_t k = 0;
+    for (int64_t b = 0; b < nb; ++b)
+      for (int i = 0; i < std::min(cnt[b], P.ridge_cap); ++i, ++k)
+        if (k < cap) {
+          const uint32_t v = xy[b * P.ridge_cap + i];
+          out[k].x = (int32_t)(v & 0xFFFFu);
+          out[k].y = (int32_t)(v >> 16);
+          out[k].dx = d[b * P.ridge_cap + i].x;
+          out[k].dy = d[b * P.ridge_cap + i].y;
+        }
+    *n_out = k;
+    return RD_OK;
+  }
+  if (what == RD_DUMP_LEVEL_FPR) {
+    static_assert(sizeof(rd_level_fpr) == 32, "fingerprint layout");
+    std::vector<unsigned long long> f(3 * (size_t)P.n_levels);
+    CK(cudaMemcpy(f.data(), P.dbg_fpr + (int64_t)frame * 3 * P.n_levels, sizeof(unsigned long long) * f.size(),
+                  cudaMemcpyDeviceToHost));
+    rd_level_fpr* out = (rd_level_fpr*)h_buf;
+    const int64_t cap = cap_bytes / (int64_t)sizeof(rd_level_fpr);
+    for (int li = 0; li < P.n_levels && li < cap; ++li) {
+      out[li].r = P.r_lo + li;
+      out[li].pad = 0;
+      out[li].votes = (int64_t)f[3 * li];
+      out[li].sq = (int64_t)f[3 * li + 1];
+      out[li].pos = (int64_t)f[3 * li + 2];
+    }
+    *n_out = P.n_levels;
+    return RD_OK;
+  }
+  if (what == RD_DUMP_HOTSPOTS) {
+    static_assert(sizeof(rd_hotspot) == sizeof(HotRec), "hotspot layout");
+    int n = 0;
+    CK(cudaMemcpy(&n, P.dbg_count + frame, sizeof(int), cudaMemcpyDeviceToHost));
+    const int64_t m = std::min<int64_t>(std::min<int64_t>(n, P.dbg_cap), cap_bytes / (int64_t)sizeof(HotRec));
+    if (m > 0)
+      CK(cudaMemcpy(h_buf, P.dbg_hot + (int64_t)frame * P.dbg_cap, sizeof(HotRec) * m, cudaMemcpyDeviceToHost));
+    *n_out = n;
+    return RD_OK;
+  }
+  int npk = 0, total = 0;   // RD_DUMP_MEMBERS
+  rd_status s = members_impl(det, frame, &npk, &total);
+  if (s != RD_OK) return s;
+  const int64_t nm = std::min<int64_t>(cap_bytes / (int64_t)sizeof(uint32_t), total);
+  if (nm > 0)
+    CK(cudaMemcpyAsync(h_buf, det->d_members, sizeof(uint32_t) * nm, cudaMemcpyDeviceToHost, det->s_aux));
+  CK(cudaStreamSynchronize(det->s_aux));
+  *n_out = total;
   return RD_OK;
 }
 

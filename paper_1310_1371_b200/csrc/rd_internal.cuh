@@ -7,13 +7,14 @@
 namespace rd {
 
 constexpr int T1 = 32;          // K1 (ridge) tile: 32x32 output pixels; also the ridge-bin size
-constexpr int KS_MAX = 15;      // smoothing half-width limit (sigma_s <= 5)
-constexpr int K1_THREADS = 256;
-constexpr int K2_THREADS = 256;
+constexpr int KS_MAX = 13;      // smoothing half-width limit: K_s = ceil(3 sigma_s) <= 13 (sigma_s <= 13/3)
 constexpr int K3_THREADS = 256;
+constexpr int ENTRY_MAX = 65535;   // voting rays per Hough tile (16-bit indices in K2's active list)
 
 // Per-frame overflow flag bits (rd_query_overflow)
-constexpr int OVF_RIDGES = 1, OVF_ENTRIES = 2, OVF_HOTSPOTS = 4, OVF_RINGS = 8, OVF_DEBUG = 16;
+constexpr int OVF_RIDGES = 1, OVF_ENTRIES = 2, OVF_HOTSPOTS = 4, OVF_RINGS = 8, OVF_DEBUG = 16, OVF_OUTPUT = 32;
+// needed capacities (rd_query_overflow): largest value met, kept with atomicMax
+constexpr int NEED_RIDGES = 0, NEED_ENTRIES = 1, NEED_HOTSPOTS = 2, NEED_RINGS = 3, NEED_N = 4;
 
 struct Peak {          // peak record produced by K2, consumed by K3 (24 B)
   int32_t x, y, r, raw;
@@ -27,6 +28,13 @@ struct HotRec {        // debug hotspot record (24 B), same layout as rd_hotspot
 
 struct Stats {         // per-frame counters (same layout as rd_frame_stats)
   unsigned long long ridges, votes, hotspots, peaks;
+};
+
+struct Ring {          // == rd_ring (64 B)
+  int32_t cx, cy, r, raw_votes;
+  int64_t score_fixed;
+  int32_t inliers, fit_ok;
+  double fx, fy, fr, rms;
 };
 
 // Shared-memory layout of the persistent Hough kernel (byte offsets; host-computed)
@@ -87,7 +95,12 @@ struct Params {
   int* peak_count;              // [F]
   int* flags;                   // [F] overflow bits
   Stats* stats;                 // [F]
+  Ring* rings;                  // [F][ring_cap] K3 output in canonical order (compacted by k_emit)
+  int* need;                    // [NEED_N] capacities needed by the call (atomicMax)
+  int n_sm;                     // SMs of the device (grid sizing)
+  int k1_slots;                 // resident K1 CTAs on the device (row-segment choice)
   int debug;
+  unsigned long long* dbg_fpr;  // [F][n_levels][3] level fingerprints (debug): sum raw, sum raw^2, sum raw*(yW+x)
   unsigned long long* prof;     // optional per-phase cycle counters (rd_phase_cycles), may be null
   int dbg_cap;
   HotRec* dbg_hot;              // [F][dbg_cap]

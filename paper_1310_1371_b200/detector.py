@@ -1,18 +1,44 @@
-"""Detector: Python face of rd_create / rd_detect / rd_detect_host (include/rd.h)."""
+"""Detector: Python face of rd_create / rd_detect / rd_detect_host (include/rd.h).
+
+Argument marshalling only: every step of the path runs in librd.so's CUDA kernels.
+"""
 from __future__ import annotations
 
 import ctypes as C
+from dataclasses import dataclass
 
 import numpy as np
 import torch
 
 from . import _rd
-from ._rd import HOT_DTYPE, RIDGE_DTYPE, RING_DTYPE, STATS_DTYPE, check, lib
+from ._rd import FPR_DTYPE, HOT_DTYPE, RIDGE_DTYPE, RING_DTYPE, STATS_DTYPE, check, lib
 
 _CFG_KEYS = ("max_value", "smoothing_sigma", "curvature_threshold", "r_min", "r_max", "vote_threshold_raw",
              "vote_threshold_norm", "sig_a", "sig_b", "sig_den", "annulus_halfwidth", "max_rings_per_frame",
              "max_ridges_per_tile", "max_entries_per_tile", "max_hotspots_per_level", "debug", "feature",
              "edge_threshold")
+
+
+@dataclass
+class RingBatch:
+    """Output of one detect call (rd.h: rings of frame f are rings[offsets[f]:offsets[f] + counts[f]],
+    canonical (r, cy, cx) order; counts[f] = -1 if a capacity overflowed for frame f).
+    rings: [capacity, 64] uint8 records (device tensor or host array/tensor)."""
+    rings: object
+    counts: object
+    offsets: object
+
+    def __iter__(self):   # (rings, counts, offsets) unpacking
+        return iter((self.rings, self.counts, self.offsets))
+
+    def to_numpy(self) -> list:
+        """Per-frame structured arrays (RING_DTYPE); None for frames with count -1."""
+        def host(x):
+            return x.cpu().numpy() if isinstance(x, torch.Tensor) else np.asarray(x)
+        c, o = host(self.counts), host(self.offsets)
+        r = host(self.rings)
+        r = r.reshape(-1).view(np.uint8).view(RING_DTYPE) if r.dtype != RING_DTYPE else r.reshape(-1)
+        return [r[o[i]:o[i] + c[i]].copy() if c[i] >= 0 else None for i in range(len(c))]
 
 
 class Detector:
@@ -49,32 +75,40 @@ class Detector:
     def frame_dtype(self):
         return torch.uint8 if self.pixel_bytes == 1 else torch.uint16
 
-    def alloc_outputs(self, n: int):
-        dev = torch.device("cuda", self.device)
-        rings = torch.empty((n, self.ring_cap, RING_DTYPE.itemsize), dtype=torch.uint8, device=dev)
-        counts = torch.empty((n,), dtype=torch.int32, device=dev)
-        return rings, counts
+    def default_capacity(self, n: int) -> int:
+        """Output capacity used when the caller gives none: every frame's peak capacity."""
+        return n * self.ring_cap
 
-    def detect(self, frames: torch.Tensor, rings: torch.Tensor | None = None, counts: torch.Tensor | None = None,
-               stream: torch.cuda.Stream | None = None):
+    def alloc_outputs(self, n: int, capacity: int | None = None) -> RingBatch:
+        dev = torch.device("cuda", self.device)
+        cap = self.default_capacity(n) if capacity is None else int(capacity)
+        return RingBatch(torch.empty((max(cap, 1), RING_DTYPE.itemsize), dtype=torch.uint8, device=dev),
+                         torch.empty((n,), dtype=torch.int32, device=dev),
+                         torch.empty((n + 1,), dtype=torch.int32, device=dev))
+
+    def detect(self, frames: torch.Tensor, out: RingBatch | None = None,
+               stream: torch.cuda.Stream | None = None) -> RingBatch:
         """frames: CUDA tensor [N, H, W] (uint8/uint16, row-contiguous).  Asynchronous on `stream`
-        (default: torch's current stream).  Returns (rings [N, cap, 64] uint8, counts [N] int32)."""
+        (default: torch's current stream).  Returns the RingBatch written (out, or a new one)."""
         if frames.dim() == 2:
             frames = frames.unsqueeze(0)
         n, H, W = frames.shape
         assert (H, W) == (self.height, self.width) and frames.dtype == self.frame_dtype and frames.is_cuda
         assert frames.stride(2) == 1
-        if rings is None or counts is None:
-            rings, counts = self.alloc_outputs(n)
+        if out is None:
+            out = self.alloc_outputs(n)
+        assert out.counts.numel() >= n and out.offsets.numel() >= n + 1
         st = stream if stream is not None else torch.cuda.current_stream(frames.device)
         es = frames.element_size()
         check(lib().rd_detect(self._h, frames.data_ptr(), frames.stride(1) * es, frames.stride(0) * es, n,
-                              rings.data_ptr(), counts.data_ptr(), C.c_void_p(st.cuda_stream)), "rd_detect")
-        return rings, counts
+                              out.rings.data_ptr(), out.rings.shape[0], out.counts.data_ptr(), out.offsets.data_ptr(),
+                              C.c_void_p(st.cuda_stream)), "rd_detect")
+        return out
 
-    def detect_host(self, frames, rings: np.ndarray | None = None, counts: np.ndarray | None = None):
+    def detect_host(self, frames, out: RingBatch | None = None, capacity: int | None = None) -> RingBatch:
         """End-to-end on host buffers (numpy or CPU torch tensor, pinned recommended): the library
-        copies frames in, detects and copies rings back, overlapping copies with compute."""
+        copies frames in, detects and returns the compacted rings, overlapping copies with compute.
+        Returns RingBatch of host arrays (rings as RING_DTYPE records)."""
         if isinstance(frames, torch.Tensor):
             assert not frames.is_cuda
             ptr, n = frames.data_ptr(), frames.shape[0]
@@ -85,16 +119,19 @@ class Detector:
                 frames = np.ascontiguousarray(frames)
             ptr, n = frames.ctypes.data, frames.shape[0]
             pitch, fstride = frames.strides[1], frames.strides[0]
-        if rings is None:
-            rings = np.empty((n, self.ring_cap), dtype=RING_DTYPE)
-        if counts is None:
-            counts = np.empty(n, dtype=np.int32)
-        rptr = rings.data_ptr() if isinstance(rings, torch.Tensor) else rings.ctypes.data
-        cptr = counts.data_ptr() if isinstance(counts, torch.Tensor) else counts.ctypes.data
-        st = lib().rd_detect_host(self._h, ptr, pitch, fstride, n, rptr, cptr)
+        if out is None:
+            cap = self.default_capacity(n) if capacity is None else int(capacity)
+            out = RingBatch(np.empty(max(cap, 1), dtype=RING_DTYPE), np.empty(n, dtype=np.int32),
+                            np.empty(n + 1, dtype=np.int32))
+
+        def ptr_of(x):
+            return x.data_ptr() if isinstance(x, torch.Tensor) else x.ctypes.data
+        cap = out.rings.shape[0]
+        st = lib().rd_detect_host(self._h, ptr, pitch, fstride, n, ptr_of(out.rings), cap, ptr_of(out.counts),
+                                  ptr_of(out.offsets))
         if st not in (_rd.RD_OK, _rd.RD_ERR_CAPACITY):
             check(st, "rd_detect_host")
-        return rings, counts
+        return out
 
     def sync(self, raise_on_overflow=True):
         st = lib().rd_sync(self._h)
@@ -103,9 +140,15 @@ class Detector:
         check(st, "rd_sync")
         return st
 
-    def overflow(self, n: int) -> np.ndarray:
+    def overflow(self) -> dict:
+        """rd_query_overflow of the last call: overflowed frames, OR of their bits, needed capacities."""
+        o = _rd.rd_overflow()
+        check(lib().rd_query_overflow(self._h, C.byref(o)), "rd_query_overflow")
+        return {name: getattr(o, name) for name, _ in _rd.rd_overflow._fields_}
+
+    def flags(self, n: int) -> np.ndarray:
         out = np.zeros(n, np.int32)
-        check(lib().rd_query_overflow(self._h, n, out.ctypes.data), "rd_query_overflow")
+        check(lib().rd_query_flags(self._h, n, out.ctypes.data), "rd_query_flags")
         return out
 
     def stats(self, n: int) -> np.ndarray:
@@ -113,13 +156,22 @@ class Detector:
         check(lib().rd_get_stats(self._h, n, out.ctypes.data), "rd_get_stats")
         return out
 
-    def dump_ridges(self, frame: int) -> np.ndarray:
+    def _dump(self, frame: int, what: int, dtype) -> np.ndarray:
         n = C.c_int64()
-        check(lib().rd_dump_ridges(self._h, frame, None, 0, C.byref(n)), "rd_dump_ridges")
-        out = np.zeros(n.value, RIDGE_DTYPE)
-        check(lib().rd_dump_ridges(self._h, frame, out.ctypes.data if n.value else None, n.value, C.byref(n)),
-              "rd_dump_ridges")
+        check(lib().rd_debug_dump(self._h, frame, what, None, 0, C.byref(n)), "rd_debug_dump")
+        out = np.zeros(n.value, dtype)
+        check(lib().rd_debug_dump(self._h, frame, what, out.ctypes.data if n.value else None, out.nbytes,
+                                  C.byref(n)), "rd_debug_dump")
         return out
+
+    def dump_ridges(self, frame: int) -> np.ndarray:
+        return self._dump(frame, _rd.RD_DUMP_RIDGES, RIDGE_DTYPE)
+
+    def dump_hotspots(self, frame: int) -> np.ndarray:
+        return self._dump(frame, _rd.RD_DUMP_HOTSPOTS, HOT_DTYPE)
+
+    def dump_level_fpr(self, frame: int) -> np.ndarray:
+        return self._dump(frame, _rd.RD_DUMP_LEVEL_FPR, FPR_DTYPE)
 
     def ring_members(self, frame: int) -> list[np.ndarray]:
         """Classification of frame `frame` of the last detect(): per ring (output order), the
@@ -134,29 +186,15 @@ class Detector:
         xy = np.stack([mem[: n.value] & 0xFFFF, mem[: n.value] >> 16], axis=1).astype(np.int32)
         return [xy[off[i]:off[i + 1]] for i in range(cnt)]
 
-    def dump_hotspots(self, frame: int) -> np.ndarray:
-        n = C.c_int64()
-        check(lib().rd_dump_hotspots(self._h, frame, None, 0, C.byref(n)), "rd_dump_hotspots")
-        out = np.zeros(n.value, HOT_DTYPE)
-        check(lib().rd_dump_hotspots(self._h, frame, out.ctypes.data if n.value else None, n.value, C.byref(n)),
-              "rd_dump_hotspots")
-        return out
-
     def set_timing(self, on: bool):
         check(lib().rd_set_timing(self._h, 1 if on else 0), "rd_set_timing")
 
     def kernel_times(self):
-        """(ms per kernel [K1 ridges, K1.5 rays, K2 hough, K3 fit] summed over timed calls, n_calls)."""
+        """(ms per kernel [K1 ridges, K1.5 rays, K2 hough, K3 fit + output] summed over timed calls, n_calls)."""
         ms = (C.c_float * 4)()
         n = C.c_int32()
         check(lib().rd_kernel_times(self._h, ms, C.byref(n)), "rd_kernel_times")
         return [ms[0], ms[1], ms[2], ms[3]], n.value
-
-    @staticmethod
-    def rings_to_numpy(rings: torch.Tensor, counts: torch.Tensor) -> list[np.ndarray]:
-        r = rings.cpu().numpy().reshape(rings.shape[0], -1).view(RING_DTYPE)
-        c = counts.cpu().numpy()
-        return [r[i, : c[i]].copy() if c[i] >= 0 else None for i in range(len(c))]
 
 
 def eigen(abc: torch.Tensor):

@@ -27,39 +27,59 @@ def shard(n_frames: int, world: int, rank: int) -> tuple[int, int]:
     return start, start + base + (1 if rank < extra else 0)
 
 
-def pack(rings: torch.Tensor, counts: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
-    """Compact a [n, cap, 64] uint8 ring buffer with per-frame counts into contiguous records
-    [total, 64] uint8 (frame order, canonical order within a frame) + counts (int64)."""
-    n, cap = rings.shape[0], rings.shape[1]
-    c = counts.to(torch.int64).clamp(min=0)
-    mask = torch.arange(cap, device=rings.device).unsqueeze(0) < c.unsqueeze(1)
-    return rings[mask].reshape(-1, REC), counts.to(torch.int64)
+def pack(rings: torch.Tensor, counts: torch.Tensor, offsets: torch.Tensor | None = None):
+    """Dense records of a detect call: (records [total, 64] uint8 in frame order, canonical order
+    within a frame; counts int64 with -1 for overflowed frames).  rings is either rd_detect's
+    compact buffer [capacity, 64] with its offsets, or a padded [n, cap, 64] buffer (offsets None)."""
+    c = counts.to(torch.int64)
+    valid = c.clamp(min=0)
+    if offsets is None:
+        n, cap = rings.shape[0], rings.shape[1]
+        mask = torch.arange(cap, device=rings.device).unsqueeze(0) < valid.unsqueeze(1)
+        return rings[mask].reshape(-1, REC), c
+    # compact: frames with count -1 may leave holes (output capacity); gather the valid ranges
+    o = offsets[:-1].to(torch.int64)
+    total = int(valid.sum())
+    if total == 0:
+        return torch.zeros((0, REC), dtype=torch.uint8, device=rings.device), c
+    frame = torch.repeat_interleave(torch.arange(len(c), device=rings.device), valid)
+    first = torch.cumsum(valid, 0) - valid
+    idx = o[frame] + (torch.arange(total, device=rings.device) - first[frame])
+    return rings.reshape(-1, REC)[idx], c
 
 
-def gather_rings(rings: torch.Tensor, counts: torch.Tensor, dst: int = 0, group=None):
-    """Gather every rank's rings to `dst`.  Returns, on dst, (records [N_total, 64] uint8 in
-    rank order, counts [n_frames_total] int64 with -1 for overflowed frames); None elsewhere."""
+def gather_rings(rings: torch.Tensor, counts: torch.Tensor, offsets: torch.Tensor | None = None, dst: int = 0,
+                 group=None):
+    """Gather every rank's rings to `dst`: an all_gather of the per-rank sizes,
+    then one gather to dst of the records padded to the largest rank (only dst receives P
+    buffers).  Returns, on dst, (records [N_total, 64] uint8 in rank order, counts
+    [n_frames_total] int64 with -1 for overflowed frames); None elsewhere."""
+    return gather_records(*pack(rings, counts, offsets), dst=dst, group=group)
+
+
+def gather_records(recs: torch.Tensor, cnt: torch.Tensor, dst: int = 0, group=None):
+    """gather_rings on already packed records ([total, 64] uint8, int64 counts per frame)."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    recs, cnt = pack(rings, counts)
     dev = recs.device
     sizes = torch.tensor([recs.shape[0], cnt.shape[0]], dtype=torch.int64, device=dev)
     all_sizes = [torch.zeros_like(sizes) for _ in range(world)]
     dist.all_gather(all_sizes, sizes, group=group)
     max_r = max(int(s[0]) for s in all_sizes)
     max_f = max(int(s[1]) for s in all_sizes)
-    pr = torch.zeros((max(max_r, 1), REC), dtype=torch.uint8, device=dev)
-    pr[: recs.shape[0]] = recs
-    pc = torch.full((max(max_f, 1),), -2, dtype=torch.int64, device=dev)
-    pc[: cnt.shape[0]] = cnt
-    gr = [torch.empty_like(pr) for _ in range(world)]
-    gc = [torch.empty_like(pc) for _ in range(world)]
-    dist.all_gather(gr, pr, group=group)
-    dist.all_gather(gc, pc, group=group)
+    # one buffer per rank: frame counts (int64) then the records, as bytes
+    cb = max(max_f, 1) * 8
+    buf = torch.zeros(cb + max(max_r, 1) * REC, dtype=torch.uint8, device=dev)
+    cpad = torch.full((max(max_f, 1),), -2, dtype=torch.int64, device=dev)
+    cpad[: cnt.shape[0]] = cnt
+    buf[:cb] = cpad.view(torch.uint8)
+    buf[cb:cb + recs.numel()] = recs.reshape(-1)
+    gl = [torch.empty_like(buf) for _ in range(world)] if rank == dst else None
+    dist.gather(buf, gl, dst=dst, group=group)
     if rank != dst:
         return None
-    out_r = torch.cat([gr[i][: int(all_sizes[i][0])] for i in range(world)])
-    out_c = torch.cat([gc[i][: int(all_sizes[i][1])] for i in range(world)])
+    out_r = torch.cat([gl[i][cb:cb + int(all_sizes[i][0]) * REC].reshape(-1, REC) for i in range(world)])
+    out_c = torch.cat([gl[i][:cb].view(torch.int64)[: int(all_sizes[i][1])] for i in range(world)])
     return out_r, out_c
 
 
@@ -76,5 +96,5 @@ def unpack(records: torch.Tensor, counts: torch.Tensor) -> list:
     return out
 
 
-__all__ = ["shard", "pack", "gather_rings", "unpack", "REC"]
+__all__ = ["shard", "pack", "gather_rings", "gather_records", "unpack", "REC"]
 _ = np  # numpy is used through RING_DTYPE views

@@ -17,7 +17,7 @@ import numpy as np
 import torch
 
 from ._rd import RING_DTYPE
-from .detector import Detector
+from .detector import Detector, RingBatch
 
 
 class StreamDetector:
@@ -28,8 +28,9 @@ class StreamDetector:
         dt = torch.uint8 if int(params["pixel_bytes"]) == 1 else torch.uint16
         self.slots = slots
         self.frames = torch.empty((slots, H, W), dtype=dt).pin_memory()
-        self.rings = np.empty((slots, self.det.ring_cap), dtype=RING_DTYPE)
-        self.counts = np.empty(slots, dtype=np.int32)
+        cap = max_batch * self.det.ring_cap   # one batch's compact output, reused
+        self.out = RingBatch(np.empty(cap, dtype=RING_DTYPE), np.empty(max_batch, dtype=np.int32),
+                             np.empty(max_batch + 1, dtype=np.int32))
         self.t_capture = np.zeros(slots)
         self._written = 0        # frames captured so far
         self._done = 0           # frames detected so far
@@ -66,12 +67,12 @@ class StreamDetector:
                 first, avail = self._done, self._written - self._done
             i0 = first % self.slots
             n = min(avail, self.max_batch, self.slots - i0)   # contiguous in the ring
-            self.det.detect_host(self.frames[i0:i0 + n], self.rings[i0:i0 + n], self.counts[i0:i0 + n])
+            out = self.det.detect_host(self.frames[i0:i0 + n], self.out)
             t = time.perf_counter()
             if on_result is not None:
                 for k in range(n):
-                    c = int(self.counts[i0 + k])
-                    on_result(first + k, self.rings[i0 + k, :max(c, 0)], t - self.t_capture[i0 + k])
+                    c, o = int(out.counts[k]), int(out.offsets[k])
+                    on_result(first + k, out.rings[o:o + max(c, 0)].copy(), t - self.t_capture[i0 + k])
             with self._cv:
                 self._done += n
                 self._cv.notify_all()

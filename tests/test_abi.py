@@ -34,7 +34,7 @@ def test_exports_match_header(rdlib):
 
 def test_status_strings_and_version(rdlib):
     L = rdlib.lib()
-    assert L.rd_abi_version() == 2
+    assert L.rd_abi_version() == 3
     for s in range(7):
         assert len(L.rd_status_string(s)) > 0
 
@@ -47,7 +47,7 @@ def test_config_init_defaults(rdlib):
 
 
 @pytest.mark.parametrize("bad,status", [
-    (dict(width=4), 2), (dict(smoothing_sigma=0.0), 1), (dict(smoothing_sigma=6.0), 1),
+    (dict(width=4), 2), (dict(smoothing_sigma=0.0), 1), (dict(smoothing_sigma=6.0), 1), (dict(smoothing_sigma=4.34), 1),
     (dict(curvature_threshold=0.5), 1), (dict(r_min=1), 1), (dict(r_max=5, r_min=9), 1),
     (dict(vote_threshold_raw=0), 1), (dict(vote_threshold_norm=0.0), 1), (dict(sig_den=0), 1),
     (dict(annulus_halfwidth=-1), 1), (dict(max_value=70000), 1)])
@@ -63,8 +63,11 @@ def test_create_rejects_invalid_config_without_gpu(rdlib, bad, status):
 def test_null_arguments(rdlib):
     L = rdlib.lib()
     assert L.rd_create(None, 1, 0, None) == rdlib.RD_ERR_PARAM
-    assert L.rd_detect(None, None, 0, 0, 1, None, None, None) == rdlib.RD_ERR_PARAM
+    assert L.rd_detect(None, None, 0, 0, 1, None, 0, None, None, None) == rdlib.RD_ERR_PARAM
+    assert L.rd_detect_host(None, None, 0, 0, 1, None, 0, None, None) == rdlib.RD_ERR_PARAM
     assert L.rd_sync(None) == rdlib.RD_ERR_PARAM
+    assert L.rd_query_overflow(None, None) == rdlib.RD_ERR_PARAM
+    assert L.rd_debug_dump(None, 0, 0, None, 0, None) == rdlib.RD_ERR_PARAM
     assert L.rd_destroy(None) == rdlib.RD_OK
 
 

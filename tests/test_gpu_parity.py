@@ -53,9 +53,9 @@ def _compare_rings(got, exp):
 def _run(rdmod, params, frames, debug=1, **extra):
     det = _det(rdmod, params, max_batch=len(frames), debug=debug, **extra)
     dev = torch.from_numpy(np.ascontiguousarray(frames)).cuda()
-    rings, counts = det.detect(dev)
+    out = det.detect(dev).to_numpy()
     det.sync()
-    return det, det.rings_to_numpy(rings, counts)
+    return det, out
 
 
 def _check_frame(rdmod, det, i, params, frame, rings_gpu, full=True):
@@ -68,6 +68,18 @@ def _check_frame(rdmod, det, i, params, frame, rings_gpu, full=True):
     if full:
         assert _ridge_set(det.dump_ridges(i)) == _ridge_set(rid)
         assert _hot_set(det.dump_hotspots(i)) == _hot_set(hot)
+
+
+def _check_batch(det, params, frames, out, n_threads=0):
+    """Every frame of a batch against the oracle (rings bit-exact / fits within FIT_TOL, and
+    the per-frame counters), computed by the oracle's host thread pool."""
+    exp, est = oracle.detect_batch(oracle.params(**params), frames, nthreads=n_threads)
+    gst = det.stats(len(frames))
+    for i in range(len(frames)):
+        assert out[i] is not None, i
+        _compare_rings(out[i], exp[i])
+        for k in ("ridges", "votes", "hotspots", "peaks"):
+            assert gst[k][i] == est[k][i], (i, k)
 
 
 # ---------------------------------------------------------------- A3 recipe
@@ -186,16 +198,62 @@ def test_random_small_frames(rdmod):
 
 # ---------------------------------------------------------------- capacities fail loudly
 def test_capacity_overflow_reported(rdmod):
+    """Every capacity overflow is reported (count -1, flag bit, rd_sync error), and
+    rd_query_overflow returns capacities that suffice: a detector recreated with them
+    reproduces the oracle's rings (rd.h rd_overflow)."""
     params = synth.preset(2)
     frames = synth.batch(2, 0, 0, 2)
-    for extra, bit in ((dict(max_rings_per_frame=2), 8), (dict(max_ridges_per_tile=2), 1),
-                       (dict(max_entries_per_tile=16), 2), (dict(max_hotspots_per_level=1), 4)):
+    dev = torch.from_numpy(frames).cuda()
+    p = oracle.params(**params)
+    exp = [oracle.detect(p, f)[0] for f in frames]
+    for extra, bit, key, cfg_key in (
+            (dict(max_rings_per_frame=2), 8, "needed_rings_per_frame", "max_rings_per_frame"),
+            (dict(max_ridges_per_tile=2), 1, "needed_ridges_per_tile", "max_ridges_per_tile"),
+            (dict(max_entries_per_tile=16), 2, "needed_entries_per_tile", "max_entries_per_tile"),
+            (dict(max_hotspots_per_level=1), 4, "needed_hotspots_per_level", "max_hotspots_per_level")):
         det = _det(rdmod, params, max_batch=2, **extra)
-        rings, counts = det.detect(torch.from_numpy(frames).cuda())
+        out = det.detect(dev)
         with pytest.raises(rdmod.RDError):
             det.sync()
-        fl = det.overflow(2)
-        assert np.all(fl & bit) and np.all(counts.cpu().numpy() == -1)
+        assert np.all(det.flags(2) & bit) and np.all(out.counts.cpu().numpy() == -1)
+        ov = det.overflow()
+        assert ov["frames_overflowed"] == 2 and ov["flags"] & bit
+        assert ov[key] > extra[cfg_key]
+        det2 = _det(rdmod, params, max_batch=2, **{cfg_key: ov[key]})
+        got = det2.detect(dev).to_numpy()
+        det2.sync()
+        assert det2.overflow()["frames_overflowed"] == 0
+        for g, e in zip(got, exp):
+            _compare_rings(g, e)
+
+
+def test_output_capacity_and_offsets(rdmod):
+    """Compact output (rd_detect's ring_capacity_total / offsets): frames are back to back;
+    a capacity one ring short of the total fails exactly the last frame with OVF_OUTPUT, and
+    rd_query_overflow reports the total needed; the host path behaves the same."""
+    params = synth.preset(2)
+    frames = synth.batch(2, 0, 3, 4)
+    det = _det(rdmod, params, max_batch=4)
+    full = det.detect(torch.from_numpy(frames).cuda())
+    det.sync()
+    counts, offsets = full.counts.cpu().numpy(), full.offsets.cpu().numpy()
+    total = int(offsets[-1])
+    assert offsets[0] == 0 and np.array_equal(np.diff(offsets), counts) and total == counts.sum() > 0
+    assert det.overflow()["needed_rings_total"] == total
+    short = det.detect(torch.from_numpy(frames).cuda(), det.alloc_outputs(4, capacity=total - 1))
+    assert det.sync(raise_on_overflow=False) == rdmod._rd.RD_ERR_CAPACITY
+    c2 = short.counts.cpu().numpy()
+    assert np.array_equal(c2[:3], counts[:3]) and c2[3] == -1
+    assert det.flags(4)[3] & 32 and det.overflow()["needed_rings_total"] == total
+    a, b = full.to_numpy(), short.to_numpy()
+    for i in range(3):
+        assert a[i].tobytes() == b[i].tobytes()
+    hb = det.detect_host(frames, capacity=total - 1)
+    assert np.array_equal(hb.counts[:3], counts[:3]) and hb.counts[3] == -1
+    ov = det.overflow()
+    assert ov["needed_rings_total"] == total and ov["frames_overflowed"] == 1 and ov["flags"] & 32
+    hb = det.detect_host(frames, capacity=total)
+    assert np.array_equal(hb.counts, counts) and np.array_equal(hb.offsets, offsets)
 
 
 def test_invalid_config_rejected(rdmod):
@@ -208,21 +266,18 @@ def test_invalid_config_rejected(rdmod):
 
 # ---------------------------------------------------------------- full size, bench launch configuration
 def test_full_batch_cfg3_bench_config(rdmod):
-    """cfg3 at BASELINE size (256 frames, the bench step): sampled frames vs the oracle,
-    all frames checked for canonical order, range and determinism."""
+    """cfg3 at BASELINE size (256 frames, the bench step, same launch configuration): every
+    frame vs the oracle; canonical order, range and determinism."""
     params = synth.preset(3)
     frames = synth.batch(3, 0, 0, 256)
     det = _det(rdmod, params, max_batch=256)
     dev = torch.from_numpy(frames).cuda()
-    rings, counts = det.detect(dev)
+    out = det.detect(dev).to_numpy()
     det.sync()
-    out = det.rings_to_numpy(rings, counts)
-    rings2, counts2 = det.detect(dev)
+    out2 = det.detect(dev).to_numpy()
     det.sync()
-    out2 = det.rings_to_numpy(rings2, counts2)
     assert all(a.tobytes() == b.tobytes() for a, b in zip(out, out2))  # deterministic
-    for i in (0, 97, 255):
-        _check_frame(rdmod, det, i, params, frames[i], out[i], full=False)
+    _check_batch(det, params, frames, out)   # all 256 frames of the bench step
     for g in out:
         assert g is not None and len(g) > 20
         key = list(zip(g["r"], g["cy"], g["cx"]))
@@ -237,14 +292,16 @@ def test_detect_host_matches_device(rdmod):
     params = synth.preset(3)
     frames = synth.batch(3, 0, 300, 70)
     det = _det(rdmod, params, max_batch=70)
-    rings, counts = det.detect(torch.from_numpy(frames).cuda())
+    dev_out = det.detect(torch.from_numpy(frames).cuda()).to_numpy()
     det.sync()
-    dev_out = det.rings_to_numpy(rings, counts)
     pinned = torch.from_numpy(frames).pin_memory()
-    hr, hc = det.detect_host(pinned)
+    hb = det.detect_host(pinned)
+    host_out = hb.to_numpy()
     for i in range(70):
-        assert hc[i] == len(dev_out[i])
-        assert hr[i, : hc[i]].tobytes() == dev_out[i].tobytes()
+        assert hb.counts[i] == len(dev_out[i])
+        assert host_out[i].tobytes() == dev_out[i].tobytes()
+    # compact output: the rings of all frames back to back, nothing else read back
+    assert hb.offsets[0] == 0 and np.array_equal(np.diff(hb.offsets), hb.counts)
 
 
 @pytest.mark.parametrize("force_redo", [False, True])
@@ -260,13 +317,12 @@ def test_detect_host_many_chunks_two_slots(rdmod, force_redo, monkeypatch):
     det = _det(rdmod, params, max_batch=8)
     ref = []
     for i in range(0, 37, 8):
-        rings, counts = det.detect(torch.from_numpy(frames[i:i + 8]).cuda())
+        ref += det.detect(torch.from_numpy(frames[i:i + 8]).cuda()).to_numpy()
         det.sync()
-        ref += det.rings_to_numpy(rings, counts)
-    hr, hc = det.detect_host(torch.from_numpy(frames).pin_memory())
+    host_out = det.detect_host(torch.from_numpy(frames).pin_memory()).to_numpy()
     for i in range(37):
-        assert hc[i] == len(ref[i]) and hc[i] > 0
-        assert hr[i, : hc[i]].tobytes() == ref[i].tobytes()
+        assert len(host_out[i]) == len(ref[i]) > 0
+        assert host_out[i].tobytes() == ref[i].tobytes()
 
 
 @pytest.mark.parametrize("cfg", [2, 3])
@@ -277,9 +333,8 @@ def test_ring_members_match_annulus_definition(rdmod, cfg):
     params = synth.preset(cfg)
     frames = synth.batch(cfg, 0, 7, 2)
     det = _det(rdmod, params, max_batch=2)
-    rings, counts = det.detect(torch.from_numpy(frames).cuda())
+    out = det.detect(torch.from_numpy(frames).cuda()).to_numpy()
     det.sync()
-    out = det.rings_to_numpy(rings, counts)
     p = oracle.params(**params)
     for i in range(2):
         R = oracle.ridges(p, frames[i])
@@ -306,30 +361,26 @@ def test_rings_independent_of_hough_tiling(rdmod, env, monkeypatch):
     params = synth.preset(3)
     frames = torch.from_numpy(synth.batch(3, 0, 60, 6)).cuda()
     det = _det(rdmod, params, max_batch=6)
-    rings, counts = det.detect(frames)
+    ref = det.detect(frames).to_numpy()
     det.sync()
-    ref = det.rings_to_numpy(rings, counts)
     monkeypatch.setenv(*env)
     det2 = _det(rdmod, params, max_batch=6)
-    rings2, counts2 = det2.detect(frames)
+    out = det2.detect(frames).to_numpy()
     det2.sync()
-    out = det2.rings_to_numpy(rings2, counts2)
     for a, b in zip(ref, out):
         assert len(a) > 20 and a.tobytes() == b.tobytes()
 
 
 def test_full_batch_cfg4_dense(rdmod):
-    """cfg4 at BASELINE size (512 frames of 1024x1024, 200 rings): sampled frames vs the
-    oracle; every frame valid (no capacity overflow with the dense-config capacities)."""
+    """cfg4 at BASELINE size (512 frames of 1024x1024, 200 rings): every frame vs the oracle
+    (no capacity overflow with the dense-config capacities)."""
     params = dict(synth.preset(4), max_entries_per_tile=6144, max_hotspots_per_level=512)
     frames = synth.batch(4, 0, 0, 512)
     det = _det(rdmod, params, max_batch=512)
-    rings, counts = det.detect(torch.from_numpy(frames).cuda())
+    out = det.detect(torch.from_numpy(frames).cuda()).to_numpy()
     det.sync()
-    out = det.rings_to_numpy(rings, counts)
     assert all(g is not None and len(g) > 100 for g in out)
-    for i in (0, 511):
-        _check_frame(rdmod, det, i, params, frames[i], out[i], full=False)
+    _check_batch(det, params, frames, out)
 
 
 def test_cfg5_high_frame_indices(rdmod):
@@ -339,11 +390,9 @@ def test_cfg5_high_frame_indices(rdmod):
     frames = synth.batch(5, 0, 8192 - 256, 256)
     assert np.array_equal(frames[-1], synth.frame(3, 0, 8191)[0])
     det = _det(rdmod, params, max_batch=256)
-    rings, counts = det.detect(torch.from_numpy(frames).cuda())
+    out = det.detect(torch.from_numpy(frames).cuda()).to_numpy()
     det.sync()
-    out = det.rings_to_numpy(rings, counts)
-    for i in (0, 255):
-        _check_frame(rdmod, det, i, params, frames[i], out[i], full=False)
+    _check_batch(det, params, frames, out)
 
 
 def test_detect_host_pitched_frames(rdmod):
@@ -353,10 +402,10 @@ def test_detect_host_pitched_frames(rdmod):
     padded = np.zeros((5, 480, 704), np.uint8)
     padded[:, :, :640] = frames
     det = _det(rdmod, params, max_batch=3)
-    hr, hc = det.detect_host(padded[:, :, :640])
+    out = det.detect_host(padded[:, :, :640]).to_numpy()
     p = oracle.params(**params)
     for i in range(5):
-        _compare_rings(hr[i, : hc[i]], oracle.detect(p, frames[i])[0])
+        _compare_rings(out[i], oracle.detect(p, frames[i])[0])
 
 
 # ---------------------------------------------------------------- K2 counter width
@@ -436,3 +485,68 @@ def test_stream_detector_matches_batch(rdmod):
     sd.close()
     cons.join()
     assert seen == list(range(40))
+
+
+# ---------------------------------------------------------------- T3: level fingerprints
+@pytest.mark.parametrize("cfg,idx", [(2, 0), (3, 5)])
+def test_level_fingerprints_match_oracle_accumulator(rdmod, cfg, idx):
+    """RD_DUMP_LEVEL_FPR: per level r, sum raw, sum raw^2 and sum raw*(yW+x)
+    over every voxel of the frame's raw accumulator equal the oracle's full (N_r x H x W) array
+    built from its own ridges (votes populate the levels)."""
+    params = synth.preset(cfg)
+    frames = synth.batch(cfg, 0, idx, 2)
+    det, _ = _run(rdmod, params, frames)
+    p = oracle.params(**params)
+    W = params["width"]
+    for i in range(2):
+        raw, nv = oracle.votes(p, oracle.ridges(p, frames[i]))
+        raw = raw.astype(np.int64).reshape(raw.shape[0], -1)
+        pos = np.arange(raw.shape[1], dtype=np.uint64)
+        fpr = det.dump_level_fpr(i)
+        assert len(fpr) == raw.shape[0] and np.array_equal(fpr["r"], np.arange(p.r_min - 1, p.r_max + 2))
+        assert np.array_equal(fpr["votes"], raw.sum(axis=1)) and int(fpr["votes"].sum()) == nv
+        assert np.array_equal(fpr["sq"], (raw * raw).sum(axis=1))
+        got_pos = fpr["pos"].astype(np.uint64)
+        exp_pos = np.array([int((raw[l].astype(np.uint64) * pos).sum(dtype=np.uint64)) for l in range(raw.shape[0])],
+                           dtype=np.uint64)
+        assert np.array_equal(got_pos, exp_pos)
+        assert W > 0
+
+
+# ---------------------------------------------------------------- parameter extremes
+@pytest.mark.parametrize("r_min,r_max", [(60, 100), (80, 150)])
+def test_large_radius_wide_windows(rdmod, r_min, r_max):
+    """r_max >= 95 gives K_r = ceil(3 sigma(r)) >= 16: window sums of 2K + 1 > 32 rows, so
+    the 16-bit K2 pass sums several rows per lane (sigma(r) grows with r)."""
+    W = H = 384
+    params = dict(width=W, height=H, pixel_bytes=2, max_value=4095, smoothing_sigma=1.5,
+                  curvature_threshold=-10.0, r_min=r_min, r_max=r_max, vote_threshold_raw=3,
+                  vote_threshold_norm=0.5, sig_a=1, sig_b=5, sig_den=20, annulus_halfwidth=0)
+    sc = synth.scene(W, H, pixel_bytes=2, max_value=4095, background=100, sigma_p=1.5, read_sigma=8, poisson=1)
+    rng = np.random.default_rng(r_max)
+    fr = []
+    for k in range(3):
+        rings = [(rng.uniform(r_max * 0.6, W - r_max * 0.6), rng.uniform(r_max * 0.6, H - r_max * 0.6),
+                  rng.uniform(r_min + 2, r_max - 2), rng.uniform(800, 3000)) for _ in range(3)]
+        fr.append(synth.render(sc, synth.make_rings(rings), noise_key=1000 + k))
+    frames = np.stack(fr)
+    det, rings = _run(rdmod, params, frames)
+    Kmax = -(-3 * (r_max + 1 + 5) // 20)
+    assert Kmax >= 16
+    for i in range(3):
+        assert len(rings[i]) >= 1
+        _check_frame(rdmod, det, i, params, frames[i], rings[i])
+
+
+def test_largest_smoothing_scale(rdmod):
+    """sigma_s = 4.3 (K_s = 13, the largest the K1 halo takes): parity on small frames."""
+    W, H = 200, 150
+    params = dict(width=W, height=H, pixel_bytes=2, max_value=4095, smoothing_sigma=4.3,
+                  curvature_threshold=-0.5, r_min=8, r_max=50, vote_threshold_raw=3,
+                  vote_threshold_norm=0.3, sig_a=1, sig_b=5, sig_den=20, annulus_halfwidth=0)
+    sc = synth.scene(W, H, pixel_bytes=2, max_value=4095, background=100, sigma_p=4.0, read_sigma=4)
+    frames = np.stack([synth.render(sc, synth.make_rings([(70, 70, 35, 2500), (140, 80, 25, 2500)]), noise_key=k)
+                       for k in range(2)])
+    det, rings = _run(rdmod, params, frames)
+    for i in range(2):
+        _check_frame(rdmod, det, i, params, frames[i], rings[i])

@@ -67,8 +67,25 @@ def build_rd(force=False):
     return out
 
 
+def build_san(force=False):
+    """tools/sanitize/rd_san: a C driver of librd.so for compute-sanitizer runs (tests/test_sanitizers.py)."""
+    d = os.path.join(ROOT, "tools", "sanitize")
+    out = os.path.join(d, "rd_san")
+    src = os.path.join(d, "rd_san.c")
+    pkg = os.path.join(ROOT, "paper_1310_1371_b200")
+    deps = [src, os.path.join(ROOT, "include", "rd.h"), os.path.join(pkg, "librd.so"),
+            os.path.join(ROOT, "synth", "libsynth.so")]
+    if force or _stale(out, deps):
+        cuda = os.path.dirname(os.path.dirname(NVCC))
+        _run(["gcc", "-O2", "-Wall", "-o", out, src, "-I", os.path.join(ROOT, "include"), "-I",
+              os.path.join(cuda, "include"), "-L", pkg, "-lrd", "-L", os.path.join(ROOT, "synth"), "-lsynth",
+              "-L", os.path.join(cuda, "lib64"), "-lcudart", f"-Wl,-rpath,{pkg}", f"-Wl,-rpath,{ROOT}/synth",
+              "-Wl,-rpath,$ORIGIN/../../paper_1310_1371_b200", "-Wl,-rpath,$ORIGIN/../../synth"])
+    return out
+
+
 def build_all(force=False):
-    return [build_synth(force), build_oracle(force), build_rd(force)]
+    return [build_synth(force), build_oracle(force), build_rd(force), build_san(force)]
 
 
 if __name__ == "__main__":

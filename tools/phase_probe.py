@@ -21,9 +21,9 @@ if os.environ.get("PROBE_HOT_CAP"):
 frames = torch.from_numpy(synth.batch(cfg, 0, 0, B)).cuda()
 det = rd.Detector(params, max_batch=B)
 for _ in range(2):
-    rings, counts = det.detect(frames)
+    det.detect(frames)
 st = det.sync(raise_on_overflow=False)
-ovf = det.overflow(B)
+ovf = det.flags(B)
 det.set_timing(True)
 for _ in range(3):
     det.detect(frames)

@@ -15,6 +15,6 @@ params = synth.preset(cfg)
 frames = torch.from_numpy(synth.batch(cfg, 0, 0, B)).cuda()
 det = rd.Detector(params, max_batch=B)
 for _ in range(calls):
-    rings, counts = det.detect(frames)
+    out = det.detect(frames)
 det.sync()
-print("ok", int(counts.sum()))
+print("ok", int(out.counts.sum()))

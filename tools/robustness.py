@@ -24,13 +24,13 @@ res = {"corpus": dict(frames=n, size=f"{robust.WIDTH}x{robust.HEIGHT} uint16", s
 for name, params in (("ridges", robust.PARAMS), ("edges", dict(robust.PARAMS, feature=1, edge_threshold=40.0))):
     det = rd.Detector(dict(params, max_entries_per_tile=4096), max_batch=n)
     dev = torch.from_numpy(frames).cuda()
-    rings, counts = det.detect(dev)
+    out = det.detect(dev)
     det.sync()
     t0 = time.perf_counter()
-    rings, counts = det.detect(dev, rings, counts)
+    det.detect(dev, out)
     det.sync()
     dt = time.perf_counter() - t0
-    got = det.rings_to_numpy(rings, counts)
+    got = out.to_numpy()
     rates, cnt = robust.score(truth, got)
     # parity on the first frames
     k = min(n, 16)

@@ -21,9 +21,8 @@ import synth  # noqa: E402
 params = synth.preset(3)
 src = synth.batch(3, 0, 0, 64)
 ref_det = rd.Detector(params, max_batch=64)
-ref, refc = ref_det.detect(torch.from_numpy(src).cuda())
+ref = ref_det.detect(torch.from_numpy(src).cuda()).to_numpy()
 ref_det.sync()
-ref = ref_det.rings_to_numpy(ref, refc)
 out = {"workload": "cfg3 frames 1024x688 uint16, 64 distinct frames cycled", "runs": []}
 for rate, seconds in ((70, 2.0), (1000, 1.0), (5000, 1.0), (0, 1.0)):
     sd = StreamDetector(params, slots=512, max_batch=64)
