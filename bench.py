@@ -27,7 +27,6 @@ box's host cores over a bounded sample of the same workload.
 from __future__ import annotations
 
 import argparse
-import hashlib
 import json
 import math
 import os
@@ -390,7 +389,7 @@ def run_sweep(args):
     gathered to rank 0.  A step = the whole sweep (strong scaling)."""
     torch, dist, rank, local, world, dev = _init_dist(args)
     import paper_1310_1371_b200 as rd
-    from paper_1310_1371_b200.distributed import gather_records, shard, unpack
+    from paper_1310_1371_b200.distributed import collect, digest, shard, unpack
     import synth
 
     N, B = args.frames, args.batch
@@ -412,12 +411,8 @@ def run_sweep(args):
             det.detect(frames_d[k * B:(k + 1) * B], outs[k], stream)
 
     def gather():
-        # pack this rank's batches, then one gather to rank 0
-        from paper_1310_1371_b200.distributed import pack
-        recs, cnts = zip(*[pack(o.rings, o.counts, o.offsets) for o in outs]) if outs else ((), ())
-        r = torch.cat(recs) if recs else torch.zeros((0, 64), dtype=torch.uint8, device=dev)
-        c = torch.cat(cnts) if cnts else torch.zeros(0, dtype=torch.int64, device=dev)
-        return gather_records(r.reshape(-1, 64), c) if world > 1 else None
+        # this rank's batches, packed, one gather to rank 0 (paper_1310_1371_b200.distributed.collect)
+        return collect([(o.rings, o.counts, o.offsets) for o in outs])
 
     for _ in range(args.warmup):
         sweep()
@@ -444,14 +439,11 @@ def run_sweep(args):
     torch.cuda.synchronize(dev)
     gms = _max_over_ranks(torch, dist, world, dev, (time.perf_counter() - g0) * 1e3)
     if rank != 0:
-        dist.destroy_process_group() if world > 1 else None
+        if world > 1:
+            dist.destroy_process_group()
         return 0
-    if res is None:   # world == 1: the local lists are the gathered ones
-        from paper_1310_1371_b200.distributed import pack
-        recs, cnts = zip(*[pack(o.rings, o.counts, o.offsets) for o in outs])
-        res = (torch.cat(recs), torch.cat(cnts))
     recs, cnts = res
-    digest = hashlib.sha256(recs.cpu().numpy().tobytes() + cnts.cpu().numpy().tobytes()).hexdigest()
+    sha = digest(recs, cnts)
     lists = unpack(recs, cnts)
     parity = None
     if args.parity != "none":
@@ -476,7 +468,7 @@ def run_sweep(args):
                        "parallelism": f"frame-sharded x{world}, gather to rank 0"},
             "compute_plus_gather": {"value": round(N / ((sweep_ms + gms) / 1e3), 1), "gather_ms": round(gms, 3),
                                     "records": int(recs.shape[0])},
-            "gathered_sha256": digest, "parity": parity, "clocks": clocks,
+            "gathered_sha256": sha, "parity": parity, "clocks": clocks,
             "gpu_launches": (6 * 2 + 2) * nb * args.steps}
     print(json.dumps(line), flush=True)
     if world > 1:

@@ -47,6 +47,7 @@ __global__ void __launch_bounds__(K3_THREADS) k_fit(Params P) {
       const Peak b = sp[j];
       rank += (b.r < a.r) || (b.r == a.r && (b.y < a.y || (b.y == a.y && b.x < a.x)));
     }
+    RD_CHECK(rank < npk, CK_K3_ORDER);
     order[rank] = i;
   }
   __syncthreads();
@@ -64,6 +65,7 @@ __global__ void __launch_bounds__(K3_THREADS) k_fit(Params P) {
       for (int bx = bx0; bx <= bx1; ++bx) {
         const int64_t b = fbins + by * P.nbx + bx;
         const int cnt = P.bin_count[b];
+        RD_CHECK(cnt >= 0 && cnt <= P.ridge_cap && bx < P.nbx && by < P.nby, CK_K3_BIN);
         const uint32_t* xy = P.bin_xy + b * P.ridge_cap;
         for (int k = lane; k < cnt; k += 32) {
           uint32_t v = xy[k];
@@ -286,6 +288,7 @@ __global__ void __launch_bounds__(128) k_copy(Params P, Ring* __restrict__ out, 
                                               const int* __restrict__ offsets) {
   const int f = blockIdx.x, n = counts[f];
   if (n <= 0) return;
+  RD_CHECK(n <= P.ring_cap, CK_EMIT);
   const uint4* src = reinterpret_cast<const uint4*>(P.rings + (int64_t)f * P.ring_cap);
   uint4* dst = reinterpret_cast<uint4*>(out + offsets[f]);
   for (int i = threadIdx.x; i < 4 * n; i += blockDim.x) dst[i] = src[i];

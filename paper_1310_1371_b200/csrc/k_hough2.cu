@@ -230,6 +230,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
         int base = 0;
         if (lane == 0) base = atomicAdd(&s_nact[p], __popc(bal));
         base = __shfl_sync(FULL, base, 0);
+        RD_CHECK(!a || base + __popc(bal & lanemask_lt()) < ecap, CK_K2_LIST);
         if (a) act[base + __popc(bal & lanemask_lt())] = (uint16_t)e;
       }
     };
@@ -254,6 +255,9 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
         s_ncand[0] = 0;
         s_ndef[par] = 0;
       }
+#ifdef RD_CHECKED
+      if (P.jitter) __nanosleep(((unsigned)(warp * 2654435761u + step * 40503u + blockIdx.x * 97u) >> 7) & 2047u);
+#endif
       // ---------------- (1) votes of levels L0..Lhi
       {
         const int nact = s_nact[par];
@@ -279,6 +283,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
               uint32_t rr, xy;
               double2 d;
               const int e = act[i];
+              RD_CHECK(e >= 0 && e < ne, CK_K2_RAY);
               if (e < rcap) {
                 d = sd[e];
                 xy = sxy[e];
@@ -315,6 +320,11 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
               addr[g] = ok ? (bc & ~3u) : dummy;
             }
   #pragma unroll
+            for (int g = 0; g < GL; ++g)
+              RD_CHECK(sh[g] == 32u ? addr[g] == dummy : (addr[g] - raw_base >= (uint32_t)(g * lvlc * CB) &&
+                                                          addr[g] - raw_base < (uint32_t)((g + 1) * lvlc * CB)),
+                       CK_K2_VOTE);
+  #pragma unroll
             for (int g = 0; g < GL; ++g) old[g] = atom_add_shared(addr[g], shl_clamp(1u, sh[g]));
             uint32_t omax = 0;
   #pragma unroll
@@ -327,12 +337,14 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
                 const int ix = cx - (hal - 1), iy = cy - (hal - 1);
                 if ((unsigned)ix >= (unsigned)(TX + 2) || (unsigned)iy >= (unsigned)(TY + 2)) continue;   // not in the ring
                 const int li = L0 + g;
+                RD_CHECK(li < nlev && iy < TY + 2 && ix < TX + 2 && ix < 256, CK_K2_LIST);
                 const int h = atomicAdd(&hcnt[li], 1);
                 if (h < hot_cap) {
                   hcell[slot_of[g] * hot_cap + h] = (uint16_t)((iy << 8) | ix);
                   if (CB == 2) {   // (byte counters take their S tasks straight from the level lists)
                     const int slot = tK[li] <= SMALL_K ? atomicAdd(&s_ntask[0], 1)
                                                        : G * hot_cap - 1 - atomicAdd(&s_ntask[1], 1);
+                    RD_CHECK(slot >= 0 && slot < G * hot_cap, CK_K2_TASK);
                     tasks[slot] = (uint16_t)((g << 12) | h);
                   }
                 } else {
@@ -350,6 +362,9 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
       }
       __syncthreads();
       PMARK(2);
+#ifdef RD_CHECKED
+      if (P.jitter) __nanosleep(((unsigned)(warp * 97u + step * 7919u + blockIdx.x * 2654435761u) >> 8) & 2047u);
+#endif
       // ---------------- (2) the next step's rays; S = sum_i w(i) sum_j w(j) raw(y+i, x+j) at
       //     each hotspot and the candidate test
       {
@@ -403,6 +418,9 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
             }
             const uint16_t* w = tW + li * P.wstride;
             const uint32_t* lvlw = raw32 + ((g * lvlc) >> 2);
+            RD_CHECK(!valid || (g < G && h < hot_cap && iy - 1 + hal - K >= 0 && iy - 1 + hal + K < P.k2o.raws &&
+                                cx0 - al >= 0 && cx0 - al + 4 * nw <= rawp * CB && nw <= NWW),
+                     CK_K2_WINDOW);
             unsigned long long acc = 0;
             if (valid && !(P.ablate & 1)) {
               for (int row = hl; row <= 2 * K; row += hsl) {
@@ -440,8 +458,15 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
                 // candidate: r in [r_min, r_max] and S > T_norm(r);
                 // the top level of the step waits for the next step's S of its upper neighbour
                 if (li >= 1 && li <= nlev - 2 && (double)(long long)S > tTn[li]) {
-                  if (li == Lhi) cdef[par * hot_cap + atomicAdd(&s_ndef[par], 1)] = (uint16_t)h;
-                  else cand[atomicAdd(s_ncand, 1)] = (uint16_t)tk;
+                  if (li == Lhi) {
+                    const int q = atomicAdd(&s_ndef[par], 1);
+                    RD_CHECK(q < hot_cap, CK_K2_TASK);
+                    cdef[par * hot_cap + q] = (uint16_t)h;
+                  } else {
+                    const int q = atomicAdd(s_ncand, 1);
+                    RD_CHECK(q < G * hot_cap, CK_K2_TASK);
+                    cand[q] = (uint16_t)tk;
+                  }
                 }
               }
             }
@@ -469,6 +494,9 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
           const int c = hcell[sl * hot_cap + h];
           const int iy = c >> 8, ix = c & 0xFF;
           const cell_t* ctr = rawc + g * lvlc + (iy - 1 + hal) * rawp + (ix - 1 + hal);   // the hotspot's cell
+          RD_CHECK(!valid || (g < G && h < hot_cap && iy - 1 + hal - K >= 0 && iy - 1 + hal + K < P.k2o.raws &&
+                              ix - 1 + hal - K >= 0 && ix - 1 + hal + K < P.k2o.rawc),
+                   CK_K2_WINDOW);
           const int sub = small ? (lane & 15) : lane;
           unsigned long long acc = 0;   // lane sum over window rows sub, sub + 32, ... (K > 15: 2K + 1 > 32 rows)
           if (valid && !(P.ablate & 1)) {
@@ -530,8 +558,15 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
               // candidate: r in [r_min, r_max] and S > T_norm(r);
               // the top level of the step waits for the next step's S of its upper neighbour
               if (li >= 1 && li <= nlev - 2 && (double)(long long)S > tTn[li]) {
-                if (li == Lhi) cdef[par * hot_cap + atomicAdd(&s_ndef[par], 1)] = (uint16_t)h;
-                else cand[atomicAdd(s_ncand, 1)] = (uint16_t)tk;
+                if (li == Lhi) {
+                  const int q = atomicAdd(&s_ndef[par], 1);
+                  RD_CHECK(q < hot_cap, CK_K2_TASK);
+                  cdef[par * hot_cap + q] = (uint16_t)h;
+                } else {
+                  const int q = atomicAdd(s_ncand, 1);
+                  RD_CHECK(q < G * hot_cap, CK_K2_TASK);
+                  cand[q] = (uint16_t)tk;
+                }
               }
             }
           }
@@ -540,6 +575,9 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
       }
       __syncthreads();
       PMARK(3);
+#ifdef RD_CHECKED
+      if (P.jitter) __nanosleep(((unsigned)(warp * 40503u + step * 2654435761u + blockIdx.x * 31u) >> 9) & 2047u);
+#endif
       // ---------------- (3) undo the step's counters, then peaks of levels L0-1 .. Lhi-1
       if (P.debug) {   // level fingerprints over the tile's own cells (each frame voxel once)
         const int x1 = min(X0 + TX, P.W), y1 = min(Y0 + TY, P.H), nx = x1 - X0, ncell = nx * (y1 - Y0);
@@ -595,6 +633,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
             h = tk & 0xFFF;
           }
           const int sc = lc % NSLOT;
+          RD_CHECK(h < min(hcnt[lc], hot_cap) && lc >= 1 && lc <= nlev - 2, CK_K2_NMS);
           const int c = hcell[sc * hot_cap + h];
           const int iy = c >> 8, ix = c & 0xFF;
           constexpr int SSH = CB == 1 ? 8 : 0;   // byte counters: raw count in the low byte

@@ -134,6 +134,7 @@ __global__ void __launch_bounds__(256, RD_K15_MINB) k_rays(Params P) {
           const int b = __shfl_sync(0xffffffffu, base, k);
           if (!((hits >> k) & 1u)) continue;
           const int e = b + __popc(bal & ((1u << lane) - 1u));
+          RD_CHECK(wy0 + k / 3 < P.nty && wx0 + k % 3 < P.ntx, CK_K15_TILE);
           if (e < P.entry_cap) {
             const int64_t o = (tile0 + (wy0 + k / 3) * P.ntx + wx0 + k % 3) * P.entry_cap + e;
             P.ray_d[o] = make_double2(u, v);

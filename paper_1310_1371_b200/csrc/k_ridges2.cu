@@ -144,6 +144,7 @@ k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, in
         if ((rd_bits >> r) & 1u) {
           const int slot = base + __popc(m & ((1u << b_i) - 1u));
           const int64_t bin = fbase + (int64_t)(yr / T1) * P.nbx + X0 / T1 + b_own;
+          RD_CHECK(X0 / T1 + b_own < P.nbx && yr / T1 < P.nby && x < P.W, CK_K1_BIN);
           if (slot < P.ridge_cap) {
             const int64_t o = bin * P.ridge_cap + slot;
             P.bin_xy[o] = (uint32_t)x | ((uint32_t)yr << 16);
@@ -269,6 +270,7 @@ k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, in
           const bool after_plus = (oy > 0) || (oy == 0 && ox > 0);
           const double kplus = sK[oy > 0 ? sp : (oy < 0 ? sm : s0)][tid + ox];
           const double kminus = sK[oy > 0 ? sm : (oy < 0 ? sp : s0)][tid - ox];
+          RD_CHECK(tid - ox >= 0 && tid + ox < KS_COLS && ox >= -1 && ox <= 1 && oy >= -1 && oy <= 1, CK_K1_SMEM);
           const double kafter = after_plus ? kplus : kminus, kbefore = after_plus ? kminus : kplus;
           // ridges: kappa a local minimum along rho (R6); edges: |grad|^2 a local maximum (R19)
           is_r = edge ? (kp >= kafter) && (kp > kbefore) : (kp <= kafter) && (kp < kbefore);

@@ -69,7 +69,7 @@ struct rd_detector {
   void* d_counters = nullptr;  // stats | peak_count | flags | dbg_count
   size_t counters_bytes = 0;
   void* d_rings_int = nullptr; // K3 output per frame, compacted into the caller's buffer by k_emit
-  int* d_need = nullptr;       // [NEED_N] capacities the call needed
+  int* d_need = nullptr;       // [NEED_N] capacities the call needed, then the checked-build flag
   int* d_cursor = nullptr;     // host path: first output offset of each chunk (chained by k_scan)
   void* d_dbg = nullptr;
   void* d_fpr = nullptr;       // debug: level fingerprints
@@ -446,7 +446,7 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   det->counters_bytes = sizeof(Stats) * B + sizeof(int) * 3 * B + sizeof(int) * B * ntl + 8 * rd_detector::NPART + sizeof(int) * B;
   ALLOC(det->d_counters, det->counters_bytes);
   ALLOC(det->d_rings_int, sizeof(Ring) * B * P.ring_cap);
-  ALLOC(det->d_need, sizeof(int) * NEED_N);
+  ALLOC(det->d_need, sizeof(int) * (NEED_N + 1));
   ALLOC(det->d_mem_off, sizeof(int) * (P.ring_cap + 1));
   if (c.debug) {
     ALLOC(det->d_dbg, sizeof(HotRec) * B * P.dbg_cap);
@@ -488,6 +488,10 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   P.redo_list = nullptr;
   P.rings = (Ring*)det->d_rings_int;
   P.need = det->d_need;
+  P.check = det->d_need + NEED_N;   // zeroed with the needs at every call
+#ifdef RD_CHECKED
+  P.jitter = getenv("RD_JITTER") ? 1 : 0;
+#endif
   P.dbg_fpr = (unsigned long long*)det->d_fpr;
   P.n_sm = det->n_sm;
   P.k1_slots = k_ridges_slots(det->n_sm);
@@ -670,7 +674,7 @@ rd_status rd_detect(rd_detector* det, const void* d_frames, int64_t pitch, int64
   cudaStream_t st = (cudaStream_t)stream;
   if (det->have_last) CK(cudaStreamWaitEvent(st, det->ev_last, 0));   // the previous call's scratch
   det->have_last = false;
-  CK(cudaMemsetAsync(det->d_need, 0, sizeof(int) * NEED_N, st));
+  CK(cudaMemsetAsync(det->d_need, 0, sizeof(int) * (NEED_N + 1), st));
   // A large batch runs as two halves on two internal streams (disjoint frame views of the
   // internal buffers), joined back into the caller's stream: each kernel's last partial
   // wave overlaps the other half's kernels.  Per-kernel timing keeps one stream.
@@ -733,6 +737,17 @@ static rd_status ensure_host_path(rd_detector* det) {
   return RD_OK;
 }
 
+// checked builds: the first failed kernel assertion of the last call (RD_ERR_CUDA with a message)
+static rd_status check_flag(rd_detector* det) {
+  int v = 0;
+  CK(cudaMemcpy(&v, det->d_need + NEED_N, sizeof(int), cudaMemcpyDeviceToHost));
+  if (v) {
+    snprintf(g_err, sizeof g_err, "checked build: kernel assertion %d failed at source line %d", v >> 16, v & 0xFFFF);
+    return RD_ERR_CUDA;
+  }
+  return RD_OK;
+}
+
 rd_status rd_detect_host(rd_detector* det, const void* h_frames, int64_t pitch, int64_t fstride, int32_t n,
                          rd_ring* h_rings, int32_t ring_cap_total, int32_t* h_counts, int32_t* h_offsets) {
   if (!det || n < 1 || !h_counts || !h_offsets || ring_cap_total < 0 || (ring_cap_total > 0 && !h_rings))
@@ -788,7 +803,7 @@ rd_status rd_detect_host(rd_detector* det, const void* h_frames, int64_t pitch, 
     for (int i = 0; i < det->n_slots; ++i) CK(cudaStreamWaitEvent(det->s_hc[i], det->ev_last, 0));
   }
   det->have_last = false;
-  CK(cudaMemsetAsync(det->d_need, 0, sizeof(int) * NEED_N, det->s_h2d));
+  CK(cudaMemsetAsync(det->d_need, 0, sizeof(int) * (NEED_N + 1), det->s_h2d));
   CK(cudaMemsetAsync(det->d_cursor, 0, sizeof(int), det->s_h2d));
   CK(cudaEventRecord(det->ev_d2h[0], det->s_h2d));   // the memsets before any chunk's kernels
   for (int i = 0; i < det->n_slots; ++i) CK(cudaStreamWaitEvent(det->s_hc[i], det->ev_d2h[0], 0));
@@ -846,6 +861,7 @@ rd_status rd_detect_host(rd_detector* det, const void* h_frames, int64_t pitch, 
     }
     for (cudaEvent_t e : tev) cudaEventDestroy(e);
   }
+  if (rd_status cs = check_flag(det)) return cs;
   memcpy(h_counts, det->h_out_co, sizeof(int) * n);
   memcpy(h_offsets, det->h_out_co + n, sizeof(int) * (n + 1));
   int64_t total = 0;   // rings written: the valid frames' ranges (all inside ring_cap_total)
@@ -868,6 +884,7 @@ rd_status rd_sync(rd_detector* det) {
   if (!det->have_last || det->last_host) return RD_ERR_STATE;
   CK(cudaSetDevice(det->device));
   CK(cudaEventSynchronize(det->ev_last));
+  if (rd_status cs = check_flag(det)) return cs;
   std::vector<int> fl(det->last_n);
   CK(cudaMemcpy(fl.data(), det->P.flags, sizeof(int) * det->last_n, cudaMemcpyDeviceToHost));
   for (int v : fl)

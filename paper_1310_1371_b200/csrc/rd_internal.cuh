@@ -101,11 +101,34 @@ struct Params {
   int k1_slots;                 // resident K1 CTAs on the device (row-segment choice)
   int debug;
   unsigned long long* dbg_fpr;  // [F][n_levels][3] level fingerprints (debug): sum raw, sum raw^2, sum raw*(yW+x)
+  int* check;                   // checked builds (RD_CHECKED): first failed assertion, code << 16 | line
+  int jitter;                   // checked builds: perturb the warp schedule of K2 (RD_JITTER=1)
   unsigned long long* prof;     // optional per-phase cycle counters (rd_phase_cycles), may be null
   int dbg_cap;
   HotRec* dbg_hot;              // [F][dbg_cap]
   int* dbg_count;               // [F]
 };
+
+// ---------------------------------------------------------------- checked builds
+// The sanitizer tier of SURVEY.md §4 (T5) by assertion: a build with -DRD_CHECKED (librd_checked.so,
+// tests/test_checked.py) tests every shared-memory and global index the kernels form against the
+// bounds of its array; the first failure is recorded in P.check (code << 16 | source line) and
+// reported by rd_sync / rd_detect_host as RD_ERR_CUDA.  Product builds compile the checks away.
+enum CheckCode { CK_K1_SMEM = 1, CK_K1_BIN, CK_K15_TILE, CK_K15_ENTRY, CK_K2_VOTE, CK_K2_LIST, CK_K2_WINDOW,
+                 CK_K2_TASK, CK_K2_NMS, CK_K2_RAY, CK_K3_ORDER, CK_K3_BIN, CK_EMIT };
+__device__ __noinline__ inline void rd_check_fail(int* check, int code, int line) {
+  if (check) atomicCAS(check, 0, (code << 16) | (line & 0xFFFF));
+}
+#ifdef RD_CHECKED
+#define RD_CHECK(cond, code)                                                   \
+  do {                                                                         \
+    if (!(cond)) ::rd::rd_check_fail(P.check, (code), __LINE__);               \
+  } while (0)
+#else
+#define RD_CHECK(cond, code) \
+  do {                       \
+  } while (0)
+#endif
 
 // ---------------------------------------------------------------- fp64 recipe (A3)
 // kappa = 0.5*(T - sqrt(e*e + 4*(b*b))) and the unit eigenvector, each operation

@@ -37,7 +37,11 @@ def pack(rings: torch.Tensor, counts: torch.Tensor, offsets: torch.Tensor | None
         n, cap = rings.shape[0], rings.shape[1]
         mask = torch.arange(cap, device=rings.device).unsqueeze(0) < valid.unsqueeze(1)
         return rings[mask].reshape(-1, REC), c
-    # compact: frames with count -1 may leave holes (output capacity); gather the valid ranges
+    # compact: the valid frames' rings are back to back unless a frame with count -1 left a hole
+    # (output capacity); then gather the valid ranges
+    cc = c.cpu()
+    if bool((cc >= 0).all()):
+        return rings.reshape(-1, REC)[: int(cc.sum())], c
     o = offsets[:-1].to(torch.int64)
     total = int(valid.sum())
     if total == 0:
@@ -83,6 +87,29 @@ def gather_records(recs: torch.Tensor, cnt: torch.Tensor, dst: int = 0, group=No
     return out_r, out_c
 
 
+def collect(batches, dst: int = 0, group=None):
+    """The multi-GPU result path of SURVEY.md §8(e) (bench.py --config 5): this rank's detect
+    outputs (a list of (rings, counts, offsets) in frame order, compact or padded) are packed and
+    gathered to `dst`.  Returns (records [N_total, 64] uint8, counts int64) on dst — in rank order,
+    so byte-identical for every world size when ranks hold contiguous frame ranges — None on the
+    other ranks.  Without an initialised process group the local lists are returned."""
+    packed = [pack(*b) for b in batches]
+    if packed:
+        recs = torch.cat([p[0] for p in packed])
+        cnts = torch.cat([p[1] for p in packed])
+    else:
+        recs, cnts = torch.zeros((0, REC), dtype=torch.uint8), torch.zeros(0, dtype=torch.int64)
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return recs, cnts
+    return gather_records(recs, cnts, dst=dst, group=group)
+
+
+def digest(records: torch.Tensor, counts: torch.Tensor) -> str:
+    """sha256 of gathered records and counts (the P-invariance check of SURVEY.md §4 T4)."""
+    import hashlib
+    return hashlib.sha256(records.cpu().numpy().tobytes() + counts.cpu().numpy().astype(np.int64).tobytes()).hexdigest()
+
+
 def unpack(records: torch.Tensor, counts: torch.Tensor) -> list:
     """Per-frame structured arrays (RING_DTYPE) from packed records; None for overflowed frames."""
     arr = records.cpu().numpy().reshape(-1).view(RING_DTYPE)
@@ -96,5 +123,4 @@ def unpack(records: torch.Tensor, counts: torch.Tensor) -> list:
     return out
 
 
-__all__ = ["shard", "pack", "gather_rings", "gather_records", "unpack", "REC"]
-_ = np  # numpy is used through RING_DTYPE views
+__all__ = ["shard", "pack", "gather_rings", "gather_records", "collect", "digest", "unpack", "REC"]

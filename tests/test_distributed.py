@@ -108,3 +108,64 @@ def test_gather_gloo_matches_single_process(world, n_frames):
     assert len(back) == n_frames
     for e, g in zip(expect, back):
         assert (e is None and g is None) or e.view(RING_DTYPE).tobytes() == g.tobytes()
+
+
+# ---------------------------------------------------------------- bench.py --config 5 path
+def _compact(ring_lists, cap_extra=3):
+    """rd_detect-style compact output of per-frame lists: rings back to back (a frame with
+    None overflowed: count -1, no rings), counts, CSR offsets."""
+    counts = np.array([-1 if r is None else len(r) for r in ring_lists], dtype=np.int32)
+    offsets = np.zeros(len(ring_lists) + 1, dtype=np.int32)
+    offsets[1:] = np.cumsum(np.maximum(counts, 0))
+    buf = np.zeros(offsets[-1] + cap_extra, dtype=RING_DTYPE)
+    for i, r in enumerate(ring_lists):
+        if r is not None:
+            buf[offsets[i]:offsets[i + 1]] = r.view(RING_DTYPE)
+    return (torch.from_numpy(buf.view(np.uint8).reshape(-1, 64).copy()), torch.from_numpy(counts),
+            torch.from_numpy(offsets))
+
+
+def _sweep_worker(rank, world, port, n_frames, batch, out_path):
+    """One rank of the cfg5 sweep (bench.run_sweep's result path): its contiguous frame range
+    in batches, detected (here by the oracle), collected to rank 0."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    p = oracle.params(**synth.preset(2))
+    a, b = D.shard(n_frames, world, rank)
+    batches = []
+    for s in range(a, b, batch):
+        lists = [oracle.detect(p, f)[0] for f in synth.batch(2, 0, s, min(batch, b - s))]
+        if s == a and rank == world - 1:
+            lists[0] = None   # an overflowed frame travels as count -1
+        batches.append(_compact(lists))
+    res = D.collect(batches)
+    if rank == 0:
+        torch.save({"recs": res[0], "counts": res[1], "digest": D.digest(*res)}, out_path)
+    else:
+        assert res is None
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sweep_collect_invariant_to_world_size(world):
+    """the gathered cfg5-style lists are byte-identical (same sha256) for every
+    world size and equal the single-process lists frame by frame."""
+    n_frames, batch = 7, 3
+    port = _free_port()
+    with tempfile.TemporaryDirectory() as td:
+        out = os.path.join(td, "s.pt")
+        mp.spawn(_sweep_worker, args=(world, port, n_frames, batch, out), nprocs=world, join=True)
+        got = torch.load(out)
+    p = oracle.params(**synth.preset(2))
+    expect = [oracle.detect(p, f)[0] for f in synth.batch(2, 0, 0, n_frames)]
+    expect[D.shard(n_frames, world, world - 1)[0]] = None
+    ref = D.collect([_compact(expect[s:s + batch]) for s in range(0, n_frames, batch)])   # one process
+    assert D.digest(*ref) != "" and got["recs"].numel() > 0
+    back = D.unpack(got["recs"], got["counts"])
+    for e, g in zip(expect, back):
+        assert (e is None and g is None) or e.view(RING_DTYPE).tobytes() == g.tobytes()
+    # byte identity with the single-process collect (the None frame sits at the same index)
+    assert torch.equal(got["recs"], ref[0]) and torch.equal(got["counts"], ref[1])
+    assert got["digest"] == D.digest(*ref)
+

@@ -47,9 +47,11 @@ def build_oracle(force=False):
     return out
 
 
-def build_rd(force=False):
+def build_rd(force=False, checked=False):
+    """librd.so, or with checked=True librd_checked.so: the same sources with -DRD_CHECKED (bounds
+    assertions in every kernel, tests/test_checked.py)."""
     pkg = os.path.join(ROOT, "paper_1310_1371_b200")
-    out = os.environ.get("RD_BUILD_OUT") or os.path.join(pkg, "librd.so")
+    out = os.environ.get("RD_BUILD_OUT") or os.path.join(pkg, "librd_checked.so" if checked else "librd.so")
     csrc = os.path.join(pkg, "csrc")
     srcs = sorted(glob.glob(os.path.join(csrc, "*.cu")) + glob.glob(os.path.join(csrc, "*.cpp")))
     deps = srcs + glob.glob(os.path.join(csrc, "*.cuh")) + glob.glob(os.path.join(csrc, "*.h")) + \
@@ -58,34 +60,19 @@ def build_rd(force=False):
         return out
     prof = ["-DRD_K2_PROF"] if os.environ.get("RD_BUILD_PROF") else []   # K2 phase-cycle counters (tools/phase_probe.py)
     prof += os.environ.get("RD_BUILD_DEFS", "").split()   # variant builds for A/B runs (-DNAME=VALUE ...)
+    if checked:
+        prof += ["-DRD_CHECKED"]
     cmd = [NVCC, "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo"] + prof + [
            "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off", "-shared",
            "-Xptxas", "-v", "-I", os.path.join(ROOT, "include"), "-o", out] + srcs + ["-lcudart"]
     r = _run(cmd)
-    with open(os.path.join(pkg, "build_ptxas.log"), "w") as f:
+    with open(os.path.join(pkg, "build_ptxas_checked.log" if checked else "build_ptxas.log"), "w") as f:
         f.write(r.stdout + r.stderr)
     return out
 
 
-def build_san(force=False):
-    """tools/sanitize/rd_san: a C driver of librd.so for compute-sanitizer runs (tests/test_sanitizers.py)."""
-    d = os.path.join(ROOT, "tools", "sanitize")
-    out = os.path.join(d, "rd_san")
-    src = os.path.join(d, "rd_san.c")
-    pkg = os.path.join(ROOT, "paper_1310_1371_b200")
-    deps = [src, os.path.join(ROOT, "include", "rd.h"), os.path.join(pkg, "librd.so"),
-            os.path.join(ROOT, "synth", "libsynth.so")]
-    if force or _stale(out, deps):
-        cuda = os.path.dirname(os.path.dirname(NVCC))
-        _run(["gcc", "-O2", "-Wall", "-o", out, src, "-I", os.path.join(ROOT, "include"), "-I",
-              os.path.join(cuda, "include"), "-L", pkg, "-lrd", "-L", os.path.join(ROOT, "synth"), "-lsynth",
-              "-L", os.path.join(cuda, "lib64"), "-lcudart", f"-Wl,-rpath,{pkg}", f"-Wl,-rpath,{ROOT}/synth",
-              "-Wl,-rpath,$ORIGIN/../../paper_1310_1371_b200", "-Wl,-rpath,$ORIGIN/../../synth"])
-    return out
-
-
 def build_all(force=False):
-    return [build_synth(force), build_oracle(force), build_rd(force), build_san(force)]
+    return [build_synth(force), build_oracle(force), build_rd(force), build_rd(force, checked=True)]
 
 
 if __name__ == "__main__":
