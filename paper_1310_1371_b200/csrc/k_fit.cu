@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(K3_THREADS) k_fit(Params P) {
     for (int by = by0; by <= by1; ++by)
       for (int bx = bx0; bx <= bx1; ++bx) {
         const int64_t b = fbins + by * P.nbx + bx;
-        const int cnt = P.bin_count[b];
+        const int cnt = min(P.bin_count[b], P.ridge_cap);
         RD_CHECK(cnt >= 0 && cnt <= P.ridge_cap && bx < P.nbx && by < P.nby, CK_K3_BIN);
         const uint32_t* xy = P.bin_xy + b * P.ridge_cap;
         for (int k = lane; k < cnt; k += 32) {
@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(K3_THREADS) k_fit(Params P) {
       for (int by = by0; by <= by1; ++by)
         for (int bx = bx0; bx <= bx1; ++bx) {
           const int64_t b = fbins + by * P.nbx + bx;
-          const int cnt = P.bin_count[b];
+          const int cnt = min(P.bin_count[b], P.ridge_cap);
           const uint32_t* xy = P.bin_xy + b * P.ridge_cap;
           for (int k = lane; k < cnt; k += 32) {
             uint32_t v = xy[k];
@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(K3_THREADS) k_members(Params P, int f, int wri
     for (int by = by0; by <= by1; ++by)
       for (int bx = bx0; bx <= bx1; ++bx) {
         const int64_t b = fbins + by * P.nbx + bx;
-        const int cnt = P.bin_count[b];
+        const int cnt = min(P.bin_count[b], P.ridge_cap);
         const uint32_t* xy = P.bin_xy + b * P.ridge_cap;
         for (int k0 = 0; k0 < cnt; k0 += 32) {
           const int k = k0 + lane;
@@ -228,13 +228,14 @@ __global__ void __launch_bounds__(1024) k_scan(Params P, int n_frames, int out_c
   __shared__ int carry;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) carry = base_in ? *base_in : 0;
-  int mx = 0;
+  int mx = 0, mxr = 0;
   __syncthreads();
   for (int f0 = 0; f0 < n_frames; f0 += 1024) {
     const int f = f0 + tid;
     int npk = 0;
     bool valid = false;
     if (f < n_frames) {
+      mxr = max(mxr, P.need_ridges[f]);
       npk = P.peak_count[f];
       valid = P.flags[f] == 0 && npk <= P.ring_cap;
       mx = max(mx, npk);
@@ -276,6 +277,8 @@ __global__ void __launch_bounds__(1024) k_scan(Params P, int n_frames, int out_c
   }
   mx = __reduce_max_sync(0xffffffffu, mx);
   if (lane == 0 && mx) atomicMax(&P.need[NEED_RINGS], mx);
+  mxr = __reduce_max_sync(0xffffffffu, mxr);
+  if (lane == 0 && mxr) atomicMax(&P.need[NEED_RIDGES], mxr);
   if (tid == 0) {
     offsets[n_frames] = carry;
     if (base_out) *base_out = carry;

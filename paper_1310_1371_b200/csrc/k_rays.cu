@@ -59,10 +59,12 @@ __global__ void __launch_bounds__(256, RD_K15_MINB) k_rays(Params P) {
   // tiles any ray of a bin can reach: |offset| <= r_hi, halo <= hal
   const int reach = rhi + hal + 1;
   const int wy0 = max((by * T1 - reach) / TY, 0), wy1 = min((by * T1 + T1 - 1 + reach) / TY, P.nty - 1);
-  int my_votes = 0;
+  int my_votes = 0, need_r = 0;
   for (int bx = warp; bx < P.nbx; bx += blockDim.x >> 5) {
     const int64_t fb = (int64_t)f * P.nbx * P.nby + by * P.nbx + bx;
-    const int cnt = P.bin_count[fb];
+    const int cnt_all = P.bin_count[fb];   // the true count: ridges beyond ridge_cap were not stored
+    need_r = max(need_r, cnt_all);
+    const int cnt = min(cnt_all, P.ridge_cap);
     if (cnt == 0) continue;
     const int wx0 = max((bx * T1 - reach) / TX, 0), wx1 = min((bx * T1 + T1 - 1 + reach) / TX, P.ntx - 1);
     for (int j0 = 0; j0 < 2 * cnt; j0 += 32) {
@@ -187,6 +189,9 @@ __global__ void __launch_bounds__(256, RD_K15_MINB) k_rays(Params P) {
   }
   my_votes = __reduce_add_sync(0xffffffffu, my_votes);
   if (lane == 0 && my_votes) atomicAdd(&P.stats[f].votes, (unsigned long long)my_votes);
+  // ridges per bin the frame needed (per-frame slot; k_scan folds the frames into P.need)
+  need_r = __reduce_max_sync(0xffffffffu, need_r);
+  if (lane == 0 && need_r) atomicMax(&P.need_ridges[f], need_r);
 }
 
 cudaError_t launch_rays(int n_frames, const Params& P, cudaStream_t st) {

@@ -48,7 +48,6 @@ struct K1SSmem {                       // dynamic shared memory of k_ridges2
   int sI[KS_COLS][RB];                 // input rows (as int), a column's RB rows adjacent
   unsigned sBal[2][RB][KS_COLS / 32];  // ridge ballots of a step's rows, by parity
   int sCur[KS_NB];                     // ridges so far in the current row of each bin
-  int sNeed;                           // largest bin of the CTA (one global atomicMax at the end)
 };
 }  // namespace
 
@@ -111,7 +110,6 @@ k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, in
   const int b_own = (tid - KS_HALO) >> 5, b_i = (tid - KS_HALO) & 31;   // bin and index in it
   const int64_t fbase = (int64_t)f * P.nbx * P.nby;
   if (tid < KS_NB) sCur[tid] = 0;
-  if (tid == 0) S.sNeed = 0;
   unsigned rd_bits = 0;            // ridge flags of the previous step's RB test rows
   int rd_y0 = 0;                   // first test row of the previous step
   bool rd_any = false;             // the previous step tested rows of this segment
@@ -156,12 +154,9 @@ k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, in
           const int bx = X0 / T1 + b_own;
           if (b_i == 0 && bx < P.nbx) {
             const int64_t bin = fbase + (int64_t)(yr / T1) * P.nbx + bx;
-            P.bin_count[bin] = min(base, P.ridge_cap);
+            P.bin_count[bin] = base;   // the true count (readers clamp to ridge_cap; K1.5 reports the need)
             if (base > P.ridge_cap) atomicOr(&P.flags[f], OVF_RIDGES);
-            if (base) {
-              atomicAdd(&P.stats[f].ridges, (unsigned long long)base);
-              atomicMax(&S.sNeed, base);
-            }
+            if (base) atomicAdd(&P.stats[f].ridges, (unsigned long long)base);
           }
           base = 0;
         }
@@ -282,8 +277,6 @@ k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, in
       rd_any |= yr >= Y0 && yr < Y1;
     }
   }
-  __syncthreads();
-  if (tid == 0 && S.sNeed) atomicMax(&P.need[NEED_RIDGES], S.sNeed);
 }
 
 template <typename PixT, int KS, bool EDGE>

@@ -313,6 +313,8 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
       std::sort(cand.begin(), cand.end());
       return cand;
     };
+    int rmin = 256;   // resident rays a shape must hold (RD_K2_RMIN for A/B)
+    if (const char* env = getenv("RD_K2_RMIN")) rmin = std::max(32, atoi(env));
     auto pick = [&](Params& Q, int cb, int& G, int& nt, int& minb, int forceT, int forceTY) {
       std::vector<Shape> sh = cb == 1 ? std::vector<Shape>{{104, 4, 512, 2}, {96, 4, 512, 2}, {64, 4, 256, 3}, {64, 4, 384, 2},
                                                            {64, 8, 512, 1}}
@@ -339,7 +341,7 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
                    Q.k2t <= 254 && Q.k2ty >= 16 && Q.k2ty <= 254) {
         } else {   // the cheapest tiling whose layout fits this shape with 256 resident rays
           Q.k2t = Q.k2ty = s.T;
-          Q.k2_rcap = 256;
+          Q.k2_rcap = rmin;
           const size_t lim = s.minb == 1 ? smax : std::min(smax, sm_sm / s.minb - 1024);
           for (const auto& t : tilings(s.T)) {
             Q.k2t = std::get<1>(t);
@@ -351,7 +353,7 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
           }
         }
         const size_t limit = s.minb == 1 ? smax : std::min(smax, sm_sm / s.minb - 1024);
-        Q.k2_rcap = 256;
+        Q.k2_rcap = rmin;
         if (k_hough2_layout(Q, s.G, s.nt, cb) > limit) continue;
         while (Q.k2_rcap < Q.entry_cap) {   // as many resident rays as fit
           Q.k2_rcap += 64;
@@ -443,7 +445,8 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   ALLOC(det->d_ray_d, sizeof(double2) * B * ntl * P.entry_cap);
   ALLOC(det->d_ray_xy, sizeof(uint32_t) * B * ntl * P.entry_cap);
   ALLOC(det->d_ray_r, sizeof(uint32_t) * B * ntl * P.entry_cap);
-  det->counters_bytes = sizeof(Stats) * B + sizeof(int) * 3 * B + sizeof(int) * B * ntl + 8 * rd_detector::NPART + sizeof(int) * B;
+  det->counters_bytes = sizeof(Stats) * B + sizeof(int) * 3 * B + sizeof(int) * B * ntl + 8 * rd_detector::NPART +
+                        sizeof(int) * B + sizeof(int) * B;
   ALLOC(det->d_counters, det->counters_bytes);
   ALLOC(det->d_rings_int, sizeof(Ring) * B * P.ring_cap);
   ALLOC(det->d_need, sizeof(int) * (NEED_N + 1));
@@ -485,6 +488,7 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   P.ray_count = P.dbg_count + B;
   P.k2_work = P.ray_count + B * ntl;
   P.redo = P.k2_work + 2 * rd_detector::NPART;
+  P.need_ridges = P.redo + B;
   P.redo_list = nullptr;
   P.rings = (Ring*)det->d_rings_int;
   P.need = det->d_need;
@@ -598,6 +602,7 @@ static void frame_view(const rd_detector* det, int f0, int slot, Params& V, Para
   if (V.dbg_hot) V.dbg_hot += (int64_t)f0 * P.dbg_cap;
   if (V.dbg_fpr) V.dbg_fpr += (int64_t)f0 * 3 * P.n_levels;
   V.redo += f0;
+  V.need_ridges += f0;
   V.k2_work = P.k2_work + 2 * slot;   // [main, redo] work counters of the slot
   V16 = V;
   V16.k2t = det->P16.k2t;
@@ -637,6 +642,7 @@ static rd_status detect_impl(rd_detector* det, const void* d_frames, int64_t pit
     CK(cudaMemsetAsync(P.ray_count, 0, sizeof(int) * n * ntl, st));
     CK(cudaMemsetAsync(P.k2_work, 0, sizeof(int) * 2, st));
     CK(cudaMemsetAsync(P.redo, 0, sizeof(int) * n, st));
+    CK(cudaMemsetAsync(P.need_ridges, 0, sizeof(int) * n, st));
   }
   if (P.dbg_fpr) CK(cudaMemsetAsync(P.dbg_fpr, 0, sizeof(unsigned long long) * 3 * P.n_levels * n, st));
   if (ev) CK(cudaEventRecord(ev[0], st));

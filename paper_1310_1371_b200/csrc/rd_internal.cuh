@@ -41,7 +41,7 @@ struct Ring {          // == rd_ring (64 B)
 struct K2Layout {
   int cb, raws, rawp, lvlc;   // counter bytes, raw rows, row pitch (cells), cells per level
   int rawc;                   // raw columns (tile width + 2 halo); raws = tile height + 2 halo
-  int raw, hS, sd, rr, xy, hcell, hraw, task, cand, cdef, act, hcnt, w, k, tn, dummy, total;
+  int raw, hS, sd, rr, xy, hcell, hraw, task, cand, cdef, act, hcnt, w, k, tn, dummy, wsm, total;
   uint32_t rawp_magic;        // ceil(2^32 / rawp): cell / rawp = umulhi(cell, magic) for cells < 2^16
 };
 
@@ -97,6 +97,7 @@ struct Params {
   Stats* stats;                 // [F]
   Ring* rings;                  // [F][ring_cap] K3 output in canonical order (compacted by k_emit)
   int* need;                    // [NEED_N] capacities needed by the call (atomicMax)
+  int* need_ridges;             // [F] largest ridge bin of each frame (K1.5; folded into need by k_scan)
   int n_sm;                     // SMs of the device (grid sizing)
   int k1_slots;                 // resident K1 CTAs on the device (row-segment choice)
   int debug;
