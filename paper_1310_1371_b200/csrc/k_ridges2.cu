@@ -16,9 +16,13 @@
 // Every integer stage is exact, so evaluation order is free; kappa/rho use the shared
 // explicit-rounding recipe (rd_internal.cuh).  Replicate border: input rows and columns are
 // clamped at load time.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 
 #include "rd_internal.cuh"
 
@@ -39,9 +43,22 @@ constexpr int KS_NB = KS_OUT / 32;  // bins per strip
 #define RD_K1_RB 2
 #endif
 constexpr double NOT_CAND = 2.0;    // rho.x of a pixel that is not a ridge candidate (|rho.x| <= 1)
+#ifndef RD_K1_NSTAGE
+#define RD_K1_NSTAGE 2   // TMA input stages: rows are fetched NSTAGE - 1 steps ahead (3, 4, 6 measured slower)
+#endif
+constexpr int NSTAGE = RD_K1_NSTAGE;
+constexpr int TMA_BOX = 128;       // a strip row is KS_COLS / 128 TMA boxes (128-byte aligned destinations)
+#ifndef RD_K1_TMA_TID
+#define RD_K1_TMA_TID (KS_COLS - 1)   // the issuing thread: a right-halo column (no ridge output)
+#endif
+constexpr int TMA_TID = RD_K1_TMA_TID;
+static_assert(KS_COLS % TMA_BOX == 0, "strip rows are whole TMA boxes");
 
 template <int RB>
-struct K1SSmem {                       // dynamic shared memory of k_ridges2
+struct K1SSmem {                       // dynamic shared memory of k_ridges2 (128-byte aligned base)
+  alignas(128) uint16_t sIn[NSTAGE][RB][KS_COLS];   // TMA: input rows of NSTAGE steps (uint8 frames: rows
+                                                    // of KS_COLS bytes at the same row offsets)
+  uint64_t bar[NSTAGE];                // TMA: one mbarrier per input stage
   double2 sD[RB + 2][KS_COLS];         // rho ring (x = NOT_CAND: no candidate)
   double sK[RB + 2][KS_COLS];          // kappa ring
   double sG[RB][KS_COLS];              // G rows
@@ -51,12 +68,19 @@ struct K1SSmem {                       // dynamic shared memory of k_ridges2
 };
 }  // namespace
 
-template <typename PixT, int KS, int RB, bool EDGE>
+// Input rows reach shared memory either by TMA (TMA = true: cp.async.bulk.tensor of each row's
+// two 192-pixel boxes into a ring of NSTAGE stages, issued by one thread NSTAGE - 1 steps ahead
+// and completed on the stage's mbarrier; rows outside the frame are fetched at the clamped row,
+// columns outside it arrive as zeros and are read at the clamped column: replicate border) or
+// by per-thread loads prefetched one step ahead in registers (frames whose address or pitch is
+// not 16-byte aligned).
+template <typename PixT, int KS, int RB, bool EDGE, bool TMA>
 __global__ void __launch_bounds__(KS_COLS, RD_K1_MINB)
-k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, int seg_rows, Params P) {
+k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, int seg_rows, Params P,
+          const __grid_constant__ CUtensorMap tmap) {
   constexpr int NTAP = 2 * KS + 1;
   constexpr int NR = RB + 2;        // kappa / rho ring rows
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   K1SSmem<RB>& S = *reinterpret_cast<K1SSmem<RB>*>(smem_raw);
   auto& sD = S.sD;
   auto& sK = S.sK;
@@ -97,12 +121,36 @@ k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, in
   for (int j = 0; j < NTAP; ++j) wR[j] = 0u;
 #pragma unroll
   for (int j = 0; j < 5; ++j) wA[j] = wB[j] = wC[j] = 0.0;
-  // input prefetch: the next step's RB rows
+  // input prefetch: the next step's RB rows (registers), or the first NSTAGE - 1 steps (TMA)
   PixT pf[RB];
+  const int xs = xc - (X0 - KS_HALO);   // this thread's clamped column inside a TMA row
+  auto tma_issue = [&](int stp) {       // one thread: the RB rows of step stp into stage stp % NSTAGE
+    const int sg = stp % NSTAGE;
+    fence_proxy_async_smem();           // generic reads of the stage (NSTAGE steps ago) before the async writes
+    mbar_expect_tx(&S.bar[sg], (uint32_t)(RB * KS_COLS * sizeof(PixT)));
 #pragma unroll
-  for (int r = 0; r < RB; ++r) {
-    const int yy = min(max(ys0 + r, 0), H - 1);
-    pf[r] = reinterpret_cast<const PixT*>(frame + (int64_t)yy * pitch)[xc];
+    for (int r = 0; r < RB; ++r) {
+      const int yy = min(max(ys0 + stp * RB + r, 0), H - 1);
+      PixT* dst = reinterpret_cast<PixT*>(&S.sIn[sg][0][0]) + r * KS_COLS;
+#pragma unroll
+      for (int b = 0; b < KS_COLS / TMA_BOX; ++b)
+        tma_load_3d(dst + b * TMA_BOX, &tmap, &S.bar[sg], X0 - KS_HALO + b * TMA_BOX, yy, f);
+    }
+  };
+  if (TMA) {
+    if (tid == 0) {
+      for (int i = 0; i < NSTAGE; ++i) mbar_init(&S.bar[i], 1);
+      mbar_fence_init();
+    }
+    __syncthreads();
+    if (tid == TMA_TID)
+      for (int i = 0; i < NSTAGE - 1 && i < n_steps; ++i) tma_issue(i);
+  } else {
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      const int yy = min(max(ys0 + r, 0), H - 1);
+      pf[r] = reinterpret_cast<const PixT*>(frame + (int64_t)yy * pitch)[xc];
+    }
   }
   // bin output: bin b of the strip covers threads 16 + 32b .. 47 + 32b (upper half of warp b,
   // lower half of warp b + 1).  A step's ridges are written in the next step, once both
@@ -119,7 +167,15 @@ k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, in
     const int yi0 = ys0 + st * RB;
     const bool compute = st < n_steps;
     // 1. input rows -> shared memory; prefetch the next step's rows
-    if (compute) {
+    if (compute && TMA) {
+      // the stage of step st + NSTAGE - 1 was last read in step st - 1 (barriers since)
+      if (tid == TMA_TID && st + NSTAGE - 1 < n_steps) tma_issue(st + NSTAGE - 1);
+      const int sg = st % NSTAGE;
+      mbar_wait(&S.bar[sg], (uint32_t)((st / NSTAGE) & 1));
+      const PixT* in = reinterpret_cast<const PixT*>(&S.sIn[sg][0][0]);
+#pragma unroll
+      for (int r = 0; r < RB; ++r) sI[tid][r] = (int)in[r * KS_COLS + xs];
+    } else if (compute) {
 #pragma unroll
       for (int r = 0; r < RB; ++r) {
         sI[tid][r] = (int)pf[r];
@@ -279,13 +335,44 @@ k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, in
   }
 }
 
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+// 3-D tensor map (x, y, frame) of the caller's frames with boxes of TMA_BOX x 1 x 1 pixels;
+// false if TMA cannot address them (16-byte alignment of base, pitch and frame stride)
+bool make_tmap(CUtensorMap* map, const void* frames, int pb, int W, int H, int n, int64_t pitch, int64_t fstride) {
+  if (!g_encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return false;
+    g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  if (((uintptr_t)frames & 15) || (pitch & 15) || (n > 1 && (fstride & 15))) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)n};
+  cuuint64_t strides[2] = {(cuuint64_t)pitch, (cuuint64_t)(n > 1 ? fstride : pitch * H)};
+  cuuint32_t box[3] = {(cuuint32_t)TMA_BOX, 1, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  return g_encode(map, pb == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 3,
+                  const_cast<void*>(frames), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+}  // namespace
+
 template <typename PixT, int KS, bool EDGE>
 static cudaError_t launch_s(const void* frames, int64_t pitch, int64_t fstride, int n_frames, const Params& P,
                             cudaStream_t st) {
   constexpr int RB = RD_K1_RB;
-  // dynamic shared memory: rings + rows (NR = RB + 2 rows of rho and kappa)
+  // dynamic shared memory: rings + rows (NR = RB + 2 rows of rho and kappa) + TMA stages
   const size_t sm = sizeof(K1SSmem<RB>);
-  cudaFuncSetAttribute(k_ridges2<PixT, KS, RB, EDGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  CUtensorMap tmap;
+  static const bool no_tma = getenv("RD_K1_NO_TMA") != nullptr;   // A/B: per-thread loads
+  const bool tma = !no_tma && make_tmap(&tmap, frames, (int)sizeof(PixT), P.W, P.H, n_frames, pitch, fstride);
+  if (!tma) memset(&tmap, 0, sizeof tmap);
+  cudaFuncSetAttribute(k_ridges2<PixT, KS, RB, EDGE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaFuncSetAttribute(k_ridges2<PixT, KS, RB, EDGE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   // segments of whole bin rows: the count that best fills the resident CTA slots (P.k1_slots,
   // from rd_create), each segment paying 3K_s + 6 rows of pipeline warm-up
   const int slots = std::max(1, P.k1_slots);
@@ -308,7 +395,10 @@ static cudaError_t launch_s(const void* frames, int64_t pitch, int64_t fstride, 
     seg = (bin_rows + ns - 1) / ns * T1;
   }
   dim3 grid(strips, (P.H + seg - 1) / seg, n_frames);
-  k_ridges2<PixT, KS, RB, EDGE><<<grid, KS_COLS, sm, st>>>((const uint8_t*)frames, pitch, fstride, seg, P);
+  if (tma)
+    k_ridges2<PixT, KS, RB, EDGE, true><<<grid, KS_COLS, sm, st>>>((const uint8_t*)frames, pitch, fstride, seg, P, tmap);
+  else
+    k_ridges2<PixT, KS, RB, EDGE, false><<<grid, KS_COLS, sm, st>>>((const uint8_t*)frames, pitch, fstride, seg, P, tmap);
   return cudaGetLastError();
 }
 
@@ -341,8 +431,9 @@ size_t k_ridges_smem(int) { return sizeof(K1SSmem<RD_K1_RB>); }
 int k_ridges_slots(int n_sm) {
   int per = 0;
   const size_t sm = sizeof(K1SSmem<RD_K1_RB>);
-  cudaFuncSetAttribute(k_ridges2<uint16_t, 5, RD_K1_RB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_ridges2<uint16_t, 5, RD_K1_RB, false>, KS_COLS, sm) !=
+  cudaFuncSetAttribute(k_ridges2<uint16_t, 5, RD_K1_RB, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sm);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_ridges2<uint16_t, 5, RD_K1_RB, false, true>, KS_COLS, sm) !=
       cudaSuccess)
     per = 1;
   return std::max(1, n_sm * std::max(per, 1));
