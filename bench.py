@@ -313,7 +313,7 @@ def run_gpu(args):
     if os.path.exists(sp):
         for d in json.load(open(sp)):
             for n in names:
-                if d.get("kernel", "").startswith(n) and "dram_bytes_per_frame" in d:
+                if d.get("kernel", "").replace("void ", "").startswith(n) and "dram_bytes_per_frame" in d:
                     summ[n] = d["dram_bytes_per_frame"] * B
     roofs = [
         {"kernel": "k_ridges", "bound": "alu", "achieved": round(k1_ach, 3), "peak": round(fp64_peak, 3),

@@ -41,10 +41,17 @@ json.dump(summ, open(os.path.join(P, f"ncu_summary_{TAG}.json"), "w"), indent=1)
 cols = ["kernel", "duration", "dram_bytes", "warp_inst", "issue_active_pct", "warps_active_pct", "fp64_pipe_pct",
         "alu_pipe_pct", "lsu_pipe_pct", "smem_wavefront_pct", "regs", "dyn_smem"]
 with open(os.path.join(P, f"ncu_summary_{TAG}.md"), "w") as f:
-    f.write("ncu --set full, one launch each on 64 cfg3 frames (tools/prof_step.py 3 64 2; tools/ncu_k.sh)\n\n")
+    f.write("ncu --set full, one launch each on 64 cfg3 frames (tools/prof_step.py 3 64 2; tools/prof_round.sh)\n\n")
     f.write("| " + " | ".join(cols) + " |\n|" + "---|" * len(cols) + "\n")
     for s in summ:
         f.write("| " + " | ".join(str(round(s[c], 2)) if isinstance(s.get(c), float) else str(s.get(c, ""))
                                   for c in cols) + " |\n")
+for k, name in (("k1full", "k1"), ("k2full", "k2")):   # per-source-line stall / instruction summaries
+    src = os.path.join(G, f"{k}_src.csv")
+    if os.path.exists(src):
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_lines.py"), src, "40"], capture_output=True,
+                           text=True)
+        open(os.path.join(P, f"ncu_lines_{name}_{TAG}.txt"), "w").write(
+            f"tools/ncu_lines.py gpurun_out/{k}_src.csv 40 (ncu --set full --import-source, 64 cfg3 frames)\n" + r.stdout)
 print(open(os.path.join(P, f"launches_{TAG}.md")).read())
 print(open(os.path.join(P, f"ncu_summary_{TAG}.md")).read())
