@@ -31,5 +31,5 @@ for _ in range(10):
     y.copy_(x, non_blocking=True)
 torch.cuda.synchronize()
 print(f"H2D pinned: {10 * x.numel() / (time.perf_counter() - t0) / 1e9:.1f} GB/s")
-for c in ["16", "32", "48", "64"]:
+for c in os.environ.get("PROBE_CHUNKS", "16 32 48 64 96 128").split():
     subprocess.run([sys.executable, __file__, "child"], env=dict(os.environ, RD_HOST_CHUNK=c))
