@@ -276,6 +276,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
         // work for the absent levels)
         auto run_votes = [&](auto GLc) {
           constexpr int GL = decltype(GLc)::value;
+          if (P.ablate & 16) return;   // timing experiments only: no votes
           for (int i0 = warp * 32; i0 < nact; i0 += NT) {
             const int i = i0 + lane;
             unsigned lm = 0;   // levels of the step inside the ray's interval
@@ -327,7 +328,8 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
                                                           addr[g] - raw_base < (uint32_t)((g + 1) * lvlc * CB)),
                        CK_K2_VOTE);
   #pragma unroll
-            for (int g = 0; g < GL; ++g) old[g] = atom_add_shared(addr[g], shl_clamp(1u, sh[g]));
+            for (int g = 0; g < GL; ++g)
+              old[g] = (P.ablate & 8) ? 0u : atom_add_shared(addr[g], shl_clamp(1u, sh[g]));   // (8: no atomics)
             uint32_t omax = 0;
   #pragma unroll
             for (int g = 0; g < GL; ++g) {
