@@ -43,6 +43,12 @@ inline size_t al16(size_t v) { return (v + 15) & ~size_t(15); }
 
 constexpr int HSL = RD_K2_HSL;   // byte-counter S tasks: lanes per hotspot (power of two <= 32; 0: per step)
 constexpr int SMALL_K = 7;   // window rows 2K+1 <= 15: a half-warp per hotspot
+// timing ablations (RD_K2_ABLATE bits, see Params::ablate) exist in profiling builds only
+#ifdef RD_K2_PROF
+#define ABL P.ablate
+#else
+#define ABL 0
+#endif
 
 // llround of an exactly computed product (|v| < 2^31): copysign(0.5) added toward zero,
 // then truncated — the same two roundings as the oracle's llround (R9)
@@ -276,7 +282,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
         // work for the absent levels)
         auto run_votes = [&](auto GLc) {
           constexpr int GL = decltype(GLc)::value;
-          if (P.ablate & 16) return;   // timing experiments only: no votes
+          if (ABL & 16) return;   // timing experiments only: no votes
           for (int i0 = warp * 32; i0 < nact; i0 += NT) {
             const int i = i0 + lane;
             unsigned lm = 0;   // levels of the step inside the ray's interval
@@ -329,7 +335,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
                        CK_K2_VOTE);
   #pragma unroll
             for (int g = 0; g < GL; ++g)
-              old[g] = (P.ablate & 8) ? 0u : atom_add_shared(addr[g], shl_clamp(1u, sh[g]));   // (8: no atomics)
+              old[g] = (ABL & 8) ? 0u : atom_add_shared(addr[g], shl_clamp(1u, sh[g]));   // (8: no atomics)
             uint32_t omax = 0;
   #pragma unroll
             for (int g = 0; g < GL; ++g) {
@@ -385,7 +391,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
           int ntask = 0;
 #pragma unroll
           for (int g = 0; g < G; ++g) ntask += lcount(g);
-          if (P.ablate & 4) ntask = 0;
+          if (ABL & 4) ntask = 0;
 #if RD_K2_HSL == 0
           // lanes per hotspot: the widest power of two that still gives every warp its share
           const int per_warp = (ntask + NW - 1) / NW;
@@ -426,7 +432,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
                                 cx0 - al >= 0 && cx0 - al + 4 * nw <= rawp * CB && nw <= NWW),
                      CK_K2_WINDOW);
             unsigned long long acc = 0;
-            if (valid && !(P.ablate & 1)) {
+            if (valid && !(ABL & 1)) {
               for (int row = hl; row <= 2 * K; row += hsl) {
                 const uint32_t* rowp = lvlw + (((iy - 1 + hal + row - K) * rawp + cx0 - al) >> 2);
                 uint32_t lo = 0, hi = 0;
@@ -476,7 +482,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
             }
           }
         } else {
-        const int nsmall = (P.ablate & 4) ? 0 : s_ntask[0], nlarge = (P.ablate & 4) ? 0 : s_ntask[1];
+        const int nsmall = (ABL & 4) ? 0 : s_ntask[0], nlarge = (ABL & 4) ? 0 : s_ntask[1];
         const int half = lane >> 4;
         // small-K hotspots: a half-warp each; large-K: a warp each (lanes over window rows)
         const int nsp = (nsmall + 1) >> 1;
@@ -503,7 +509,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
                    CK_K2_WINDOW);
           const int sub = small ? (lane & 15) : lane;
           unsigned long long acc = 0;   // lane sum over window rows sub, sub + 32, ... (K > 15: 2K + 1 > 32 rows)
-          if (valid && !(P.ablate & 1)) {
+          if (valid && !(ABL & 1)) {
             for (int row = sub; row <= 2 * K; row += small ? 16 : 32) {
               const cell_t* rowp = ctr + (row - K) * rawp;
               if (kWide) {
@@ -625,7 +631,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
 #if RD_K2_SETUP3 == 2
         if (L0 + G < nlev) setup(L0 + G, par ^ 1);
 #endif
-        const int nd = (L0 > 0 && !(P.ablate & 2)) ? s_ndef[par ^ 1] : 0, nc = (P.ablate & 2) ? 0 : s_ncand[0];
+        const int nd = (L0 > 0 && !(ABL & 2)) ? s_ndef[par ^ 1] : 0, nc = (ABL & 2) ? 0 : s_ncand[0];
         for (int p = warp; p < nd + nc; p += NW) {
           int lc, h;
           if (p < nd) {
