@@ -106,8 +106,10 @@ typedef struct rd_frame_stats { int64_t ridges, votes, hotspots, peaks; } rd_fra
 typedef struct rd_level_fpr { int32_t r, pad; int64_t votes, sq, pos; } rd_level_fpr;  /* 32 B */
 
 /* Capacities a call needed (rd_query_overflow).  Each needed_* is the largest value the last
- * call met (not only when it overflowed), so a caller can size a detector for its data: a
- * capacity >= needed_* makes that overflow impossible for the same frames. */
+ * call met (not only when it overflowed), so a caller can size a detector for its data.  The
+ * per-tile needs (rays per tile, hotspots per level) refer to the Hough tiling of that detector;
+ * other capacities change the shared-memory layout and may change the tiling rd_create picks,
+ * so resizing can take more than one round (Detector.sized_for in the Python binding iterates). */
 typedef struct rd_overflow {
   int32_t frames_overflowed;         /* frames of the call whose count is -1 */
   int32_t flags;                     /* OR of the per-frame RD_OVF_* bits */

@@ -60,6 +60,33 @@ class Detector:
         check(lib().rd_create(C.byref(self.cfg), self.max_batch, self.device, C.byref(h)), "rd_create")
         self._h = h
 
+    @classmethod
+    def sized_for(cls, params: dict, frames: torch.Tensor, max_batch: int | None = None, device: int = 0,
+                  margin: float = 1.25, rounds: int = 4) -> "Detector":
+        """A detector whose capacities fit `frames` (a representative CUDA batch): detect, read the
+        capacities the call needed (rd_query_overflow) and recreate with them plus a margin until
+        nothing overflows.  Capacities change the shared-memory layout and hence the Hough tiling,
+        and the needs depend on the tiling, so this iterates (at most `rounds` times)."""
+        keys = {"needed_ridges_per_tile": "max_ridges_per_tile", "needed_entries_per_tile": "max_entries_per_tile",
+                "needed_hotspots_per_level": "max_hotspots_per_level", "needed_rings_per_frame": "max_rings_per_frame"}
+        p = dict(params)
+        n = frames.shape[0] if frames.dim() == 3 else 1
+        for _ in range(rounds):
+            det = cls(p, max_batch=max_batch or n, device=device)
+            det.detect(frames)
+            det.sync(raise_on_overflow=False)
+            ov = det.overflow()
+            if ov["frames_overflowed"] == 0:
+                return det
+            for need, cfg_key in keys.items():
+                cur = getattr(det.cfg, cfg_key)
+                if cfg_key == "max_hotspots_per_level" and cur == 0:   # automatic (rd_create)
+                    cur = 256 if det.cfg.feature == 1 else 160
+                if ov[need] > cur:
+                    p[cfg_key] = int(ov[need] * margin) + 1
+            det.close()
+        raise RuntimeError(f"capacities still overflow after {rounds} rounds: {ov}")
+
     def close(self):
         if getattr(self, "_h", None):
             lib().rd_destroy(self._h)

@@ -129,7 +129,7 @@ def test_parity_cfg3_sample(rdmod):
 def test_parity_cfg4_sample(rdmod):
     params = synth.preset(4)
     frames = synth.batch(4, 0, 0, 2)
-    det, rings = _run(rdmod, params, frames, max_entries_per_tile=6144)
+    det, rings = _run(rdmod, params, frames, max_entries_per_tile=5120, max_hotspots_per_level=256)
     for i in range(2):
         _check_frame(rdmod, det, i, params, frames[i], rings[i], full=(i < 1))
 
@@ -225,6 +225,22 @@ def test_capacity_overflow_reported(rdmod):
         assert det2.overflow()["frames_overflowed"] == 0
         for g, e in zip(got, exp):
             _compare_rings(g, e)
+
+
+def test_sized_for_iterates_to_fitting_capacities(rdmod):
+    """Detector.sized_for: from the default capacities, cfg4 (200 dense rings) overflows the ray
+    lists; the needed capacities change the Hough tiling, so resizing iterates until nothing
+    overflows, and the result equals the oracle."""
+    params = synth.preset(4)
+    frames = synth.batch(4, 0, 3, 2)
+    dev = torch.from_numpy(frames).cuda()
+    det = rdmod.Detector.sized_for(params, dev)
+    assert det.cfg.max_entries_per_tile > 3072
+    out = det.detect(dev).to_numpy()
+    det.sync()
+    exp, _ = oracle.detect_batch(oracle.params(**params), frames)
+    for g, e in zip(out, exp):
+        _compare_rings(g, e)
 
 
 def test_output_capacity_and_offsets(rdmod):
@@ -374,7 +390,7 @@ def test_rings_independent_of_hough_tiling(rdmod, env, monkeypatch):
 def test_full_batch_cfg4_dense(rdmod):
     """cfg4 at BASELINE size (512 frames of 1024x1024, 200 rings): every frame vs the oracle
     (no capacity overflow with the dense-config capacities)."""
-    params = dict(synth.preset(4), max_entries_per_tile=6144, max_hotspots_per_level=512)
+    params = dict(synth.preset(4), max_entries_per_tile=5120, max_hotspots_per_level=256)
     frames = synth.batch(4, 0, 0, 512)
     det = _det(rdmod, params, max_batch=512)
     out = det.detect(torch.from_numpy(frames).cuda()).to_numpy()
