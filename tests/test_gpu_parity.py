@@ -243,6 +243,33 @@ def test_sized_for_iterates_to_fitting_capacities(rdmod):
         _compare_rings(g, e)
 
 
+def test_api_state_and_dumps(rdmod):
+    """rd.h call order: dumps and stats describe the last rd_detect; after rd_detect_host (whose
+    chunks reuse the internal buffers) they return RD_ERR_STATE while rd_query_overflow still
+    describes that call; RD_DUMP_MEMBERS equals rd_ring_members back to back."""
+    import ctypes as C
+    params = synth.preset(2)
+    frames = synth.batch(2, 0, 5, 3)
+    det = _det(rdmod, params, max_batch=3)
+    L = rdmod.lib()
+    n = C.c_int64()
+    assert L.rd_debug_dump(det._h, 0, 0, None, 0, C.byref(n)) == rdmod._rd.RD_ERR_STATE   # no call yet
+    det.detect(torch.from_numpy(frames).cuda())
+    det.sync()
+    mem = det.ring_members(1)
+    flat = det._dump(1, rdmod._rd.RD_DUMP_MEMBERS, np.uint32)
+    both = np.concatenate([m[:, 0] | (m[:, 1] << 16) for m in mem]).astype(np.uint32)
+    assert np.array_equal(flat, both) and len(flat) > 0
+    assert L.rd_debug_dump(det._h, 0, 1, None, 0, C.byref(n)) == rdmod._rd.RD_ERR_STATE   # LEVEL_FPR needs debug
+    assert np.all(det.flags(3) == 0)
+    det.detect_host(frames)
+    assert det.overflow()["frames_overflowed"] == 0
+    for bad in (lambda: det.stats(1), lambda: det.flags(1), lambda: det.dump_ridges(0), lambda: det.ring_members(0),
+                lambda: det.sync()):
+        with pytest.raises(rdmod.RDError):
+            bad()
+
+
 def test_output_capacity_and_offsets(rdmod):
     """Compact output (rd_detect's ring_capacity_total / offsets): frames are back to back;
     a capacity one ring short of the total fails exactly the last frame with OVF_OUTPUT, and
