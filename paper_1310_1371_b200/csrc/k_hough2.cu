@@ -737,6 +737,7 @@ static cudaError_t launch2_one(int n_frames, const Params& P, int n_sm, cudaStre
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hough2<Wd, Gv, NT, MB, CB>, NT, sm);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  if (P.k2_ctas_per_sm > 0) per_sm = std::min(per_sm, P.k2_ctas_per_sm);   // leave room for concurrent kernels
   const int items = n_frames * P.ntx * P.nty;
   const int grid = std::min(items, per_sm * n_sm);
   k_hough2<Wd, Gv, NT, MB, CB><<<grid, NT, sm, st>>>(P, n_frames);

@@ -500,6 +500,7 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   P.n_sm = det->n_sm;
   P.k1_slots = k_ridges_slots(det->n_sm);
   P.force_redo = getenv("RD_K2_FORCE_REDO") ? 1 : 0;
+  P.k2_ctas_per_sm = getenv("RD_K2_CTAS") ? atoi(getenv("RD_K2_CTAS")) : 0;
   P.u8_limit = 255;
   P.ablate = getenv("RD_K2_ABLATE") ? atoi(getenv("RD_K2_ABLATE")) : 0;
   if (const char* env = getenv("RD_K2_U8_LIMIT")) P.u8_limit = std::max(1, std::min(255, atoi(env)));
