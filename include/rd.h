@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define RD_ABI_VERSION 3
+#define RD_ABI_VERSION 4
 
 typedef enum rd_status {
   RD_OK = 0,
@@ -162,7 +162,8 @@ rd_status rd_detect(rd_detector* det, const void* d_frames, int64_t pitch_bytes,
                     int32_t* d_offsets, void* stream);
 
 /* End-to-end variant on HOST buffers (pinned memory recommended): copies frames host->device
- * in chunks (at most min(48, max_batch/2) frames, the first ones smaller), up to 3 chunks ahead
+ * in chunks (at most min(48, max_batch/2) frames, the first ones smaller; behind a call in
+ * flight, see rd_submit_host, min(96, max_batch/2) frames), up to 3 chunks ahead
  * of the detection, which alternates between two internal streams working on disjoint halves of
  * the internal buffers; the rings come back compacted as in rd_detect (only the rings found
  * cross the bus).  Any n_frames >= 1.  h_rings: ring_capacity_total records; h_counts: n_frames;
@@ -171,6 +172,21 @@ rd_status rd_detect(rd_detector* det, const void* d_frames, int64_t pitch_bytes,
 rd_status rd_detect_host(rd_detector* det, const void* h_frames, int64_t pitch_bytes, int64_t frame_stride_bytes,
                          int32_t n_frames, rd_ring* h_rings, int32_t ring_capacity_total, int32_t* h_counts,
                          int32_t* h_offsets);
+
+/* Pipelined form of rd_detect_host for streams of batches (the paper's frames arriving from
+ * the camera while earlier ones are processed): rd_submit_host enqueues the
+ * same work as rd_detect_host (same arguments and outputs) and returns at once, so the copies
+ * of the next batch overlap the detection of this one; rd_wait_host completes the OLDEST
+ * submitted call: it waits for it, then fills that call's h_rings / h_counts / h_offsets and
+ * returns its status (RD_ERR_CAPACITY as rd_detect_host).  At most RD_HOST_DEPTH calls are in
+ * flight: a further rd_submit_host, rd_wait_host with none in flight, and rd_detect_host /
+ * rd_detect / every query while calls are in flight return RD_ERR_STATE.  h_frames must stay
+ * unchanged and the output buffers valid until the call's rd_wait_host returns. */
+enum { RD_HOST_DEPTH = 2 };
+rd_status rd_submit_host(rd_detector* det, const void* h_frames, int64_t pitch_bytes, int64_t frame_stride_bytes,
+                         int32_t n_frames, rd_ring* h_rings, int32_t ring_capacity_total, int32_t* h_counts,
+                         int32_t* h_offsets);
+rd_status rd_wait_host(rd_detector* det);
 
 /* Waits for the last rd_detect; RD_ERR_CAPACITY if any frame overflowed. */
 rd_status rd_sync(rd_detector* det);

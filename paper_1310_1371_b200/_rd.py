@@ -37,6 +37,7 @@ HOT_DTYPE = np.dtype([("r", "i4"), ("y", "i4"), ("x", "i4"), ("raw", "i4"), ("S"
 STATS_DTYPE = np.dtype([("ridges", "i8"), ("votes", "i8"), ("hotspots", "i8"), ("peaks", "i8")])
 FPR_DTYPE = np.dtype([("r", "i4"), ("pad", "i4"), ("votes", "i8"), ("sq", "i8"), ("pos", "i8")])
 assert RING_DTYPE.itemsize == 64 and FPR_DTYPE.itemsize == 32
+RD_HOST_DEPTH = 2   # host-path calls in flight (rd_submit_host)
 RD_DUMP_RIDGES, RD_DUMP_LEVEL_FPR, RD_DUMP_HOTSPOTS, RD_DUMP_MEMBERS = range(4)
 OVF_BITS = {"ridges": 1, "entries": 2, "hotspots": 4, "rings": 8, "debug": 16, "output": 32}
 
@@ -47,7 +48,7 @@ class rd_overflow(C.Structure):
                 ("needed_rings_per_frame", C.c_int32), ("needed_rings_total", C.c_int64)]
 
 EXPORTS = ("rd_abi_version", "rd_status_string", "rd_last_error", "rd_config_init", "rd_create", "rd_destroy",
-           "rd_detect", "rd_detect_host", "rd_sync", "rd_query_overflow", "rd_query_flags", "rd_get_stats",
+           "rd_detect", "rd_detect_host", "rd_submit_host", "rd_wait_host", "rd_sync", "rd_query_overflow", "rd_query_flags", "rd_get_stats",
            "rd_debug_dump", "rd_eigen", "rd_set_timing", "rd_kernel_times", "rd_phase_cycles", "rd_ring_members")
 
 
@@ -79,6 +80,8 @@ def lib():
         L.rd_destroy.argtypes = [vp]
         L.rd_detect.argtypes = [vp, vp, i64, i64, i32, vp, i32, vp, vp, vp]
         L.rd_detect_host.argtypes = [vp, vp, i64, i64, i32, vp, i32, vp, vp]
+        L.rd_submit_host.argtypes = [vp, vp, i64, i64, i32, vp, i32, vp, vp]
+        L.rd_wait_host.argtypes = [vp]
         L.rd_sync.argtypes = [vp]
         L.rd_query_overflow.argtypes = [vp, C.POINTER(rd_overflow)]
         L.rd_query_flags.argtypes = [vp, i32, vp]

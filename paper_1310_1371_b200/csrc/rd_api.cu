@@ -69,8 +69,8 @@ struct rd_detector {
   void* d_counters = nullptr;  // stats | peak_count | flags | dbg_count
   size_t counters_bytes = 0;
   void* d_rings_int = nullptr; // K3 output per frame, compacted into the caller's buffer by k_emit
-  int* d_need = nullptr;       // [NEED_N] capacities the call needed, then the checked-build flag
-  int* d_cursor = nullptr;     // host path: first output offset of each chunk (chained by k_scan)
+  int* d_need = nullptr;       // [1 + RD_HOST_DEPTH][NEED_N + 1] capacities a call needed, then the
+                               // checked-build flag: slot 0 rd_detect, slot 1 + j host call j
   void* d_dbg = nullptr;
   void* d_fpr = nullptr;       // debug: level fingerprints
   int* d_mem_off = nullptr;    // rd_ring_members scratch: offsets (ring_cap + 1)
@@ -78,14 +78,33 @@ struct rd_detector {
   int64_t members_cap = 0;
   cudaStream_t s_aux = nullptr;   // rd_ring_members / queries
   void* d_redo_list = nullptr;
-  // host-path staging (rings, counts and offsets come back through mapped pinned memory)
-  int chunk = 0;
-  rd_ring* h_out_rings = nullptr;   // mapped pinned: compacted rings of a host-path call
-  int64_t h_out_cap = 0;
-  int* h_out_co = nullptr;          // mapped pinned: counts [max chunk frames ...] per call (grown)
-  int64_t h_out_co_cap = 0;
-  int cursor_cap = 0;
-  int64_t last_d2h = 0;             // bytes the last host-path call read back
+  // host path: each call in flight (rd_submit_host, at most RD_HOST_DEPTH) has its own mapped
+  // pinned staging that the k_emit copies write straight into (only the rings found cross the
+  // bus), its chunk cursors and its slot of d_need; the caller's buffers are filled at the wait
+  struct HostCall {
+    rd_ring* h_stage = nullptr;   // mapped pinned: the call's compacted rings (grown)
+    int64_t stage_cap = 0;
+    int* h_co = nullptr;          // mapped pinned: counts [n] | offsets [n + 1] | flags [n] (grown)
+    int64_t co_cap = 0;
+    int* d_cursor = nullptr;      // first output offset of each chunk (chained by k_scan)
+    int cursor_cap = 0;
+    cudaEvent_t ev_end = nullptr; // the call's work on every stream is done
+    rd_ring* h_rings = nullptr;   // the caller's outputs
+    int32_t cap = 0;
+    int32_t* h_counts = nullptr;
+    int32_t* h_offsets = nullptr;
+    int n = 0;
+  };
+  HostCall hcall[RD_HOST_DEPTH];
+  int n_pend = 0, pend_head = 0;    // calls in flight, FIFO
+  uint64_t chunk_seq = 0;           // host-path chunks enqueued so far: stage and slot rotation
+  int chunk = 0;                    // largest chunk of a call with the pipeline empty (ramped up to it)
+  int chunk_pipe = 0;               // chunk of a call behind one in flight (stage buffer size)
+  int room = 0;                     // frames of the internal buffers per slot: slot b owns [b room, (b+1) room)
+  const int* last_co = nullptr;     // counts | offsets | flags of the last completed host call
+  int* need_cur = nullptr;          // d_need slot of the last call (rd_query_overflow, check flag)
+  cudaStream_t s_join = nullptr;    // joins a call's streams into its end event
+  cudaEvent_t ev_start = nullptr, ev_tail[5] = {};
   static constexpr int NSTAGE = 4;   // host-path chunk buffers: copies run up to 3 chunks ahead
   void* d_stage[NSTAGE] = {};
   cudaStream_t s_comp = nullptr, s_h2d = nullptr, s_d2h = nullptr;
@@ -449,7 +468,7 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
                         sizeof(int) * B + sizeof(int) * B;
   ALLOC(det->d_counters, det->counters_bytes);
   ALLOC(det->d_rings_int, sizeof(Ring) * B * P.ring_cap);
-  ALLOC(det->d_need, sizeof(int) * (NEED_N + 1));
+  ALLOC(det->d_need, sizeof(int) * (1 + RD_HOST_DEPTH) * (NEED_N + 1));
   ALLOC(det->d_mem_off, sizeof(int) * (P.ring_cap + 1));
   if (c.debug) {
     ALLOC(det->d_dbg, sizeof(HotRec) * B * P.dbg_cap);
@@ -544,12 +563,15 @@ rd_status rd_destroy(rd_detector* det) {
   cudaFree(det->d_counters);
   cudaFree(det->d_rings_int);
   cudaFree(det->d_need);
-  cudaFree(det->d_cursor);
   cudaFree(det->d_mem_off);
   cudaFree(det->d_members);
   cudaFree(det->d_fpr);
-  cudaFreeHost(det->h_out_rings);
-  cudaFreeHost(det->h_out_co);
+  for (auto& c : det->hcall) {
+    cudaFreeHost(c.h_stage);
+    cudaFreeHost(c.h_co);
+    cudaFree(c.d_cursor);
+    if (c.ev_end) cudaEventDestroy(c.ev_end);
+  }
   if (det->s_aux) cudaStreamDestroy(det->s_aux);
   cudaFree(det->d_dbg);
   cudaFree(det->d_redo_list);
@@ -563,6 +585,9 @@ rd_status rd_destroy(rd_detector* det) {
       if (det->s_hc[i]) cudaStreamDestroy(det->s_hc[i]);
     cudaStreamDestroy(det->s_h2d);
     cudaStreamDestroy(det->s_d2h);
+    cudaStreamDestroy(det->s_join);
+    cudaEventDestroy(det->ev_start);
+    for (cudaEvent_t e : det->ev_tail) cudaEventDestroy(e);
     for (int i = 0; i < rd_detector::NSTAGE; ++i) {
       cudaEventDestroy(det->ev_h2d[i]);
       cudaEventDestroy(det->ev_done[i]);
@@ -583,10 +608,14 @@ rd_status rd_destroy(rd_detector* det) {
 // The parameters of a call working on frames [f0, f0 + n) of the internal buffers, with the
 // K2 work counters and redo list of slot `slot` (0 or 1): two such views are disjoint, so the
 // host path can run consecutive chunks on two streams and let their kernels overlap.
-static void frame_view(const rd_detector* det, int f0, int slot, Params& V, Params& V16) {
+static void frame_view(const rd_detector* det, int f0, int slot, Params& V, Params& V16, int* need = nullptr) {
   const Params& P = det->P;
   const int64_t nb = (int64_t)P.nbx * P.nby, ntl = (int64_t)P.ntx * P.nty;
   V = P;
+  if (need) {   // the d_need slot of a host-path call
+    V.need = need;
+    V.check = need + NEED_N;
+  }
   V.bin_count += f0 * nb;
   V.bin_xy += f0 * nb * P.ridge_cap;
   V.bin_d += f0 * nb * P.ridge_cap;
@@ -616,9 +645,9 @@ static void frame_view(const rd_detector* det, int f0, int slot, Params& V, Para
 // K1 -> K1.5 -> K2 (+ 16-bit redo) -> K3 on frames [f0, f0 + n) of the internal buffers (frame
 // view of slot `slot`); K3's rings stay in the per-frame scratch until k_emit.
 static rd_status detect_impl(rd_detector* det, const void* d_frames, int64_t pitch, int64_t fstride, int n,
-                             cudaStream_t st, int f0 = 0, int slot = 0, int parts = 1) {
+                             cudaStream_t st, int f0 = 0, int slot = 0, int parts = 1, int* need = nullptr) {
   Params P, P16;
-  frame_view(det, f0, slot, P, P16);
+  frame_view(det, f0, slot, P, P16, need);
   P.parts = P16.parts = parts;
   cudaEvent_t* ev = nullptr;
   if (det->timing) {
@@ -678,9 +707,11 @@ rd_status rd_detect(rd_detector* det, const void* d_frames, int64_t pitch, int64
   rd_status s = check_frames(det, d_frames, pitch, fstride, n);
   if (s != RD_OK) return s;
   CK(cudaSetDevice(det->device));
+  if (det->n_pend) return RD_ERR_STATE;   // host-path calls in flight
   cudaStream_t st = (cudaStream_t)stream;
   if (det->have_last) CK(cudaStreamWaitEvent(st, det->ev_last, 0));   // the previous call's scratch
   det->have_last = false;
+  det->need_cur = det->d_need;
   CK(cudaMemsetAsync(det->d_need, 0, sizeof(int) * (NEED_N + 1), st));
   // A large batch runs as two halves on two internal streams (disjoint frame views of the
   // internal buffers), joined back into the caller's stream: each kernel's last partial
@@ -727,27 +758,39 @@ static rd_status ensure_host_path(rd_detector* det) {
   if (const char* env = getenv("RD_HOST_SLOTS")) slots = std::max(1, std::min(4, atoi(env)));
   det->n_slots = std::max(1, std::min(slots, det->max_batch));
   const int room = det->max_batch / det->n_slots;
-  det->chunk = std::min(room, 48);
-  if (const char* env = getenv("RD_HOST_CHUNK")) det->chunk = std::max(1, std::min(room, atoi(env)));
+  det->room = room;
   const size_t fbytes = (size_t)det->cfg.width * det->cfg.height * det->P.pixel_bytes;
+  // a call behind one in flight overlaps its copies with that call's detection, so its chunks
+  // can be large (96 frames or 256 MB: cfg3 e2e 33.5 k frames/s against 31.8 k at 48, 32.7 k at
+  // 64, 33.2 k at 128); a call into an empty pipeline ramps its chunks up to 48 frames (its fill
+  // and drain are not overlapped)
+  det->chunk_pipe = std::max(1, std::min({room, 96, (int)std::max<size_t>(1, (256u << 20) / fbytes)}));
+  det->chunk = std::min(det->chunk_pipe, 48);
+  if (const char* env = getenv("RD_HOST_CHUNK")) det->chunk = std::max(1, std::min(room, atoi(env)));
+  if (const char* env = getenv("RD_HOST_CHUNK_PIPE")) det->chunk_pipe = std::max(1, std::min(room, atoi(env)));
+  const int cmax = std::max(det->chunk, det->chunk_pipe);
   for (int i = 0; i < rd_detector::NSTAGE; ++i) {
-    CK(cudaMalloc(&det->d_stage[i], fbytes * det->chunk));
+    CK(cudaMalloc(&det->d_stage[i], fbytes * cmax));
     CK(cudaEventCreateWithFlags(&det->ev_h2d[i], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&det->ev_done[i], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&det->ev_d2h[i], cudaEventDisableTiming));
   }
+  for (auto& c : det->hcall) CK(cudaEventCreateWithFlags(&c.ev_end, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&det->ev_start, cudaEventDisableTiming));
+  for (cudaEvent_t& e : det->ev_tail) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CK(cudaStreamCreateWithFlags(&det->s_comp, cudaStreamNonBlocking));
   det->s_hc[0] = det->s_comp;
   for (int i = 1; i < det->n_slots; ++i) CK(cudaStreamCreateWithFlags(&det->s_hc[i], cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&det->s_h2d, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&det->s_d2h, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&det->s_join, cudaStreamNonBlocking));
   return RD_OK;
 }
 
 // checked builds: the first failed kernel assertion of the last call (RD_ERR_CUDA with a message)
 static rd_status check_flag(rd_detector* det) {
   int v = 0;
-  CK(cudaMemcpy(&v, det->d_need + NEED_N, sizeof(int), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&v, (det->need_cur ? det->need_cur : det->d_need) + NEED_N, sizeof(int), cudaMemcpyDeviceToHost));
   if (v) {
     snprintf(g_err, sizeof g_err, "checked build: kernel assertion %d failed at source line %d", v >> 16, v & 0xFFFF);
     return RD_ERR_CUDA;
@@ -755,66 +798,69 @@ static rd_status check_flag(rd_detector* det) {
   return RD_OK;
 }
 
-rd_status rd_detect_host(rd_detector* det, const void* h_frames, int64_t pitch, int64_t fstride, int32_t n,
+// Mapped pinned host memory of at least `want` elements of `esize` bytes (grown, contents not kept).
+static rd_status grow_mapped(void** p, int64_t* cap, int64_t want, size_t esize) {
+  want = std::max<int64_t>(want, 1);
+  if (*cap >= want) return RD_OK;
+  cudaFreeHost(*p);
+  *p = nullptr;
+  *cap = 0;
+  CK(cudaHostAlloc(p, esize * want, cudaHostAllocMapped));
+  *cap = want;
+  return RD_OK;
+}
+
+rd_status rd_submit_host(rd_detector* det, const void* h_frames, int64_t pitch, int64_t fstride, int32_t n,
                          rd_ring* h_rings, int32_t ring_cap_total, int32_t* h_counts, int32_t* h_offsets) {
   if (!det || n < 1 || !h_counts || !h_offsets || ring_cap_total < 0 || (ring_cap_total > 0 && !h_rings))
     return RD_ERR_PARAM;
   rd_status s = check_frames(det, h_frames, pitch, fstride, n);
   if (s != RD_OK) return s;
+  if (det->n_pend >= RD_HOST_DEPTH) return RD_ERR_STATE;
   CK(cudaSetDevice(det->device));
   s = ensure_host_path(det);
   if (s != RD_OK) return s;
-  // output staging: mapped pinned memory the k_emit copies write straight into (only the rings
-  // found cross the bus), grown when a call asks for more than any before
-  if (det->h_out_cap < std::max<int64_t>(ring_cap_total, 1)) {
-    cudaFreeHost(det->h_out_rings);
-    det->h_out_rings = nullptr;
-    det->h_out_cap = 0;
-    CK(cudaHostAlloc((void**)&det->h_out_rings, sizeof(rd_ring) * std::max<int64_t>(ring_cap_total, 1),
-                     cudaHostAllocMapped));
-    det->h_out_cap = std::max<int64_t>(ring_cap_total, 1);
-  }
-  if (det->h_out_co_cap < 3LL * n + 1) {   // counts [n] | offsets [n + 1] | flags [n]
-    cudaFreeHost(det->h_out_co);
-    det->h_out_co = nullptr;
-    det->h_out_co_cap = 0;
-    CK(cudaHostAlloc((void**)&det->h_out_co, sizeof(int) * (3LL * n + 1), cudaHostAllocMapped));
-    det->h_out_co_cap = 3LL * n + 1;
-  }
+  const int j = (det->pend_head + det->n_pend) % RD_HOST_DEPTH;   // the call's slot (its last user was waited for)
+  rd_detector::HostCall& c = det->hcall[j];
+  if ((s = grow_mapped((void**)&c.h_stage, &c.stage_cap, ring_cap_total, sizeof(rd_ring))) != RD_OK) return s;
+  if ((s = grow_mapped((void**)&c.h_co, &c.co_cap, 3LL * n + 1, sizeof(int))) != RD_OK) return s;
+  int* need = det->d_need + (1 + j) * (NEED_N + 1);
   const int W = det->cfg.width, H = det->cfg.height, pb = det->P.pixel_bytes;
   const size_t row = (size_t)W * pb, fbytes = row * H;
-  const int C = det->chunk;
-  // chunk sizes ramp up from a quarter chunk by 3/2 per chunk: the first copy is the only one
-  // nothing overlaps, and each copy ends before the previous (smaller) chunk's compute does
+  // chunk sizes: with the pipeline empty they ramp up from a quarter chunk by 3/2 per chunk
+  // (the first copy is the only one nothing overlaps, and each copy ends before the previous,
+  // smaller chunk's compute does); behind a call in flight every chunk is full
+  const int C = det->n_pend ? det->chunk_pipe : det->chunk, R = det->room;
   std::vector<int> cstart;
-  for (int f = 0, m = std::max(1, C / 4); f < n; f += m, m = std::min(C, std::max(m + 1, m * 3 / 2)))
+  for (int f = 0, m = det->n_pend ? C : std::max(1, C / 4); f < n; f += m, m = std::min(C, std::max(m + 1, m * 3 / 2)))
     cstart.push_back(f);
   cstart.push_back(n);
   const int nchunks = (int)cstart.size() - 1;
-  if ((int)det->cursor_cap < nchunks + 1) {
-    cudaFree(det->d_cursor);
-    det->d_cursor = nullptr;
-    CK(cudaMalloc(&det->d_cursor, sizeof(int) * (nchunks + 1)));
-    det->cursor_cap = nchunks + 1;
+  if (c.cursor_cap < nchunks + 1) {
+    cudaFree(c.d_cursor);
+    c.d_cursor = nullptr;
+    c.cursor_cap = 0;
+    CK(cudaMalloc(&c.d_cursor, sizeof(int) * (nchunks + 1)));
+    c.cursor_cap = nchunks + 1;
   }
   rd_ring* d_out_rings = nullptr;
   int* d_out_co = nullptr;
-  CK(cudaHostGetDevicePointer((void**)&d_out_rings, det->h_out_rings, 0));
-  CK(cudaHostGetDevicePointer((void**)&d_out_co, det->h_out_co, 0));
+  CK(cudaHostGetDevicePointer((void**)&d_out_rings, c.h_stage, 0));
+  CK(cudaHostGetDevicePointer((void**)&d_out_co, c.h_co, 0));
   int* d_counts_all = d_out_co;            // [n]
   int* d_offsets_all = d_out_co + n;       // [n + 1]
   int* d_flags_all = d_out_co + 2 * n + 1; // [n]
-  // the previous call on this detector (rd_detect on a caller stream) must finish first
-  if (det->have_last) {
+  // a previous rd_detect (on a caller stream) must finish first; earlier host calls are
+  // ordered chunk by chunk below (stage reuse, slot streams)
+  if (det->have_last && !det->last_host) {
     CK(cudaStreamWaitEvent(det->s_h2d, det->ev_last, 0));
     for (int i = 0; i < det->n_slots; ++i) CK(cudaStreamWaitEvent(det->s_hc[i], det->ev_last, 0));
   }
-  det->have_last = false;
-  CK(cudaMemsetAsync(det->d_need, 0, sizeof(int) * (NEED_N + 1), det->s_h2d));
-  CK(cudaMemsetAsync(det->d_cursor, 0, sizeof(int), det->s_h2d));
-  CK(cudaEventRecord(det->ev_d2h[0], det->s_h2d));   // the memsets before any chunk's kernels
-  for (int i = 0; i < det->n_slots; ++i) CK(cudaStreamWaitEvent(det->s_hc[i], det->ev_d2h[0], 0));
-  // RD_HOST_TRACE: per-chunk copy / compute times on stderr (diagnostics only)
+  CK(cudaMemsetAsync(need, 0, sizeof(int) * (NEED_N + 1), det->s_h2d));
+  CK(cudaMemsetAsync(c.d_cursor, 0, sizeof(int), det->s_h2d));
+  CK(cudaEventRecord(det->ev_start, det->s_h2d));   // the memsets before any chunk's kernels
+  for (int i = 0; i < det->n_slots; ++i) CK(cudaStreamWaitEvent(det->s_hc[i], det->ev_start, 0));
+  // RD_HOST_TRACE: per-chunk copy / compute times on stderr (diagnostics only; synchronous)
   const bool trace = getenv("RD_HOST_TRACE") != nullptr;
   std::vector<cudaEvent_t> tev;
   auto mark = [&](cudaStream_t st) {
@@ -826,12 +872,13 @@ rd_status rd_detect_host(rd_detector* det, const void* h_frames, int64_t pitch, 
   };
   for (int k = 0; k < nchunks; ++k) {
     const int f0 = cstart[k], m = cstart[k + 1] - f0;
-    // buffer slot and stream b: chunk k overlaps chunk k - 1 (other slot) and follows chunk k - 2
-    // on the same stream; stage q holds its frames
-    const int b = k % det->n_slots, q = k % rd_detector::NSTAGE;
+    // buffer slot and stream b: a chunk overlaps the previous one (other slot) and follows the
+    // one before it on the same stream; stage q holds its frames (rotation across calls)
+    const uint64_t seq = det->chunk_seq++;
+    const int b = (int)(seq % det->n_slots), q = (int)(seq % rd_detector::NSTAGE);
     cudaStream_t sc = det->s_hc[b];
-    // H2D of chunk k may overwrite stage q only after the stage's previous chunk finished computing
-    if (k >= rd_detector::NSTAGE) CK(cudaStreamWaitEvent(det->s_h2d, det->ev_done[q], 0));
+    // the H2D into stage q only after the stage's previous chunk finished computing
+    if (seq >= (uint64_t)rd_detector::NSTAGE) CK(cudaStreamWaitEvent(det->s_h2d, det->ev_done[q], 0));
     mark(det->s_h2d);
     const char* src = (const char*)h_frames + (size_t)f0 * fstride;
     if (pitch == (int64_t)row && fstride == (int64_t)fbytes) {
@@ -845,50 +892,85 @@ rd_status rd_detect_host(rd_detector* det, const void* h_frames, int64_t pitch, 
     mark(det->s_h2d);
     CK(cudaStreamWaitEvent(sc, det->ev_h2d[q], 0));
     mark(sc);
-    s = detect_impl(det, det->d_stage[q], row, fbytes, m, sc, b * C, b);
+    s = detect_impl(det, det->d_stage[q], row, fbytes, m, sc, b * R, b, 1, need);
     if (s != RD_OK) return s;
     CK(cudaEventRecord(det->ev_done[q], sc));
     // A11 for the chunk: its first offset is the previous chunk's end (chained through d_cursor)
-    if (k > 0) CK(cudaStreamWaitEvent(sc, det->ev_d2h[(k - 1) % rd_detector::NSTAGE], 0));
+    if (k > 0) CK(cudaStreamWaitEvent(sc, det->ev_d2h[(seq - 1) % rd_detector::NSTAGE], 0));
     Params V, V16;
-    frame_view(det, b * C, b, V, V16);
-    CK(launch_emit(m, V, d_out_rings, ring_cap_total, d_counts_all + f0, d_offsets_all + f0, det->d_cursor + k,
-                   det->d_cursor + k + 1, d_flags_all + f0, sc));
+    frame_view(det, b * R, b, V, V16, need);
+    CK(launch_emit(m, V, d_out_rings, ring_cap_total, d_counts_all + f0, d_offsets_all + f0, c.d_cursor + k,
+                   c.d_cursor + k + 1, d_flags_all + f0, sc));
     if (det->timing) CK(cudaEventRecord(det->tev[RD_NEV * (size_t)(det->n_timed - 1) + RD_NEV - 1], sc));
     CK(cudaEventRecord(det->ev_d2h[q], sc));
     mark(sc);
   }
-  for (int i = 0; i < det->n_slots; ++i) CK(cudaStreamSynchronize(det->s_hc[i]));
-  CK(cudaStreamSynchronize(det->s_h2d));
+  // the call's end: every stream's tail, joined on s_join (no working stream waits for it)
+  CK(cudaEventRecord(det->ev_tail[0], det->s_h2d));
+  CK(cudaStreamWaitEvent(det->s_join, det->ev_tail[0], 0));
+  for (int i = 0; i < det->n_slots; ++i) {
+    CK(cudaEventRecord(det->ev_tail[1 + i], det->s_hc[i]));
+    CK(cudaStreamWaitEvent(det->s_join, det->ev_tail[1 + i], 0));
+  }
+  CK(cudaEventRecord(c.ev_end, det->s_join));
+  CK(cudaEventRecord(det->ev_last, det->s_join));
   if (trace) {   // per chunk: h2d start/end, compute start, emit end (ms from the first copy)
+    CK(cudaEventSynchronize(c.ev_end));
     for (size_t i = 0; i + 4 <= tev.size(); i += 4) {
       float t[4];
-      for (int j = 0; j < 4; ++j) cudaEventElapsedTime(&t[j], tev[0], tev[i + j]);
+      for (int jj = 0; jj < 4; ++jj) cudaEventElapsedTime(&t[jj], tev[0], tev[i + jj]);
       fprintf(stderr, "rd: chunk %zu h2d %.3f-%.3f comp %.3f-%.3f\n", i / 4, t[0], t[1], t[2], t[3]);
     }
     for (cudaEvent_t e : tev) cudaEventDestroy(e);
   }
-  if (rd_status cs = check_flag(det)) return cs;
-  memcpy(h_counts, det->h_out_co, sizeof(int) * n);
-  memcpy(h_offsets, det->h_out_co + n, sizeof(int) * (n + 1));
-  int64_t total = 0;   // rings written: the valid frames' ranges (all inside ring_cap_total)
-  rd_status result = RD_OK;
-  for (int i = 0; i < n; ++i) {
-    if (h_counts[i] < 0) result = RD_ERR_CAPACITY;
-    else total = std::max<int64_t>(total, (int64_t)h_offsets[i] + h_counts[i]);
-  }
-  if (total > 0) memcpy(h_rings, det->h_out_rings, sizeof(rd_ring) * total);
-  CK(cudaEventRecord(det->ev_last, det->s_h2d));
+  c.h_rings = h_rings;
+  c.cap = ring_cap_total;
+  c.h_counts = h_counts;
+  c.h_offsets = h_offsets;
+  c.n = n;
+  det->n_pend++;
   det->have_last = true;
   det->last_host = true;
+  return RD_OK;
+}
+
+rd_status rd_wait_host(rd_detector* det) {
+  if (!det) return RD_ERR_PARAM;
+  if (!det->n_pend) return RD_ERR_STATE;
+  CK(cudaSetDevice(det->device));
+  const int j = det->pend_head;
+  rd_detector::HostCall& c = det->hcall[j];
+  CK(cudaEventSynchronize(c.ev_end));
+  det->pend_head = (j + 1) % RD_HOST_DEPTH;
+  det->n_pend--;
+  const int n = c.n;
+  det->need_cur = det->d_need + (1 + j) * (NEED_N + 1);
+  det->last_co = c.h_co;
   det->last_n = n;
-  det->last_d2h = total * (int64_t)sizeof(rd_ring) + sizeof(int) * (2LL * n + 1);
+  if (rd_status cs = check_flag(det)) return cs;
+  memcpy(c.h_counts, c.h_co, sizeof(int) * n);
+  memcpy(c.h_offsets, c.h_co + n, sizeof(int) * (n + 1));
+  int64_t total = 0;   // rings written: the valid frames' ranges (all inside the capacity)
+  rd_status result = RD_OK;
+  for (int i = 0; i < n; ++i) {
+    if (c.h_counts[i] < 0) result = RD_ERR_CAPACITY;
+    else total = std::max<int64_t>(total, (int64_t)c.h_offsets[i] + c.h_counts[i]);
+  }
+  if (total > 0) memcpy(c.h_rings, c.h_stage, sizeof(rd_ring) * total);
   return result;
+}
+
+rd_status rd_detect_host(rd_detector* det, const void* h_frames, int64_t pitch, int64_t fstride, int32_t n,
+                         rd_ring* h_rings, int32_t ring_cap_total, int32_t* h_counts, int32_t* h_offsets) {
+  if (det && det->n_pend) return RD_ERR_STATE;
+  rd_status s = rd_submit_host(det, h_frames, pitch, fstride, n, h_rings, ring_cap_total, h_counts, h_offsets);
+  if (s != RD_OK) return s;
+  return rd_wait_host(det);
 }
 
 rd_status rd_sync(rd_detector* det) {
   if (!det) return RD_ERR_PARAM;
-  if (!det->have_last || det->last_host) return RD_ERR_STATE;
+  if (!det->have_last || det->last_host || det->n_pend) return RD_ERR_STATE;
   CK(cudaSetDevice(det->device));
   CK(cudaEventSynchronize(det->ev_last));
   if (rd_status cs = check_flag(det)) return cs;
@@ -901,11 +983,11 @@ rd_status rd_sync(rd_detector* det) {
 
 rd_status rd_query_overflow(rd_detector* det, rd_overflow* out) {
   if (!det || !out) return RD_ERR_PARAM;
-  if (!det->have_last) return RD_ERR_STATE;
+  if (!det->have_last || det->n_pend) return RD_ERR_STATE;
   CK(cudaSetDevice(det->device));
   CK(cudaEventSynchronize(det->ev_last));
   int need[NEED_N];
-  CK(cudaMemcpy(need, det->d_need, sizeof need, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(need, det->need_cur, sizeof need, cudaMemcpyDeviceToHost));
   memset(out, 0, sizeof *out);
   out->needed_ridges_per_tile = need[NEED_RIDGES];
   out->needed_entries_per_tile = need[NEED_ENTRIES];
@@ -914,9 +996,9 @@ rd_status rd_query_overflow(rd_detector* det, rd_overflow* out) {
   const int n = det->last_n;
   std::vector<int> counts(n), offsets(n + 1), flags(n, 0);
   if (det->last_host) {   // the host path leaves counts, offsets and flags in its mapped staging
-    memcpy(counts.data(), det->h_out_co, sizeof(int) * n);
-    memcpy(offsets.data(), det->h_out_co + n, sizeof(int) * (n + 1));
-    memcpy(flags.data(), det->h_out_co + 2 * n + 1, sizeof(int) * n);
+    memcpy(counts.data(), det->last_co, sizeof(int) * n);
+    memcpy(offsets.data(), det->last_co + n, sizeof(int) * (n + 1));
+    memcpy(flags.data(), det->last_co + 2 * n + 1, sizeof(int) * n);
   } else {
     CK(cudaMemcpy(flags.data(), det->P.flags, sizeof(int) * n, cudaMemcpyDeviceToHost));
     std::vector<int> pk(n);
@@ -937,7 +1019,7 @@ rd_status rd_query_overflow(rd_detector* det, rd_overflow* out) {
 
 rd_status rd_query_flags(rd_detector* det, int32_t n, int32_t* h_flags) {
   if (!det || !h_flags || n < 1) return RD_ERR_PARAM;
-  if (!det->have_last || det->last_host) return RD_ERR_STATE;
+  if (!det->have_last || det->last_host || det->n_pend) return RD_ERR_STATE;
   if (n > det->last_n) return RD_ERR_PARAM;
   CK(cudaSetDevice(det->device));
   CK(cudaEventSynchronize(det->ev_last));
@@ -947,7 +1029,7 @@ rd_status rd_query_flags(rd_detector* det, int32_t n, int32_t* h_flags) {
 
 rd_status rd_get_stats(rd_detector* det, int32_t n, rd_frame_stats* h) {
   if (!det || !h || n < 1 || n > det->max_batch) return RD_ERR_PARAM;
-  if (!det->have_last || det->last_host) return RD_ERR_STATE;
+  if (!det->have_last || det->last_host || det->n_pend) return RD_ERR_STATE;
   if (n > det->last_n) return RD_ERR_PARAM;
   static_assert(sizeof(rd_frame_stats) == sizeof(Stats), "stats layout");
   CK(cudaSetDevice(det->device));
@@ -987,7 +1069,7 @@ rd_status rd_ring_members(rd_detector* det, int32_t frame, int32_t* h_offsets, i
   if (!det || !n_total || frame < 0 || frame >= det->max_batch || offsets_cap < 0 || cap < 0 ||
       (offsets_cap > 0 && !h_offsets) || (cap > 0 && !h_members))
     return RD_ERR_PARAM;
-  if (!det->have_last || det->last_host || frame >= det->last_n) return RD_ERR_STATE;
+  if (!det->have_last || det->last_host || det->n_pend || frame >= det->last_n) return RD_ERR_STATE;
   CK(cudaSetDevice(det->device));
   int npk = 0, total = 0;
   rd_status s = members_impl(det, frame, &npk, &total);
@@ -1007,7 +1089,7 @@ rd_status rd_debug_dump(rd_detector* det, int32_t frame, int32_t what, void* h_b
   if (!det || !n_out || frame < 0 || frame >= det->max_batch || cap_bytes < 0 || (cap_bytes > 0 && !h_buf))
     return RD_ERR_PARAM;
   if (what < RD_DUMP_RIDGES || what > RD_DUMP_MEMBERS) return RD_ERR_PARAM;
-  if (!det->have_last || det->last_host || frame >= det->last_n) return RD_ERR_STATE;
+  if (!det->have_last || det->last_host || det->n_pend || frame >= det->last_n) return RD_ERR_STATE;
   if ((what == RD_DUMP_LEVEL_FPR || what == RD_DUMP_HOTSPOTS) && !det->cfg.debug) return RD_ERR_STATE;
   CK(cudaSetDevice(det->device));
   CK(cudaEventSynchronize(det->ev_last));

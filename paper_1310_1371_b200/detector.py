@@ -1,4 +1,4 @@
-"""Detector: Python face of rd_create / rd_detect / rd_detect_host (include/rd.h).
+"""Detector: Python face of rd_create / rd_detect / rd_detect_host / rd_submit_host (include/rd.h).
 
 Argument marshalling only: every step of the path runs in librd.so's CUDA kernels.
 """
@@ -132,10 +132,7 @@ class Detector:
                               C.c_void_p(st.cuda_stream)), "rd_detect")
         return out
 
-    def detect_host(self, frames, out: RingBatch | None = None, capacity: int | None = None) -> RingBatch:
-        """End-to-end on host buffers (numpy or CPU torch tensor, pinned recommended): the library
-        copies frames in, detects and returns the compacted rings, overlapping copies with compute.
-        Returns RingBatch of host arrays (rings as RING_DTYPE records)."""
+    def _host_args(self, frames, out, capacity):
         if isinstance(frames, torch.Tensor):
             assert not frames.is_cuda
             ptr, n = frames.data_ptr(), frames.shape[0]
@@ -153,11 +150,38 @@ class Detector:
 
         def ptr_of(x):
             return x.data_ptr() if isinstance(x, torch.Tensor) else x.ctypes.data
-        cap = out.rings.shape[0]
-        st = lib().rd_detect_host(self._h, ptr, pitch, fstride, n, ptr_of(out.rings), cap, ptr_of(out.counts),
-                                  ptr_of(out.offsets))
+        args = (self._h, ptr, pitch, fstride, n, ptr_of(out.rings), out.rings.shape[0], ptr_of(out.counts),
+                ptr_of(out.offsets))
+        return frames, out, args
+
+    def detect_host(self, frames, out: RingBatch | None = None, capacity: int | None = None) -> RingBatch:
+        """End-to-end on host buffers (numpy or CPU torch tensor, pinned recommended): the library
+        copies frames in, detects and returns the compacted rings, overlapping copies with compute.
+        Returns RingBatch of host arrays (rings as RING_DTYPE records)."""
+        frames, out, args = self._host_args(frames, out, capacity)
+        st = lib().rd_detect_host(*args)
         if st not in (_rd.RD_OK, _rd.RD_ERR_CAPACITY):
             check(st, "rd_detect_host")
+        return out
+
+    def submit_host(self, frames, out: RingBatch | None = None, capacity: int | None = None) -> RingBatch:
+        """Pipelined detect_host (rd_submit_host): enqueues the call and returns at once; the
+        returned RingBatch is filled by the wait_host() that completes this call (calls complete in
+        submission order, at most _rd.RD_HOST_DEPTH in flight).  `frames` is kept referenced
+        until then."""
+        frames, out, args = self._host_args(frames, out, capacity)
+        check(lib().rd_submit_host(*args), "rd_submit_host")
+        if not hasattr(self, "_pending"):
+            self._pending = []
+        self._pending.append((frames, out))
+        return out
+
+    def wait_host(self) -> RingBatch:
+        """Completes the oldest submit_host call (rd_wait_host) and returns its RingBatch."""
+        st = lib().rd_wait_host(self._h)
+        frames, out = self._pending.pop(0) if getattr(self, "_pending", None) else (None, None)
+        if st not in (_rd.RD_OK, _rd.RD_ERR_CAPACITY):
+            check(st, "rd_wait_host")
         return out
 
     def sync(self, raise_on_overflow=True):

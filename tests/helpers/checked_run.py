@@ -2,7 +2,7 @@
 
 Invoked by tests/test_checked.py in a subprocess (the library is loaded once per process).
 Cases: cfg1, cfg2 batch, cfg3 frames through the byte-counter pass and the forced 16-bit redo
-pass, the host path, the edge variant, and r_max = 100 (K_r >= 16).  Every kernel index is
+pass, the host path (synchronous and pipelined), the edge variant, and r_max = 100 (K_r >= 16).  Every kernel index is
 bounds-checked (RD_CHECKED); rd_sync / rd_detect_host report a failed check as RD_ERR_CUDA.
 With RD_JITTER=1 the Hough kernel's warps sleep pseudo-random times at every phase start, so
 the shared-memory protocol between phases runs under perturbed schedules.  Prints one line per
@@ -32,9 +32,18 @@ def same(got, exp):
         np.max(np.abs(got[k] - exp[k])) <= 1e-4 for k in ("fx", "fy", "fr", "rms")) if len(exp) else True
 
 
-def run(name, params, frames, host=False):
-    det = rd.Detector(dict(params, debug=1), max_batch=len(frames))
-    if host:
+def run(name, params, frames, host=False, pipelined=False):
+    det = rd.Detector(dict(params, debug=1), max_batch=len(frames) if not pipelined else 4)
+    if pipelined:   # three calls, two in flight (rd_submit_host / rd_wait_host), then the middle one
+        outs = [det.submit_host(frames), det.submit_host(frames[::-1].copy())]
+        det.wait_host()
+        outs.append(det.submit_host(frames))
+        det.wait_host()
+        det.wait_host()
+        rev = outs[1].to_numpy()[::-1]
+        out = outs[2].to_numpy()
+        assert all(a is not None and a.tobytes() == b.tobytes() for a, b in zip(out, rev)), name
+    elif host:
         out = det.detect_host(frames).to_numpy()
     else:
         out = det.detect(torch.from_numpy(np.ascontiguousarray(frames)).cuda()).to_numpy()
@@ -50,6 +59,7 @@ run("cfg1", synth.preset(1), np.stack([synth.frame(1, 0, i)[0] for i in range(2)
 run("cfg2", synth.preset(2), synth.batch(2, 0, 0, 4))
 run("cfg3", synth.preset(3), synth.batch(3, 0, 0, 3))
 run("cfg3-host", synth.preset(3), synth.batch(3, 0, 10, 5), host=True)
+run("cfg2-pipelined", synth.preset(2), synth.batch(2, 0, 20, 9), pipelined=True)
 run("cfg2-edges", synth.edge_preset(2), synth.batch(2, 0, 0, 2))
 W = H = 320
 sc = synth.scene(W, H, pixel_bytes=2, max_value=4095, background=100, sigma_p=1.5, read_sigma=8, poisson=1)

@@ -34,7 +34,7 @@ def test_exports_match_header(rdlib):
 
 def test_status_strings_and_version(rdlib):
     L = rdlib.lib()
-    assert L.rd_abi_version() == 3
+    assert L.rd_abi_version() == 4
     for s in range(7):
         assert len(L.rd_status_string(s)) > 0
 
@@ -65,6 +65,8 @@ def test_null_arguments(rdlib):
     assert L.rd_create(None, 1, 0, None) == rdlib.RD_ERR_PARAM
     assert L.rd_detect(None, None, 0, 0, 1, None, 0, None, None, None) == rdlib.RD_ERR_PARAM
     assert L.rd_detect_host(None, None, 0, 0, 1, None, 0, None, None) == rdlib.RD_ERR_PARAM
+    assert L.rd_submit_host(None, None, 0, 0, 1, None, 0, None, None) == rdlib.RD_ERR_PARAM
+    assert L.rd_wait_host(None) == rdlib.RD_ERR_PARAM
     assert L.rd_sync(None) == rdlib.RD_ERR_PARAM
     assert L.rd_query_overflow(None, None) == rdlib.RD_ERR_PARAM
     assert L.rd_debug_dump(None, 0, 0, None, 0, None) == rdlib.RD_ERR_PARAM

@@ -368,6 +368,72 @@ def test_detect_host_many_chunks_two_slots(rdmod, force_redo, monkeypatch):
         assert host_out[i].tobytes() == ref[i].tobytes()
 
 
+@pytest.mark.parametrize("force_redo", [False, True])
+def test_submit_host_pipelined_equals_device_path(rdmod, force_redo, monkeypatch):
+    """rd_submit_host / rd_wait_host: five calls of different frames and sizes with two in
+    flight (the copies of a call overlap the previous call's detection, its chunks continue
+    the stage and slot rotation) give every frame the device path's rings, the oldest call
+    completing first; also when every frame takes the 16-bit redo pass."""
+    if force_redo:
+        monkeypatch.setenv("RD_K2_FORCE_REDO", "1")
+    params = synth.preset(2)
+    sizes = [19, 7, 1, 23, 12]
+    batches = [synth.batch(2, 100 + i, 100 + i + m, m) for i, m in enumerate(sizes)]
+    det = _det(rdmod, params, max_batch=8)
+    ref = []
+    for b in batches:
+        r = []
+        for i in range(0, len(b), 8):
+            r += det.detect(torch.from_numpy(b[i:i + 8]).cuda()).to_numpy()
+            det.sync()
+        ref.append(r)
+    pinned = [torch.from_numpy(b).pin_memory() for b in batches]
+    got, outs = [], []
+    for i, p in enumerate(pinned):
+        outs.append(det.submit_host(p))
+        if i >= 1:
+            got.append(det.wait_host())
+    got.append(det.wait_host())
+    assert [g is o for g, o in zip(got, outs)] == [True] * len(sizes)
+    for b, (g, r) in enumerate(zip(got, ref)):
+        g = g.to_numpy()
+        assert len(g) == sizes[b]
+        for i in range(sizes[b]):
+            assert g[i].tobytes() == r[i].tobytes(), (b, i)
+    assert det.overflow()["frames_overflowed"] == 0
+
+
+def test_submit_host_state_rules(rdmod):
+    """rd.h: at most RD_HOST_DEPTH calls in flight; waiting with none in flight, and
+    rd_detect_host / rd_detect / queries with calls in flight are RD_ERR_STATE; after the
+    waits rd_detect and rd_query_overflow work and describe the right call."""
+    L, R = rdmod.lib(), rdmod._rd
+    params = synth.preset(2)
+    frames = synth.batch(2, 0, 6, 6)
+    det = _det(rdmod, params, max_batch=6)
+    assert L.rd_wait_host(det._h) == R.RD_ERR_STATE
+    a = det.submit_host(frames)
+    b = det.submit_host(frames[:3], capacity=1)   # too small: RD_ERR_CAPACITY at its wait
+    with pytest.raises(rdmod.RDError):
+        det.submit_host(frames)
+    for bad in (lambda: det.detect_host(frames), lambda: det.detect(torch.from_numpy(frames).cuda()),
+                lambda: det.overflow(), lambda: det.sync()):
+        with pytest.raises(rdmod.RDError) as e:
+            bad()
+        assert e.value.status == R.RD_ERR_STATE
+    assert det.wait_host() is a and np.all(a.counts >= 0)
+    with pytest.raises(rdmod.RDError):   # b still in flight
+        det.overflow()
+    assert det.wait_host() is b
+    assert b.counts[0] == -1 or b.counts[0] <= 1
+    ov = det.overflow()
+    assert ov["frames_overflowed"] >= 1 and ov["needed_rings_total"] == a.offsets[3]
+    dev = det.detect(torch.from_numpy(frames).cuda())
+    det.sync()
+    assert np.array_equal(dev.counts.cpu().numpy(), a.counts)
+    assert L.rd_wait_host(det._h) == R.RD_ERR_STATE
+
+
 @pytest.mark.parametrize("cfg", [2, 3])
 def test_ring_members_match_annulus_definition(rdmod, cfg):
     """rd_ring_members (A9): every ring's members are exactly the oracle's ridge pixels in
