@@ -124,7 +124,7 @@ size_t k_hough2_layout(Params& P, int G, int nt, int cb) {
   L.k = o;     o = al16(o + 4 * (size_t)nlev);
   L.tn = o;    o = al16(o + 8 * (size_t)nlev);
   L.dummy = o; o = al16(o + 4 * 32);
-  L.wsm = o;
+  L.mbar = o;  o = al16(o + 8);          // completion of the tile's bulk ray copies
   L.total = (int)o;
   L.rawp_magic = (uint32_t)((1ull << 32) / (uint64_t)L.rawp + 1);
   return o;
@@ -158,6 +158,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
   int* tK = SM(int, k);                         // [nlev] K_r
   double* tTn = SM(double, tn);                 // [nlev] T_norm(r)
   uint32_t* dummy_w = SM(uint32_t, dummy);      // [32] targets of masked-out votes (+0)
+  uint64_t* mbar = SM(uint64_t, mbar);          // bulk ray copies of a tile
 #undef SM
   const int nlev = P.n_levels;
   int* cnt = hcnt + nlev;
@@ -206,6 +207,14 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
     cnt[i] = 0;
     dummy_w[i] = 0;
   }
+  // the tile's resident rays arrive by bulk copies (TMA engine) when every array slice is
+  // 16-byte aligned (entry_cap and rcap multiples of 4), else by per-thread cp.async
+  const bool bulk = ((P.entry_cap | rcap) & 3) == 0;
+  uint32_t mpar = 0;   // mbarrier phase
+  if (tid == 0) {
+    mbar_init(mbar, 1);
+    mbar_fence_init();
+  }
   __syncthreads();
 
   for (;;) {
@@ -243,12 +252,28 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
       }
     };
     // the tile's rays (up to rcap) become resident in shared memory
-    for (int e = tid; e < min(ne, rcap); e += NT) {
-      cp_async16(&sd[e], P.ray_d + gbase + e);
-      cp_async4(&sxy[e], P.ray_xy + gbase + e);
-      cp_async4(&rr_s[e], P.ray_r + gbase + e);
+    const int nres = min(ne, rcap);
+    if (bulk) {
+      if (nres > 0) {
+        if (tid == 0) {
+          const int n4 = (nres + 3) & ~3;   // x | y and the intervals: whole 16-byte lines (n4 <= rcap)
+          fence_proxy_async_smem();         // this CTA's reads of the previous tile's rays (behind a barrier) first
+          mbar_expect_tx(mbar, (uint32_t)(16 * nres + 8 * n4));
+          bulk_g2s(sd, P.ray_d + gbase, 16u * nres, mbar);
+          bulk_g2s(sxy, P.ray_xy + gbase, 4u * n4, mbar);
+          bulk_g2s(rr_s, P.ray_r + gbase, 4u * n4, mbar);
+        }
+        mbar_wait(mbar, mpar);
+        mpar ^= 1u;
+      }
+    } else {
+      for (int e = tid; e < nres; e += NT) {
+        cp_async16(&sd[e], P.ray_d + gbase + e);
+        cp_async4(&sxy[e], P.ray_xy + gbase + e);
+        cp_async4(&rr_s[e], P.ray_r + gbase + e);
+      }
+      cp_async_wait_all();
     }
-    cp_async_wait_all();
     __syncthreads();
     setup(0, 0);
     PMARK(0);

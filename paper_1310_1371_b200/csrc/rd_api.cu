@@ -382,6 +382,7 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
           }
         }
         Q.k2_rcap = std::min(Q.k2_rcap, Q.entry_cap);
+        if (Q.k2_rcap >= 4) Q.k2_rcap &= ~3;   // whole 16-byte lines of 4-byte ray fields (K2 bulk copies)
         k_hough2_layout(Q, s.G, s.nt, cb);
         G = s.G;
         nt = s.nt;

@@ -41,7 +41,7 @@ struct Ring {          // == rd_ring (64 B)
 struct K2Layout {
   int cb, raws, rawp, lvlc;   // counter bytes, raw rows, row pitch (cells), cells per level
   int rawc;                   // raw columns (tile width + 2 halo); raws = tile height + 2 halo
-  int raw, hS, sd, rr, xy, hcell, hraw, task, cand, cdef, act, hcnt, w, k, tn, dummy, wsm, total;
+  int raw, hS, sd, rr, xy, hcell, hraw, task, cand, cdef, act, hcnt, w, k, tn, dummy, mbar, total;
   uint32_t rawp_magic;        // ceil(2^32 / rawp): cell / rawp = umulhi(cell, magic) for cells < 2^16
 };
 
@@ -186,6 +186,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// 1-D bulk copy (TMA engine) of `bytes` (a multiple of 16; 16-byte aligned ends) from global
+// to shared memory; completes on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
 }
 // 3-D tiled TMA load of box (x, y, z) of the tensor map into shared memory; completes on `bar`
 __device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, uint64_t* bar, int x, int y, int z) {
