@@ -25,7 +25,7 @@ for r in rows[1:]:
 tot = sum(sum(v) for v in d.values())
 out = ["ncu launch list (gpu__time_duration.sum, --clock-control none) of `python bench.py --steps 2 --warmup 3 --no-cpu`",
        f"(profiles/launches_{TAG}.csv): cold-cache, serialised per-launch times over all launches of that run (warm-up,",
-       "timed steps, the debug pass and the 64-frame e2e chunks); the shares are what must agree with bench.py.", "",
+       "timed steps, the debug pass and the host-path chunks of the e2e runs); the shares are what must agree with bench.py.", "",
        "| kernel | launches | mean us | share |", "|---|---|---|---|"]
 for k, v in sorted(d.items(), key=lambda x: -sum(x[1])):
     out.append(f"| {k} | {len(v)} | {sum(v) / len(v) / 1e3:.1f} | {100 * sum(v) / tot:.1f}% |")
