@@ -41,16 +41,20 @@ __device__ __forceinline__ void half_ge(float a, float b, float& lo, float& hi) 
 }
 }  // namespace
 
-// One CTA per (row of ridge bins, frame), one warp per bin at a time (32 rays per pass).
+// One warp per (ridge bin, frame) (32 rays per pass), K15_WPB warps per CTA: small CTAs, so a
+// CTA's slot is not held by warps that finished while another one still walks a busy bin.
 // The clip of a ray's level interval splits into frame constraints (per ray), row
 // constraints (per tile row ty) and column constraints (per tile column tx), so the inner
 // tile loop evaluates two half-planes with precomputed reciprocals.
-#ifndef RD_K15_MINB
-#define RD_K15_MINB 4   // 64 registers: occupancy decides this latency-bound kernel
+#ifndef RD_K15_WPB
+#define RD_K15_WPB 1
 #endif
-__global__ void __launch_bounds__(256, RD_K15_MINB) k_rays(Params P) {
+constexpr int K15_WPB = RD_K15_WPB;
+#ifndef RD_K15_MINB
+#define RD_K15_MINB (32 / RD_K15_WPB)   // 64 registers: occupancy decides this latency-bound kernel
+#endif
+__global__ void __launch_bounds__(32 * K15_WPB, RD_K15_MINB) k_rays(Params P) {
   const int f = blockIdx.y;
-  const int by = blockIdx.x;
   const int TX = P.k2t, TY = P.k2ty, hal = P.hal, W = P.W, H = P.H;
   const int rlo = P.r_lo, rhi = P.r_hi;
   const float m = P.k_slope, c = P.k_icpt;
@@ -58,14 +62,15 @@ __global__ void __launch_bounds__(256, RD_K15_MINB) k_rays(Params P) {
   const int64_t tile0 = (int64_t)f * P.ntx * P.nty;
   // tiles any ray of a bin can reach: |offset| <= r_hi, halo <= hal
   const int reach = rhi + hal + 1;
-  const int wy0 = max((by * T1 - reach) / TY, 0), wy1 = min((by * T1 + T1 - 1 + reach) / TY, P.nty - 1);
   int my_votes = 0, need_r = 0;
-  for (int bx = warp; bx < P.nbx; bx += blockDim.x >> 5) {
+  const int bin = blockIdx.x * K15_WPB + warp;
+  if (bin < P.nbx * P.nby) {
+    const int by = bin / P.nbx, bx = bin - by * P.nbx;
+    const int wy0 = max((by * T1 - reach) / TY, 0), wy1 = min((by * T1 + T1 - 1 + reach) / TY, P.nty - 1);
     const int64_t fb = (int64_t)f * P.nbx * P.nby + by * P.nbx + bx;
     const int cnt_all = P.bin_count[fb];   // the true count: ridges beyond ridge_cap were not stored
     need_r = max(need_r, cnt_all);
     const int cnt = min(cnt_all, P.ridge_cap);
-    if (cnt == 0) continue;
     const int wx0 = max((bx * T1 - reach) / TX, 0), wx1 = min((bx * T1 + T1 - 1 + reach) / TX, P.ntx - 1);
     for (int j0 = 0; j0 < 2 * cnt; j0 += 32) {
       const int j = j0 + lane;
@@ -195,7 +200,7 @@ __global__ void __launch_bounds__(256, RD_K15_MINB) k_rays(Params P) {
 }
 
 cudaError_t launch_rays(int n_frames, const Params& P, cudaStream_t st) {
-  k_rays<<<dim3(P.nby, n_frames), 256, 0, st>>>(P);
+  k_rays<<<dim3((P.nbx * P.nby + K15_WPB - 1) / K15_WPB, n_frames), 32 * K15_WPB, 0, st>>>(P);
   return cudaGetLastError();
 }
 
