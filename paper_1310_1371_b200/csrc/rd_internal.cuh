@@ -87,7 +87,7 @@ struct Params {
   int* redo_list;               // redo pass only: [0] count, [1..] frames; null in the main pass
   int force_redo;               // test knob (RD_K2_FORCE_REDO): every frame takes the 16-bit redo pass
   int ablate;                   // timing experiments only (RD_K2_ABLATE bits: 1 no window sums, 2 no NMS, 4 no S tasks,
-                                //   8 no vote atomics, 16 no votes)
+                                //   8 no vote atomics, 16 no votes, 32 integer fixed-point vote targets)
   int u8_limit;                 // byte-counter value that triggers the redo (255; RD_K2_U8_LIMIT in tests)
   int k2_rcap;                  // K2: rays of a tile resident in shared memory (the rest read from global)
   int k2_ctas_per_sm;           // K2: resident CTAs per SM of a launch (0: as many as fit)
