@@ -41,6 +41,13 @@ inline size_t al16(size_t v) { return (v + 15) & ~size_t(15); }
 #ifndef RD_K2_HSL
 #define RD_K2_HSL 0
 #endif
+#ifndef RD_K2_TMA_CLEAR
+#define RD_K2_TMA_CLEAR 1   // clear the level buffers by a bulk copy of zeros instead of 16-byte stores
+#endif
+#ifndef RD_K2_LP
+#define RD_K2_LP 2   // steps per active-ray listing (rays idle in one step of the pair vote masked)
+#endif
+constexpr int LP = RD_K2_LP;
 
 constexpr int HSL = RD_K2_HSL;   // byte-counter S tasks: lanes per hotspot (power of two <= 32; 0: per step)
 constexpr int SMALL_K = 7;   // window rows 2K+1 <= 15: a half-warp per hotspot
@@ -88,7 +95,7 @@ size_t k_hough2_layout(Params& P, int G, int nt, int cb) {
   L.k = o;     o = al16(o + 4 * (size_t)nlev);
   L.tn = o;    o = al16(o + 8 * (size_t)nlev);
   L.dummy = o; o = al16(o + 4 * 32);
-  L.mbar = o;  o = al16(o + 8);          // completion of the tile's bulk ray copies
+  L.mbar = o;  o = al16(o + 16);         // [0] the tile's bulk ray copies, [1] the level-buffer clear
   L.total = (int)o;
   L.rawp_magic = (uint32_t)((1ull << 32) / (uint64_t)L.rawp + 1);
   return o;
@@ -175,8 +182,11 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
   // 16-byte aligned (entry_cap and rcap multiples of 4), else by per-thread cp.async
   const bool bulk = ((P.entry_cap | rcap) & 3) == 0;
   uint32_t mpar = 0;   // mbarrier phase
+  uint32_t cpar = 0;   // clear mbarrier phase
+  bool clear_pending = false;   // a bulk clear of the level buffers is in flight (RD_K2_TMA_CLEAR)
   if (tid == 0) {
     mbar_init(mbar, 1);
+    mbar_init(mbar + 1, 1);
     mbar_fence_init();
   }
   __syncthreads();
@@ -199,9 +209,9 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
     const int64_t gbase = tl * P.entry_cap;
     int my_hot = 0;   // interior hotspots (the per-frame vote count comes from K1.5)
 
-    // list the rays active in the step starting at level L0s (count: s_nact[p])
+    // list the rays active in the LP steps starting at level L0s (count: s_nact[p])
     auto setup = [&](int L0s, int p) {
-      const int Lhs = min(L0s + G - 1, nlev - 1);
+      const int Lhs = min(L0s + LP * G - 1, nlev - 1);
       for (int e0 = warp * 32; e0 < ne; e0 += NT) {
         const int e = e0 + lane;
         const uint32_t rr = e < ne ? (e < rcap ? rr_s[e] : __ldg(P.ray_r + gbase + e)) : 0xFFFFu;
@@ -244,20 +254,26 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
 
     for (int L0 = 0, step = 0; L0 < nlev; L0 += G, ++step) {
       const int Lhi = min(L0 + G - 1, nlev - 1);
-      const int par = step & 1;
+      const int par = step & 1, lpar = (step / LP) & 1;   // step parity, listing parity
+      const bool list_next = (step + 1) % LP == 0;       // this step lists the next LP steps' rays
       __syncthreads();
       PMARK(1);
       if (tid == 0) {   // counters whose last reader is behind the barrier above; first used after the next
-        s_nact[par ^ 1] = 0;
+        s_nact[lpar ^ 1] = 0;
         s_ncand[0] = 0;
         s_ndef[par] = 0;
       }
 #ifdef RD_CHECKED
       if (P.jitter) __nanosleep(((unsigned)(warp * 2654435761u + step * 40503u + blockIdx.x * 97u) >> 7) & 2047u);
 #endif
+      if (RD_K2_TMA_CLEAR && clear_pending) {   // the previous step's levels are zero again
+        mbar_wait(mbar + 1, cpar);
+        cpar ^= 1u;
+        clear_pending = false;
+      }
       // ---------------- (1) votes of levels L0..Lhi
       {
-        const int nact = s_nact[par];
+        const int nact = s_nact[lpar];
         const double rb0 = (double)(P.r_lo + L0);
         int slot_of[G];   // hotspot-list slot of each level of the step
 #pragma unroll
@@ -384,7 +400,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
       //     each hotspot and the candidate test
       {
 #if !RD_K2_SETUP3
-        if (L0 + G < nlev) setup(L0 + G, par ^ 1);
+        if (L0 + G < nlev && list_next) setup(L0 + G, lpar ^ 1);
 #endif
         if (CB == 1) {
           // byte counters: HSL lanes per hotspot, lane hl sums window rows hl, hl + HSL, ...;
@@ -616,9 +632,17 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
       }
       {
 #if RD_K2_SETUP3 == 1
-        if (L0 + G < nlev) setup(L0 + G, par ^ 1);
+        if (L0 + G < nlev && list_next) setup(L0 + G, lpar ^ 1);
 #endif
-        {   // clear the step's level buffers
+        if (RD_K2_TMA_CLEAR) {   // clear the step's level buffers: one bulk copy of zeros (TMA engine)
+          if (tid == 0) {
+            const uint32_t nb = (uint32_t)(CB * min(G, nlev - L0) * lvlc);   // the levels the step used
+            fence_proxy_async_smem();   // the S phase's reads (behind the barrier above) before the async writes
+            mbar_expect_tx(mbar + 1, nb);
+            bulk_g2s(raw32, P.zeros, nb, mbar + 1);
+          }
+          clear_pending = true;
+        } else {   // clear the step's level buffers
           uint4* r4 = reinterpret_cast<uint4*>(raw32);
           constexpr int U = 4;
           const int n16 = (CB * min(G, nlev - L0) * lvlc) / 16;   // the levels the step used
@@ -634,7 +658,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
           s_ntask[1] = 0;
         }
 #if RD_K2_SETUP3 == 2
-        if (L0 + G < nlev) setup(L0 + G, par ^ 1);
+        if (L0 + G < nlev && list_next) setup(L0 + G, lpar ^ 1);
 #endif
         const int nd = (L0 > 0 && !(ABL & 2)) ? s_ndef[par ^ 1] : 0, nc = (ABL & 2) ? 0 : s_ncand[0];
         for (int p = warp; p < nd + nc; p += NW) {
@@ -703,6 +727,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
       if (P.prof) atomicAdd(&P.prof[15], 1ull);
     }
   }
+  if (RD_K2_TMA_CLEAR && clear_pending) mbar_wait(mbar + 1, cpar);   // no bulk write may outlive the CTA
   if (tid == 0 && need_e) atomicMax(&P.need[NEED_ENTRIES], need_e);
   if (tid == 0 && need_h) atomicMax(&P.need[NEED_HOTSPOTS], need_h);
   if (P.prof && tid == 0) {

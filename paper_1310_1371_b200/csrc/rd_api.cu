@@ -78,6 +78,7 @@ struct rd_detector {
   int64_t members_cap = 0;
   cudaStream_t s_aux = nullptr;   // rd_ring_members / queries
   void* d_redo_list = nullptr;
+  void* d_zeros = nullptr;      // zero block the K2 level buffers are cleared from
   // host path: each call in flight (rd_submit_host, at most RD_HOST_DEPTH) has its own mapped
   // pinned staging that the k_emit copies write straight into (only the rings found cross the
   // bus), its chunk cursors and its slot of d_need; the caller's buffers are filled at the wait
@@ -471,6 +472,13 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   ALLOC(det->d_rings_int, sizeof(Ring) * B * P.ring_cap);
   ALLOC(det->d_need, sizeof(int) * (1 + RD_HOST_DEPTH) * (NEED_N + 1));
   ALLOC(det->d_mem_off, sizeof(int) * (P.ring_cap + 1));
+  {   // zeros the Hough kernel's level buffers are cleared from (bulk copies, K2 phase 3)
+    const size_t zb = (size_t)std::max(P.k2o.total, det->P16.k2o.total);
+    ALLOC(det->d_zeros, zb);
+    e = cudaMemset(det->d_zeros, 0, zb);
+    if (e != cudaSuccess) { rd_destroy(det); return cuda_fail(e, "cudaMemset zeros"); }
+    P.zeros = det->d_zeros;
+  }
   if (c.debug) {
     ALLOC(det->d_dbg, sizeof(HotRec) * B * P.dbg_cap);
     ALLOC(det->d_fpr, sizeof(unsigned long long) * 3 * B * P.n_levels);
@@ -576,6 +584,7 @@ rd_status rd_destroy(rd_detector* det) {
   if (det->s_aux) cudaStreamDestroy(det->s_aux);
   cudaFree(det->d_dbg);
   cudaFree(det->d_redo_list);
+  cudaFree(det->d_zeros);
   cudaFree(det->d_prof);
   for (int i = 0; i < rd_detector::NSTAGE; ++i) {
     cudaFree(det->d_stage[i]);

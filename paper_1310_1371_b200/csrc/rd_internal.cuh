@@ -91,6 +91,7 @@ struct Params {
   int u8_limit;                 // byte-counter value that triggers the redo (255; RD_K2_U8_LIMIT in tests)
   int k2_rcap;                  // K2: rays of a tile resident in shared memory (the rest read from global)
   int k2_ctas_per_sm;           // K2: resident CTAs per SM of a launch (0: as many as fit)
+  const void* zeros;            // K2: a zero block at least as large as its level buffers (bulk-copy clears)
   K2Layout k2o;
   int ring_cap;
   Peak* peaks;                  // [F][ring_cap]
