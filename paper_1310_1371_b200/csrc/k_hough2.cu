@@ -41,9 +41,6 @@ inline size_t al16(size_t v) { return (v + 15) & ~size_t(15); }
 #ifndef RD_K2_HSL
 #define RD_K2_HSL 0
 #endif
-#ifndef RD_K2_TMA_CLEAR
-#define RD_K2_TMA_CLEAR 1   // clear the level buffers by a bulk copy of zeros instead of 16-byte stores
-#endif
 #ifndef RD_K2_LP
 #define RD_K2_LP 2   // steps per active-ray listing (rays idle in one step of the pair vote masked)
 #endif
@@ -90,8 +87,9 @@ size_t k_hough2_layout(Params& P, int G, int nt, int cb) {
   L.cand = o;  o = al16(o + 2 * (size_t)G * hot_cap);
   L.cdef = o;  o = al16(o + 2 * 2 * (size_t)hot_cap);
   L.act = o;   o = al16(o + 2 * (size_t)P.entry_cap);   // one list: written in phase (2), read in (1)
-  L.hcnt = o;  o = al16(o + 4 * (size_t)(nlev + 32));
+  L.hcnt = o;  o = al16(o + 4 * (size_t)(nlev + 16));
   L.w = o;     o = al16(o + 2 * (size_t)nlev * P.wstride);
+  L.wst = o;   o = al16(o + (cb == 1 ? 32 * (size_t)P.wp_nw * G : 0));   // the step's dp4a weight words (bulk copy)
   L.k = o;     o = al16(o + 4 * (size_t)nlev);
   L.tn = o;    o = al16(o + 8 * (size_t)nlev);
   L.dummy = o; o = al16(o + 4 * 32);
@@ -175,7 +173,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
     for (int i = tid; i < (CB * G * lvlc) / 16; i += NT) r4[i] = make_uint4(0, 0, 0, 0);
   }
   for (int i = tid; i < 32; i += NT) {
-    cnt[i] = 0;
+    if (i < 16) cnt[i] = 0;
     dummy_w[i] = 0;
   }
   // the tile's resident rays arrive by bulk copies (TMA engine) when every array slice is
@@ -183,13 +181,28 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
   const bool bulk = ((P.entry_cap | rcap) & 3) == 0;
   uint32_t mpar = 0;   // mbarrier phase
   uint32_t cpar = 0;   // clear mbarrier phase
-  bool clear_pending = false;   // a bulk clear of the level buffers is in flight (RD_K2_TMA_CLEAR)
+  bool clear_pending = false;   // bulk copies on mbar[1] (clear, weight words) are in flight
   if (tid == 0) {
     mbar_init(mbar, 1);
     mbar_init(mbar + 1, 1);
     mbar_fence_init();
   }
   __syncthreads();
+  // byte counters: the dp4a weight words of a step's levels (all four row alignments, one
+  // contiguous block of the table) are bulk-copied into shared memory one step ahead, with the
+  // clear, on mbar[1]; the first tile's first step's here
+  const uint32_t wlev = CB == 1 ? 32u * (uint32_t)P.wp_nw : 0u;   // bytes per level
+  auto issue_w = [&](int L0s) {   // (one thread; the caller has armed mbar[1] for the bytes)
+    const uint32_t nb = wlev * (uint32_t)min(G, nlev - L0s);
+    if (nb) bulk_g2s(smem + P.k2o.wst, P.lvlWP + (size_t)L0s * 8 * P.wp_nw, nb, mbar + 1);
+  };
+  if (CB == 1) {
+    if (tid == 0) {
+      mbar_expect_tx(mbar + 1, wlev * (uint32_t)min(G, nlev));
+      issue_w(0);
+    }
+    clear_pending = true;
+  }
 
   for (;;) {
     if (tid == 0) *s_item = atomicAdd(redo_pass ? P.k2_work + 1 : P.k2_work, 1);
@@ -266,7 +279,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
 #ifdef RD_CHECKED
       if (P.jitter) __nanosleep(((unsigned)(warp * 2654435761u + step * 40503u + blockIdx.x * 97u) >> 7) & 2047u);
 #endif
-      if (RD_K2_TMA_CLEAR && clear_pending) {   // the previous step's levels are zero again
+      if (clear_pending) {   // the previous step's levels are zero again, this step's weight words staged
         mbar_wait(mbar + 1, cpar);
         cpar ^= 1u;
         clear_pending = false;
@@ -440,12 +453,13 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
             const int iy = c >> 8, ix = c & 0xFF;
             const int cx0 = ix - 1 + hal - K;        // first window column (raw-local)
             const int al = cx0 & 3, nw = (al + 2 * K + 4) >> 2;
-            const uint32_t* wp = P.lvlWP + (size_t)((li * 4 + al) * P.wp_nw) * 2;
-            uint32_t wl[NWW], wh[NWW];   // (staging them in shared memory a step ahead measured slower:
-#pragma unroll                            //  fewer resident rays, 16.33 vs 16.13 us/frame)
+            const uint2* wp = reinterpret_cast<const uint2*>(smem + P.k2o.wst) + (size_t)(g * 4 + al) * P.wp_nw;
+            uint32_t wl[NWW], wh[NWW];   // (bulk-copied a step ahead: 32 B per level and word)
+#pragma unroll
             for (int k = 0; k < NWW; ++k) {
-              wl[k] = k < nw ? __ldg(wp + 2 * k) : 0u;
-              wh[k] = k < nw ? __ldg(wp + 2 * k + 1) : 0u;
+              const uint2 w2 = k < nw ? wp[k] : make_uint2(0u, 0u);
+              wl[k] = w2.x;
+              wh[k] = w2.y;
             }
             const uint16_t* w = tW + li * P.wstride;
             const uint32_t* lvlw = raw32 + ((g * lvlc) >> 2);
@@ -634,24 +648,16 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
 #if RD_K2_SETUP3 == 1
         if (L0 + G < nlev && list_next) setup(L0 + G, lpar ^ 1);
 #endif
-        if (RD_K2_TMA_CLEAR) {   // clear the step's level buffers: one bulk copy of zeros (TMA engine)
+        {   // clear the step's level buffers: one bulk copy of zeros (TMA engine)
           if (tid == 0) {
             const uint32_t nb = (uint32_t)(CB * min(G, nlev - L0) * lvlc);   // the levels the step used
+            const int Ln = L0 + G < nlev ? L0 + G : 0;   // the next step (of this tile or the next one)
             fence_proxy_async_smem();   // the S phase's reads (behind the barrier above) before the async writes
-            mbar_expect_tx(mbar + 1, nb);
+            mbar_expect_tx(mbar + 1, nb + wlev * (uint32_t)min(G, nlev - Ln));
             bulk_g2s(raw32, P.zeros, nb, mbar + 1);
+            issue_w(Ln);
           }
           clear_pending = true;
-        } else {   // clear the step's level buffers
-          uint4* r4 = reinterpret_cast<uint4*>(raw32);
-          constexpr int U = 4;
-          const int n16 = (CB * min(G, nlev - L0) * lvlc) / 16;   // the levels the step used
-          int i = tid;
-          for (; i + (U - 1) * NT < n16; i += U * NT) {
-#pragma unroll
-            for (int u = 0; u < U; ++u) r4[i + u * NT] = make_uint4(0u, 0u, 0u, 0u);
-          }
-          for (; i < n16; i += NT) r4[i] = make_uint4(0u, 0u, 0u, 0u);
         }
         if (tid == 0) {
           s_ntask[0] = 0;
@@ -727,7 +733,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
       if (P.prof) atomicAdd(&P.prof[15], 1ull);
     }
   }
-  if (RD_K2_TMA_CLEAR && clear_pending) mbar_wait(mbar + 1, cpar);   // no bulk write may outlive the CTA
+  if (clear_pending) mbar_wait(mbar + 1, cpar);   // no bulk write may outlive the CTA
   if (tid == 0 && need_e) atomicMax(&P.need[NEED_ENTRIES], need_e);
   if (tid == 0 && need_h) atomicMax(&P.need[NEED_HOTSPOTS], need_h);
   if (P.prof && tid == 0) {

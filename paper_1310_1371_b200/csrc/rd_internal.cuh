@@ -41,7 +41,7 @@ struct Ring {          // == rd_ring (64 B)
 struct K2Layout {
   int cb, raws, rawp, lvlc;   // counter bytes, raw rows, row pitch (cells), cells per level
   int rawc;                   // raw columns (tile width + 2 halo); raws = tile height + 2 halo
-  int raw, hS, sd, rr, xy, hcell, hraw, task, cand, cdef, act, hcnt, w, k, tn, dummy, mbar, total;
+  int raw, hS, sd, rr, xy, hcell, hraw, task, cand, cdef, act, hcnt, w, wst, k, tn, dummy, mbar, total;
   uint32_t rawp_magic;        // ceil(2^32 / rawp): cell / rawp = umulhi(cell, magic) for cells < 2^16
 };
 
