@@ -421,10 +421,14 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
           // weights for the row's alignment (w = 64 wh + wl): exact integer S as below
           constexpr int NWW = 9;   // weight words per row: (3 + 2K + 1 + 3) / 4 <= 9 for K <= 15
           // S tasks: the step's level lists back to back (task t -> level g, list index h)
-          auto lcount = [&](int g) { return L0 + g < nlev ? min(hcnt[L0 + g], hot_cap) : 0; };
+          // the step's level counts, once (task decode below uses the prefix sums)
+          int pre[G];   // pre[g] = tasks of levels 0 .. g
           int ntask = 0;
 #pragma unroll
-          for (int g = 0; g < G; ++g) ntask += lcount(g);
+          for (int g = 0; g < G; ++g) {
+            ntask += L0 + g < nlev ? min(hcnt[L0 + g], hot_cap) : 0;
+            pre[g] = ntask;
+          }
           if (ABL & 4) ntask = 0;
 #if RD_K2_HSL == 0
           // lanes per hotspot: the widest power of two that still gives every warp its share
@@ -440,12 +444,10 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
             const int t = t0 + grp;
             const bool valid = t < ntask;
             const int tv = valid ? t : t0;
-            int g = 0, h = tv, cum = 0;
+            int g = 0, h = tv;
 #pragma unroll
-            for (int gg = 0; gg < G - 1; ++gg) {
-              cum += lcount(gg);
-              if (tv >= cum) g = gg + 1, h = tv - cum;
-            }
+            for (int gg = 0; gg < G - 1; ++gg)
+              if (tv >= pre[gg]) g = gg + 1, h = tv - pre[gg];
             const int tk = (g << 12) | h;
             const int li = L0 + g, sl = li % NSLOT;
             const int K = tK[li];
