@@ -106,26 +106,39 @@ __global__ void __launch_bounds__(32 * K15_WPB, RD_K15_MINB) k_rays(Params P) {
         // round of atomics (lane k: tile k), then write; one global round trip per 32 rays
         uint32_t rng[9];
         unsigned kbal = 0, hits = 0;
+        // a tile's clip is the intersection of a row part (frame + the tile row's two
+        // half-planes) and a column part (the tile column's two), each evaluated once per row or
+        // column, branch-free against the four slopes' reciprocals (per ray)
+        const float ay1 = fv + m, ay2 = m - fv, ax1 = fu + m, ax2 = m - fu;
+        const float iy1 = ay1 != 0.f ? __frcp_rn(ay1) : 0.f, iy2 = ay2 != 0.f ? __frcp_rn(ay2) : 0.f;
+        const float ix1 = ax1 != 0.f ? __frcp_rn(ax1) : 0.f, ix2 = ax2 != 0.f ? __frcp_rn(ax2) : 0.f;
+        auto clip = [](float a, float ia, float b, float& lo, float& hi) {   // a r >= b (as half_ge)
+          const float t = b * ia;
+          lo = a > 0.f ? fmaxf(lo, t) : lo;
+          hi = a < 0.f ? fminf(hi, t) : ((a == 0.f && b > 0.f) ? -1e30f : hi);
+        };
+        float xlo[3], xhi[3];
+#pragma unroll
+        for (int kx = 0; kx < 3; ++kx) {
+          const int X0 = (wx0 + kx) * TX;
+          xlo[kx] = -1e30f;
+          xhi[kx] = 1e30f;
+          clip(ax1, ix1, (float)X0 - 1.5f - c - fx, xlo[kx], xhi[kx]);
+          clip(ax2, ix2, fx - (float)(X0 + TX) - 0.5f - c, xlo[kx], xhi[kx]);
+        }
 #pragma unroll
         for (int ky = 0; ky < 3; ++ky) {
           const int ty = wy0 + ky, Y0 = ty * TY;
           float ylo = flo, yhi = fhi;
-          half_ge(fv + m, (float)Y0 - 1.5f - c - fy, ylo, yhi);
-          half_ge(m - fv, fy - (float)(Y0 + TY) - 0.5f - c, ylo, yhi);
+          clip(ay1, iy1, (float)Y0 - 1.5f - c - fy, ylo, yhi);
+          clip(ay2, iy2, fy - (float)(Y0 + TY) - 0.5f - c, ylo, yhi);
           const bool yhit = valid && ty <= wy1 && sy1 >= Y0 && sy0 <= Y0 + TY - 1 && yhi >= ylo - 2.f;
 #pragma unroll
           for (int kx = 0; kx < 3; ++kx) {
             const int k = 3 * ky + kx, tx = wx0 + kx, X0 = tx * TX;
-            bool hit = yhit && tx <= wx1 && sx1 >= X0 && sx0 <= X0 + TX - 1;
-            int ra = 0, rb = -1;
-            if (hit) {
-              float lo = ylo, hi = yhi;
-              half_ge(fu + m, (float)X0 - 1.5f - c - fx, lo, hi);
-              half_ge(m - fu, fx - (float)(X0 + TX) - 0.5f - c, lo, hi);
-              ra = max((int)floorf(lo) - 1, rlo);
-              rb = min((int)ceilf(hi) + 1, rhi);
-              hit = hi >= lo - 2.f && ra <= rb;
-            }
+            const float lo = fmaxf(ylo, xlo[kx]), hi = fminf(yhi, xhi[kx]);
+            const int ra = max((int)floorf(lo) - 1, rlo), rb = min((int)ceilf(hi) + 1, rhi);
+            const bool hit = yhit && tx <= wx1 && sx1 >= X0 && sx0 <= X0 + TX - 1 && hi >= lo - 2.f && ra <= rb;
             rng[k] = (uint32_t)(ra - rlo) | ((uint32_t)(rb - rlo) << 16);
             const unsigned bal = __ballot_sync(0xffffffffu, hit);
             if (lane == k) kbal = bal;
