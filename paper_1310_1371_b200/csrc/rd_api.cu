@@ -424,9 +424,9 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
     }
   }
   if (k_ridges_smem(P.Ks) > smax || det->G == 0 || k_fit_smem(P) > smax) {
-    delete det;
     snprintf(g_err, sizeof g_err, "shared memory: K1 %zu K3 %zu (limit %zu); K2 %s", k_ridges_smem(P.Ks),
              k_fit_smem(P), smax, det->G ? "fits" : "no persistent shape fits (halo K_max + 1 or capacities too large)");
+    delete det;
     return RD_ERR_CONFIG;
   }
 
