@@ -25,9 +25,9 @@ __device__ __forceinline__ bool inframe_at(int c, double d, int n, int r) {
   const int t = c + rnd_half_away(__dmul_rn((double)r, d));
   return t >= 0 && t <= n - 1;
 }
-__device__ int inframe_prefix(int c, double d, int n, int rlo, int rhi) {
-  const float fd = (float)d;
-  const float lim = fd > 0.f ? ((float)n - 0.5f - (float)c) / fd : fd < 0.f ? (-0.5f - (float)c) / fd : 1e9f;
+__device__ int inframe_prefix(int c, double d, float inv_d, int n, int rlo, int rhi) {
+  const float fd = (float)d;   // (inv_d = 1 / fd, 0 if fd = 0)
+  const float lim = fd > 0.f ? ((float)n - 0.5f - (float)c) * inv_d : fd < 0.f ? (-0.5f - (float)c) * inv_d : 1e9f;
   int r = (int)fminf(fmaxf(floorf(lim), (float)(rlo - 1)), (float)rhi);
   while (r < rhi && inframe_at(c, d, n, r + 1)) ++r;
   while (r >= rlo && !inframe_at(c, d, n, r)) --r;
@@ -39,6 +39,13 @@ __device__ __forceinline__ void half_ge(float a, float b, float& lo, float& hi) 
   else if (a < 0.f) hi = fminf(hi, __fdividef(b, a));
   else if (b > 0.f) hi = -1e30f;
 }
+// the same half-plane a r >= b, branch-free, with ia = 1 / a (0 if a = 0)
+__device__ __forceinline__ void clip(float a, float ia, float b, float& lo, float& hi) {
+  const float t = b * ia;
+  lo = a > 0.f ? fmaxf(lo, t) : lo;
+  hi = a < 0.f ? fminf(hi, t) : ((a == 0.f && b > 0.f) ? -1e30f : hi);
+}
+__device__ __forceinline__ float rcp0(float a) { return a != 0.f ? __frcp_rn(a) : 0.f; }
 }  // namespace
 
 // One warp per (ridge bin, frame) (32 rays per pass), K15_WPB warps per CTA: small CTAs, so a
@@ -85,17 +92,18 @@ __global__ void __launch_bounds__(32 * K15_WPB, RD_K15_MINB) k_rays(Params P) {
       const double sgn = (j & 1) ? -1.0 : 1.0;
       const int x = (int)(xy & 0xFFFFu), y = (int)(xy >> 16);
       const double u = sgn * d.x, v = sgn * d.y;
+      const float fu = (float)u, fv = (float)v, fx = (float)x, fy = (float)y;
+      const float iu = rcp0(fu), iv = rcp0(fv);
       if (valid) {   // the ray's in-frame votes (per-frame vote count)
-        const int px = inframe_prefix(x, u, W, rlo, rhi), py = inframe_prefix(y, v, H, rlo, rhi);
+        const int px = inframe_prefix(x, u, iu, W, rlo, rhi), py = inframe_prefix(y, v, iv, H, rlo, rhi);
         my_votes += max(0, min(px, py) - rlo + 1);
       }
-      const float fu = (float)u, fv = (float)v, fx = (float)x, fy = (float)y;
       // frame constraints (tile independent)
       float flo = (float)rlo, fhi = (float)rhi;
-      half_ge(fu, -0.5f - fx, flo, fhi);
-      half_ge(-fu, fx - (float)W + 0.5f, flo, fhi);
-      half_ge(fv, -0.5f - fy, flo, fhi);
-      half_ge(-fv, fy - (float)H + 0.5f, flo, fhi);
+      clip(fu, iu, -0.5f - fx, flo, fhi);
+      clip(-fu, -iu, fx - (float)W + 0.5f, flo, fhi);
+      clip(fv, iv, -0.5f - fy, flo, fhi);
+      clip(-fv, -iv, fy - (float)H + 0.5f, flo, fhi);
       // bounding box of the target segment, widened by the largest halo and rounding
       const float ax = fx + fu * rlo, bxp = fx + fu * rhi, ay = fy + fv * rlo, byp = fy + fv * rhi;
       const float sx0 = fminf(ax, bxp) - hal - 1.f, sx1 = fmaxf(ax, bxp) + hal + 1.f;
@@ -110,13 +118,7 @@ __global__ void __launch_bounds__(32 * K15_WPB, RD_K15_MINB) k_rays(Params P) {
         // half-planes) and a column part (the tile column's two), each evaluated once per row or
         // column, branch-free against the four slopes' reciprocals (per ray)
         const float ay1 = fv + m, ay2 = m - fv, ax1 = fu + m, ax2 = m - fu;
-        const float iy1 = ay1 != 0.f ? __frcp_rn(ay1) : 0.f, iy2 = ay2 != 0.f ? __frcp_rn(ay2) : 0.f;
-        const float ix1 = ax1 != 0.f ? __frcp_rn(ax1) : 0.f, ix2 = ax2 != 0.f ? __frcp_rn(ax2) : 0.f;
-        auto clip = [](float a, float ia, float b, float& lo, float& hi) {   // a r >= b (as half_ge)
-          const float t = b * ia;
-          lo = a > 0.f ? fmaxf(lo, t) : lo;
-          hi = a < 0.f ? fminf(hi, t) : ((a == 0.f && b > 0.f) ? -1e30f : hi);
-        };
+        const float iy1 = rcp0(ay1), iy2 = rcp0(ay2), ix1 = rcp0(ax1), ix2 = rcp0(ax2);
         float xlo[3], xhi[3];
 #pragma unroll
         for (int kx = 0; kx < 3; ++kx) {
