@@ -462,6 +462,31 @@ def test_ring_members_match_annulus_definition(rdmod, cfg):
             assert key == sorted(key)
 
 
+@pytest.mark.parametrize("n", [193, 200])
+def test_batch_parts_do_not_change_results(rdmod, n, monkeypatch):
+    """rd_detect runs a large batch as two or three parts on internal streams (frame views of
+    the internal buffers; three from 192 frames).  Ragged part boundaries and every part count
+    give the same ring lists, counts and per-frame counters as one part."""
+    params = synth.preset(2)
+    frames = torch.from_numpy(synth.batch(2, 0, 0, n)).cuda()
+    det = _det(rdmod, params, max_batch=n)
+    monkeypatch.setenv("RD_SPLIT", "1")
+    ref = det.detect(frames).to_numpy()
+    det.sync()
+    ref_st = det.stats(n)
+    for split in ("2", "3", "4", None):
+        if split is None:
+            monkeypatch.delenv("RD_SPLIT")
+        else:
+            monkeypatch.setenv("RD_SPLIT", split)
+        out = det.detect(frames).to_numpy()
+        det.sync()
+        assert [a.tobytes() for a in out] == [a.tobytes() for a in ref], split
+        st = det.stats(n)
+        for k in ("ridges", "votes", "hotspots", "peaks"):
+            assert np.array_equal(st[k], ref_st[k]), (split, k)
+
+
 @pytest.mark.parametrize("env", [("RD_K2_SQUARE", "1"), ("RD_K2_TILE", "86,77"), ("RD_K2_TILE", "200,60")])
 def test_rings_independent_of_hough_tiling(rdmod, env, monkeypatch):
     """The Hough tiling (square, rectangular, thin) changes how K1.5 routes rays and K2
