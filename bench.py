@@ -185,6 +185,13 @@ def _init_dist(args):
     return torch, dist, rank, local, world, dev
 
 
+def _parts(n: int) -> int:
+    """Parts rd_detect splits a batch of n frames into (rd_api.cu detect: 3 from 192 frames, 2
+    from 128); each part launches K1, K1.5, K2, the redo reset, the 16-bit K2 pass and K3, and
+    the call adds k_scan and k_copy."""
+    return 3 if n >= 192 else 2 if n >= 128 else 1
+
+
 def _max_over_ranks(torch, dist, world, dev, v: float) -> float:
     if world > 1:
         t = torch.tensor([v], device=dev, dtype=torch.float64)
@@ -393,7 +400,7 @@ def run_gpu(args):
                     "synchronous_value": round(e2e_sync, 1)},
             # K1, K1.5, K2, K2 redo reset, K2 redo pass, K3 per part (a batch of >= 128 frames runs
             # as two halves) + k_scan and k_copy per call
-            "gpu_launches": (6 * (2 if B >= 128 else 1) + 2) * args.steps,
+            "gpu_launches": (6 * _parts(B) + 2) * args.steps,
             "clocks": clocks}
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -488,7 +495,7 @@ def run_sweep(args):
             "compute_plus_gather": {"value": round(N / ((sweep_ms + gms) / 1e3), 1), "gather_ms": round(gms, 3),
                                     "records": int(recs.shape[0])},
             "gathered_sha256": sha, "parity": parity, "clocks": clocks,
-            "gpu_launches": (6 * 2 + 2) * nb * args.steps}
+            "gpu_launches": (6 * _parts(B) + 2) * nb * args.steps}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
