@@ -79,6 +79,7 @@ size_t k_hough2_layout(Params& P, int G, int nt, int cb) {
   L.sd = o;    o = al16(o + 16 * (size_t)P.k2_rcap);
   L.rr = o;    o = al16(o + 4 * (size_t)P.k2_rcap);
   L.xy = o;    o = al16(o + 4 * (size_t)P.k2_rcap);
+  L.rr16 = o;  o = al16(o + (P.k2_rr16 ? 2 * (size_t)P.entry_cap : 0));   // every entry's 2-byte interval
   L.hcell = o; o = al16(o + 2 * (size_t)NSLOT * hot_cap);
   // byte counters keep a hotspot's raw count in the low byte of its S word and take their
   // S tasks straight from the level lists: no raw or task arrays
@@ -99,7 +100,7 @@ size_t k_hough2_layout(Params& P, int G, int nt, int cb) {
   return o;
 }
 
-template <bool kWide, int G, int NT, int MINB, int CB>
+template <bool kWide, int G, int NT, int MINB, int CB, bool R16>
 __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Params P, int n_frames) {
   constexpr int NSLOT = G + 2;
   constexpr int NW = NT / 32;
@@ -116,6 +117,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
   double2* sd = SM(double2, sd);                // [rcap] the tile's rays: (s*dx, s*dy)
   uint32_t* rr_s = SM(uint32_t, rr);            // [rcap] level interval ra | rb<<16
   uint32_t* sxy = SM(uint32_t, xy);             // [rcap] x | y<<16 (frame coordinates)
+  uint16_t* rr16 = SM(uint16_t, rr16);          // [entry_cap] ra | rb<<8 of every entry (Params::k2_rr16)
   uint16_t* hcell = SM(uint16_t, hcell);        // [NSLOT][hot_cap] iy<<8 | ix (ring coordinates)
   uint16_t* hraw = SM(uint16_t, hraw);          // [NSLOT][hot_cap] raw count
   uint16_t* tasks = SM(uint16_t, task);         // [G*hot_cap] g<<12 | h (small K front, large K back)
@@ -222,12 +224,13 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
     const int64_t gbase = tl * P.entry_cap;
     int my_hot = 0;   // interior hotspots (the per-frame vote count comes from K1.5)
 
+    auto rr_of16 = [&](int e) { const uint32_t v = rr16[e]; return (v & 0xFFu) | ((v >> 8) << 16); };
     // list the rays active in the LP steps starting at level L0s (count: s_nact[p])
     auto setup = [&](int L0s, int p) {
       const int Lhs = min(L0s + LP * G - 1, nlev - 1);
       for (int e0 = warp * 32; e0 < ne; e0 += NT) {
         const int e = e0 + lane;
-        const uint32_t rr = e < ne ? (e < rcap ? rr_s[e] : __ldg(P.ray_r + gbase + e)) : 0xFFFFu;
+        const uint32_t rr = e < ne ? (R16 ? rr_of16(e) : e < rcap ? rr_s[e] : __ldg(P.ray_r + gbase + e)) : 0xFFFFu;
         const bool a = (int)(rr & 0xFFFFu) <= Lhs && (int)(rr >> 16) >= L0s;
         const unsigned bal = __ballot_sync(FULL, a);
         if (!bal) continue;
@@ -240,7 +243,18 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
     };
     // the tile's rays (up to rcap) become resident in shared memory
     const int nres = min(ne, rcap);
-    if (bulk) {
+    if (R16) {   // every entry's interval (2 bytes) by one bulk copy; no resident rays (Params::k2_rr16)
+      if (ne > 0) {
+        if (tid == 0) {
+          const int n8 = (ne + 7) & ~7;   // whole 16-byte lines (n8 <= entry_cap, a multiple of 8)
+          fence_proxy_async_smem();
+          mbar_expect_tx(mbar, (uint32_t)(2 * n8));
+          bulk_g2s(rr16, reinterpret_cast<const uint16_t*>(P.ray_r) + gbase, 2u * n8, mbar);
+        }
+        mbar_wait(mbar, mpar);
+        mpar ^= 1u;
+      }
+    } else if (bulk) {
       if (nres > 0) {
         if (tid == 0) {
           const int n4 = (nres + 3) & ~3;   // x | y and the intervals: whole 16-byte lines (n4 <= rcap)
@@ -310,7 +324,11 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
             if (i < nact) {
               const int e = act[i];
               RD_CHECK(e >= 0 && e < ne, CK_K2_RAY);
-              if (e < rcap) {
+              if (R16) {   // interval resident, pixel and direction from L2
+                rr = rr_of16(e);
+                xy = __ldg(P.ray_xy + gbase + e);
+                d = __ldg(P.ray_d + gbase + e);
+              } else if (e < rcap) {
                 d = sd[e];
                 xy = sxy[e];
                 rr = rr_s[e];
@@ -765,20 +783,20 @@ __global__ void k_redo_reset(Params P, int n_frames) {
   if (threadIdx.x == 0) P.redo_list[0] = n;
 }
 
-template <bool Wd, int Gv, int NT, int MB, int CB>
+template <bool Wd, int Gv, int NT, int MB, int CB, bool R16>
 static cudaError_t launch2_one(int n_frames, const Params& P, int n_sm, cudaStream_t st) {
   const size_t sm = (size_t)P.k2o.total;
   cudaError_t e =
-      cudaFuncSetAttribute(k_hough2<Wd, Gv, NT, MB, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      cudaFuncSetAttribute(k_hough2<Wd, Gv, NT, MB, CB, R16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hough2<Wd, Gv, NT, MB, CB>, NT, sm);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hough2<Wd, Gv, NT, MB, CB, R16>, NT, sm);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   if (P.k2_ctas_per_sm > 0) per_sm = std::min(per_sm, P.k2_ctas_per_sm);   // leave room for concurrent kernels
   const int items = n_frames * P.ntx * P.nty;
   const int grid = std::min(items, per_sm * n_sm);
-  k_hough2<Wd, Gv, NT, MB, CB><<<grid, NT, sm, st>>>(P, n_frames);
+  k_hough2<Wd, Gv, NT, MB, CB, R16><<<grid, NT, sm, st>>>(P, n_frames);
   return cudaGetLastError();
 }
 
@@ -798,9 +816,11 @@ cudaError_t launch_hough2(int n_frames, const Params& P, bool wide, int G, int n
   const int key = (cb << 20) | (G << 12) | (nt << 2) | (minb << 1) | (wide ? 1 : 0);
 #define CASE(CBv, Gv, NTv, MBv)                                                                       \
   case (CBv << 20) | (Gv << 12) | (NTv << 2) | (MBv << 1) | 0:                                       \
-    return launch2_one<false, Gv, NTv, MBv, CBv>(n_frames, P, n_sm, st);                          \
+    return P.k2_rr16 ? launch2_one<false, Gv, NTv, MBv, CBv, true>(n_frames, P, n_sm, st)          \
+                     : launch2_one<false, Gv, NTv, MBv, CBv, false>(n_frames, P, n_sm, st);        \
   case (CBv << 20) | (Gv << 12) | (NTv << 2) | (MBv << 1) | 1:                                       \
-    return launch2_one<true, Gv, NTv, MBv, CBv>(n_frames, P, n_sm, st);
+    return P.k2_rr16 ? launch2_one<true, Gv, NTv, MBv, CBv, true>(n_frames, P, n_sm, st)           \
+                     : launch2_one<true, Gv, NTv, MBv, CBv, false>(n_frames, P, n_sm, st);
   switch (key) {
     CASE(1, 4, 384, 2)
     CASE(1, 4, 512, 2)

@@ -161,7 +161,8 @@ __global__ void __launch_bounds__(32 * K15_WPB, RD_K15_MINB) k_rays(Params P) {
             const int64_t o = (tile0 + (wy0 + k / 3) * P.ntx + wx0 + k % 3) * P.entry_cap + e;
             P.ray_d[o] = make_double2(u, v);
             P.ray_xy[o] = xy;
-            P.ray_r[o] = rng[k];
+            if (P.k2_rr16) reinterpret_cast<uint16_t*>(P.ray_r)[o] = (uint16_t)((rng[k] & 0xFFu) | ((rng[k] >> 16) << 8));
+            else P.ray_r[o] = rng[k];
           } else {
             atomicOr(&P.flags[f], OVF_ENTRIES);
           }
@@ -199,7 +200,8 @@ __global__ void __launch_bounds__(32 * K15_WPB, RD_K15_MINB) k_rays(Params P) {
             const int64_t o = t * P.entry_cap + e;
             P.ray_d[o] = make_double2(u, v);
             P.ray_xy[o] = xy;
-            P.ray_r[o] = (uint32_t)(ra - rlo) | ((uint32_t)(rb - rlo) << 16);
+            if (P.k2_rr16) reinterpret_cast<uint16_t*>(P.ray_r)[o] = (uint16_t)((ra - rlo) | ((rb - rlo) << 8));
+            else P.ray_r[o] = (uint32_t)(ra - rlo) | ((uint32_t)(rb - rlo) << 16);
           } else {
             atomicOr(&P.flags[f], OVF_ENTRIES);
           }

@@ -333,6 +333,9 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
       std::sort(cand.begin(), cand.end());
       return cand;
     };
+    // 2-byte level intervals, all resident (Params::k2_rr16) when the levels fit a byte
+    P.k2_rr16 = P.n_levels <= 255 && P.entry_cap % 8 == 0 ? 1 : 0;
+    if (const char* env = getenv("RD_K2_RR16")) P.k2_rr16 = P.k2_rr16 && atoi(env) != 0;
     int rmin = 256;   // resident rays a shape must hold (RD_K2_RMIN for A/B)
     if (const char* env = getenv("RD_K2_RMIN")) rmin = std::max(32, atoi(env));
     auto pick = [&](Params& Q, int cb, int& G, int& nt, int& minb, int forceT, int forceTY) {
@@ -361,7 +364,7 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
                    Q.k2t <= 254 && Q.k2ty >= 16 && Q.k2ty <= 254) {
         } else {   // the cheapest tiling whose layout fits this shape with 256 resident rays
           Q.k2t = Q.k2ty = s.T;
-          Q.k2_rcap = rmin;
+          Q.k2_rcap = Q.k2_rr16 ? 0 : rmin;
           const size_t lim = s.minb == 1 ? smax : std::min(smax, sm_sm / s.minb - 1024);
           for (const auto& t : tilings(s.T)) {
             Q.k2t = std::get<1>(t);
@@ -373,9 +376,9 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
           }
         }
         const size_t limit = s.minb == 1 ? smax : std::min(smax, sm_sm / s.minb - 1024);
-        Q.k2_rcap = rmin;
+        Q.k2_rcap = Q.k2_rr16 ? 0 : rmin;
         if (k_hough2_layout(Q, s.G, s.nt, cb) > limit) continue;
-        while (Q.k2_rcap < Q.entry_cap) {   // as many resident rays as fit
+        while (!Q.k2_rr16 && Q.k2_rcap < Q.entry_cap) {   // as many resident rays as fit
           Q.k2_rcap += 64;
           if (k_hough2_layout(Q, s.G, s.nt, cb) > limit) {
             Q.k2_rcap -= 64;

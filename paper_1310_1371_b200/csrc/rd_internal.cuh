@@ -41,7 +41,7 @@ struct Ring {          // == rd_ring (64 B)
 struct K2Layout {
   int cb, raws, rawp, lvlc;   // counter bytes, raw rows, row pitch (cells), cells per level
   int rawc;                   // raw columns (tile width + 2 halo); raws = tile height + 2 halo
-  int raw, hS, sd, rr, xy, hcell, hraw, task, cand, cdef, act, hcnt, w, wst, k, tn, dummy, mbar, total;
+  int raw, hS, sd, rr, xy, rr16, hcell, hraw, task, cand, cdef, act, hcnt, w, wst, k, tn, dummy, mbar, total;
   uint32_t rawp_magic;        // ceil(2^32 / rawp): cell / rawp = umulhi(cell, magic) for cells < 2^16
 };
 
@@ -92,6 +92,9 @@ struct Params {
   int k2_rcap;                  // K2: rays of a tile resident in shared memory (the rest read from global)
   int k2_ctas_per_sm;           // K2: resident CTAs per SM of a launch (0: as many as fit)
   const void* zeros;            // K2: a zero block at least as large as its level buffers (bulk-copy clears)
+  int k2_rr16;                  // 1: level intervals as 2 bytes (ra | rb << 8; levels < 255): K1.5 writes
+                                //   ray_r as uint16_t, K2 keeps every entry's interval in shared memory
+                                //   (no resident rays: direction and pixel from L2)
   K2Layout k2o;
   int ring_cap;
   Peak* peaks;                  // [F][ring_cap]

@@ -487,11 +487,13 @@ def test_batch_parts_do_not_change_results(rdmod, n, monkeypatch):
             assert np.array_equal(st[k], ref_st[k]), (split, k)
 
 
-@pytest.mark.parametrize("env", [("RD_K2_SQUARE", "1"), ("RD_K2_TILE", "86,77"), ("RD_K2_TILE", "200,60")])
+@pytest.mark.parametrize("env", [("RD_K2_SQUARE", "1"), ("RD_K2_TILE", "86,77"), ("RD_K2_TILE", "200,60"),
+                                 ("RD_K2_RR16", "0")])
 def test_rings_independent_of_hough_tiling(rdmod, env, monkeypatch):
     """The Hough tiling (square, rectangular, thin) changes how K1.5 routes rays and K2
     sweeps tiles, never the result: every frame's ring list is byte-identical to the default
-    tiling's."""
+    tiling's.  So does K2's ray storage: 2-byte level intervals all resident (the default
+    below 255 levels) or 4-byte intervals with the first rays resident (RD_K2_RR16=0)."""
     params = synth.preset(3)
     frames = torch.from_numpy(synth.batch(3, 0, 60, 6)).cuda()
     det = _det(rdmod, params, max_batch=6)
