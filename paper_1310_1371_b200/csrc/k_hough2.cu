@@ -6,18 +6,21 @@
 // tile) work items from a global counter.  For its tile a CTA sweeps r upward G levels
 // per step, keeping on chip G levels of packed counters (CB = 1 or 2 bytes) over the tile
 // + (K_max+1) halo and the hotspot lists of the last G + 2 levels (the paper's rolling
-// level window).  A step has three phases separated by CTA barriers:
-//   (1) votes: one thread per active ray (ridge pixel x sense of rho, routed to this tile
-//       by K1.5; the tile's rays are resident in shared memory) casts its votes for the G
-//       levels of the step; the atomic that lifts a counter past T_raw registers the
+// level window).  The tile's ray list (routed by K1.5) arrives by bulk
+// copies: every entry's 2-byte level interval below 255 levels (R16), else the first rcap
+// rays whole.  A step has three phases separated by CTA barriers:
+//   (1) votes: one thread per active ray (ridge pixel x sense of rho) casts its votes for
+//       the G levels of the step; the atomic that lifts a counter past T_raw registers the
 //       hotspot;
-//   (2) the rays active in the next step are listed; S at each hotspot
-//       — one warp (K > 7) or half-warp (K <= 7) per hotspot, lanes over window rows — and
-//       the candidate test S > T_norm(r) in the same pass;
-//   (3) the step's level buffers are cleared (16-byte stores; the paper resets the cells it
-//       registered, PAPER.md:426-434 — with byte counters a whole-buffer clear costs fewer
-//       instructions than tracking the touched words), and 3x3x3 peak extraction of the
-//       levels whose upper neighbour is complete, one warp per candidate.
+//   (2) S at each hotspot — lanes over window rows, dp4a against the
+//       step's weight words (bulk-copied a step ahead) — and the candidate test
+//       S > T_norm(r) in the same pass;
+//   (3) every second step the rays active in the next two steps are listed; the step's
+//       level buffers are cleared by one bulk copy of zeros on the TMA engine (the paper
+//       resets the cells it registered, PAPER.md:426-434 — with byte counters a whole-buffer
+//       clear is cheaper than tracking the touched words), which the next step's votes wait
+//       for on an mbarrier; 3x3x3 peak extraction of the levels whose upper neighbour is
+//       complete, one warp per candidate.
 // Byte counters (CB = 1) are exact while no counter passes 255: the atomic that finds 255
 // (P.u8_limit; lower only in tests) marks the frame, whose K2 results are then discarded and recomputed by the CB = 2
 // instance (k_redo_reset + the redo list), so results never depend on the counter width.
