@@ -196,6 +196,41 @@ def test_random_small_frames(rdmod):
         _check_frame(rdmod, det, i, params, frames[i], rings[i], full=(i < 6))
 
 
+@pytest.mark.parametrize("seed", range(40))
+def test_random_configs(rdmod, seed):
+    """A seeded walk over the configuration space rd_create accepts — frame sizes, pixel
+    type, smoothing scale, curvature threshold, radius range, both thresholds, the sigma(r)
+    rational, fixed annulus widths, ridges or edges — with every stage against the oracle
+    (ridge sets incl. the bits of rho, hotspot sets with S, counters, rings).  A config the
+    library rejects must be rejected with RD_ERR_PARAM / RD_ERR_DIM / RD_ERR_CONFIG."""
+    from paper_1310_1371_b200._rd import RDError, RD_ERR_PARAM, RD_ERR_DIM, RD_ERR_CONFIG
+    rng = np.random.default_rng(1000 + seed)
+    W, H = int(rng.integers(24, 260)), int(rng.integers(24, 260))
+    pb = int(rng.integers(1, 3))
+    a, b, den = [(1, 5, 20), (1, 3, 10), (2, 5, 40), (1, 10, 20)][int(rng.integers(0, 4))]
+    r_min = int(rng.integers(2, 16))
+    r_max = int(min(r_min + rng.integers(1, 100), min(W, H) - 1))
+    if r_max <= r_min:
+        r_min, r_max = 2, max(3, min(W, H) - 1)
+    edge = rng.random() < 0.25
+    params = dict(width=W, height=H, pixel_bytes=pb,
+                  max_value=255 if pb == 1 else (65535 if rng.random() < 0.25 else 4095),
+                  smoothing_sigma=float(rng.uniform(0.7, 4.3)),
+                  curvature_threshold=-float(rng.uniform(1, 8) if pb == 1 else rng.uniform(4, 20)),
+                  r_min=r_min, r_max=r_max, vote_threshold_raw=int(rng.integers(1, 7)),
+                  vote_threshold_norm=float(rng.uniform(0.2, 0.8)), sig_a=a, sig_b=b, sig_den=den,
+                  annulus_halfwidth=[0, 0, 1, 3][int(rng.integers(0, 4))],
+                  feature=1 if edge else 0, edge_threshold=(10.0 if pb == 1 else 40.0) if edge else 0.0)
+    frames = np.stack([_random_small(7919 * seed + k, W, H, pb) for k in range(3)])
+    try:
+        det, rings = _run(rdmod, params, frames)
+    except RDError as e:   # outside what the library takes: rejected with a reason, not run
+        assert e.status in (RD_ERR_PARAM, RD_ERR_DIM, RD_ERR_CONFIG), e
+        pytest.skip(f"config rejected: {e}")
+    for i in range(len(frames)):
+        _check_frame(rdmod, det, i, params, frames[i], rings[i])
+
+
 # ---------------------------------------------------------------- capacities fail loudly
 def test_capacity_overflow_reported(rdmod):
     """Every capacity overflow is reported (count -1, flag bit, rd_sync error), and
