@@ -47,6 +47,9 @@ inline size_t al16(size_t v) { return (v + 15) & ~size_t(15); }
 #ifndef RD_K2_HSL_MIN
 #define RD_K2_HSL_MIN 2   // fewest lanes per hotspot in the byte-counter S phase (8: 14.75, 4: 14.19, 2: 13.95, 1: 13.95 us/frame)
 #endif
+#ifndef RD_K2_HSL_TGT
+#define RD_K2_HSL_TGT 32   // lanes per hotspot: the widest hsl with hsl x (hotspots per warp) <= this (16: 14.29, 64: 14.94, 32: 13.99 us/frame)
+#endif
 #ifndef RD_K2_LP
 #define RD_K2_LP 2   // steps per active-ray listing (rays idle in one step of the pair vote masked)
 #endif
@@ -458,7 +461,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
           // lanes per hotspot: the widest power of two that still gives every warp its share
           const int per_warp = (ntask + NW - 1) / NW;
           int hsl = 32;
-          while (hsl > RD_K2_HSL_MIN && hsl * per_warp > 32) hsl >>= 1;
+          while (hsl > RD_K2_HSL_MIN && hsl * per_warp > RD_K2_HSL_TGT) hsl >>= 1;
 #else
           const int hsl = HSL;
 #endif
