@@ -333,8 +333,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
             if (i < nact) {
               const int e = act[i];
               RD_CHECK(e >= 0 && e < ne, CK_K2_RAY);
-              if (R16) {   // interval resident, pixel and direction from L2
-                rr = rr_of16(e);
+              if (R16) {   // pixel and direction from L2 (the interval is read at use, below)
                 xy = __ldg(P.ray_xy + gbase + e);
                 d = __ldg(P.ray_d + gbase + e);
               } else if (e < rcap) {
@@ -353,7 +352,12 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
           load_ray(warp * 32 + lane, nd, nxy, nrr);
           for (int i0 = warp * 32; i0 < nact; i0 += NT) {
             const double2 d = nd;
-            const uint32_t xy = nxy, rr = nrr;
+            const uint32_t xy = nxy;
+            uint32_t rr = nrr;
+            if (R16) {   // the resident interval, not carried in the prefetch registers
+              const int i = i0 + lane;
+              rr = i < nact ? rr_of16(act[i]) : 0xFFFFu;
+            }
             if (i0 + NT < nact) load_ray(i0 + NT + lane, nd, nxy, nrr);
             const int ga = max((int)(rr & 0xFFFFu) - L0, 0), gb = min((int)(rr >> 16) - L0, G - 1);
             const unsigned lm = gb >= ga ? (2u << gb) - (1u << ga) : 0u;   // levels of the step inside the ray's interval
