@@ -47,6 +47,10 @@ constexpr double NOT_CAND = 2.0;    // rho.x of a pixel that is not a ridge cand
 #define RD_K1_NSTAGE 2   // TMA input stages: rows are fetched NSTAGE - 1 steps ahead (3, 4, 6 measured slower)
 #endif
 constexpr int NSTAGE = RD_K1_NSTAGE;
+#ifndef RD_K1_LOCALSYNC
+#define RD_K1_LOCALSYNC 1   // phases joined by neighbour-warp mbarriers instead of CTA barriers
+#endif
+constexpr int KS_NW = KS_COLS / 32;  // warps per CTA
 constexpr int TMA_BOX = 128;       // a strip row is KS_COLS / 128 TMA boxes (128-byte aligned destinations)
 #ifndef RD_K1_TMA_TID
 #define RD_K1_TMA_TID (KS_COLS - 1)   // the issuing thread: a right-halo column (no ridge output)
@@ -58,7 +62,10 @@ template <int RB>
 struct K1SSmem {                       // dynamic shared memory of k_ridges2 (128-byte aligned base)
   alignas(128) uint16_t sIn[NSTAGE][RB][KS_COLS];   // TMA: input rows of NSTAGE steps (uint8 frames: rows
                                                     // of KS_COLS bytes at the same row offsets)
-  uint64_t bar[NSTAGE];                // TMA: one mbarrier per input stage
+  uint64_t bar[NSTAGE];                // TMA: one mbarrier per input stage (full)
+  uint64_t empty[NSTAGE];              // TMA: every thread has copied the stage out (local sync)
+  uint64_t nbar[3][KS_NW];             // local sync: phase boundary x of warp w, arrived on by
+                                       // the threads of warps w - 1, w, w + 1
   double2 sD[RB + 2][KS_COLS];         // rho ring (x = NOT_CAND: no candidate)
   double sK[RB + 2][KS_COLS];          // kappa ring
   double sG[RB][KS_COLS];              // G rows
@@ -126,6 +133,8 @@ k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, in
   const int xs = xc - (X0 - KS_HALO);   // this thread's clamped column inside a TMA row
   auto tma_issue = [&](int stp) {       // one thread: the RB rows of step stp into stage stp % NSTAGE
     const int sg = stp % NSTAGE;
+    // local sync: warps can be steps apart, so the stage's previous step must be copied out by all
+    if (RD_K1_LOCALSYNC && stp >= NSTAGE) mbar_wait(&S.empty[sg], (uint32_t)((stp / NSTAGE - 1) & 1));
     fence_proxy_async_smem();           // generic reads of the stage (NSTAGE steps ago) before the async writes
     mbar_expect_tx(&S.bar[sg], (uint32_t)(RB * KS_COLS * sizeof(PixT)));
 #pragma unroll
@@ -137,12 +146,32 @@ k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, in
         tma_load_3d(dst + b * TMA_BOX, &tmap, &S.bar[sg], X0 - KS_HALO + b * TMA_BOX, yy, f);
     }
   };
-  if (TMA) {
-    if (tid == 0) {
-      for (int i = 0; i < NSTAGE; ++i) mbar_init(&S.bar[i], 1);
-      mbar_fence_init();
+  if (tid == 0) {
+    for (int i = 0; i < NSTAGE; ++i) {
+      mbar_init(&S.bar[i], 1);
+      mbar_init(&S.empty[i], KS_COLS);
     }
-    __syncthreads();
+    for (int x = 0; x < 3; ++x)
+      for (int w = 0; w < KS_NW; ++w) mbar_init(&S.nbar[x][w], 32u * (1 + (w > 0) + (w < KS_NW - 1)));
+    mbar_fence_init();
+  }
+  __syncthreads();
+  // Phase boundaries (RD_K1_LOCALSYNC): every shared-memory exchange of this kernel is between
+  // columns at most K_s + 3 <= 16 apart, i.e. between neighbouring warps (a bin spans two), so a
+  // warp waits at a boundary only for warps w - 1 and w + 1 to reach it, not for the whole CTA;
+  // a slow warp (many rho candidates) delays its neighbours instead of every warp.  Neighbours
+  // stay within one boundary of each other, so one mbarrier per (boundary, warp) suffices.
+  auto phase_sync = [&](int x, int st) {
+    if (RD_K1_LOCALSYNC) {
+      if (warp > 0) mbar_arrive(&S.nbar[x][warp - 1]);
+      mbar_arrive(&S.nbar[x][warp]);
+      if (warp < KS_NW - 1) mbar_arrive(&S.nbar[x][warp + 1]);
+      mbar_wait(&S.nbar[x][warp], (uint32_t)(st & 1));
+    } else {
+      __syncthreads();
+    }
+  };
+  if (TMA) {
     if (tid == TMA_TID)
       for (int i = 0; i < NSTAGE - 1 && i < n_steps; ++i) tma_issue(i);
   } else {
@@ -157,7 +186,7 @@ k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, in
   // halves' ballots are in shared memory, so every bin keeps row-major order.
   const int b_own = (tid - KS_HALO) >> 5, b_i = (tid - KS_HALO) & 31;   // bin and index in it
   const int64_t fbase = (int64_t)f * P.nbx * P.nby;
-  if (tid < KS_NB) sCur[tid] = 0;
+  if (b_own >= 0 && b_own < KS_NB && b_i == 0) sCur[b_own] = 0;   // (by its writer: local sync)
   unsigned rd_bits = 0;            // ridge flags of the previous step's RB test rows
   int rd_y0 = 0;                   // first test row of the previous step
   bool rd_any = false;             // the previous step tested rows of this segment
@@ -175,6 +204,7 @@ k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, in
       const PixT* in = reinterpret_cast<const PixT*>(&S.sIn[sg][0][0]);
 #pragma unroll
       for (int r = 0; r < RB; ++r) sI[tid][r] = (int)in[r * KS_COLS + xs];
+      if (RD_K1_LOCALSYNC) mbar_arrive(&S.empty[sg]);
     } else if (compute) {
 #pragma unroll
       for (int r = 0; r < RB; ++r) {
@@ -183,7 +213,7 @@ k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, in
         pf[r] = reinterpret_cast<const PixT*>(frame + (int64_t)yy * pitch)[xc];
       }
     }
-    __syncthreads();
+    phase_sync(0, st);
     // ridges of the previous step's test rows (ballots of parity (st - 1) & 1): slots follow
     // from the bin cursor and the popcounts of earlier rows, so no shared state changes here
     const bool in_bin = b_own >= 0 && b_own < KS_NB;
@@ -255,7 +285,7 @@ k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, in
       for (int j = 0; j < KS; ++j) g += (unsigned long long)(uint32_t)q[j] * (unsigned long long)(wR[j] + wR[NTAP - 1 - j]);
       sG[r][tid] = (double)g;
     }
-    __syncthreads();
+    phase_sync(1, st);
     if (rd_any && in_bin && b_i == 0) sCur[b_own] = rd_cur;
     // 3. horizontal Sobel passes, vertical windows, kappa and rho of the kappa rows, RB rows
 #pragma unroll
@@ -303,7 +333,7 @@ k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, in
       sK[slot][tid] = kap;
       sD[slot][tid] = dir;
     }
-    __syncthreads();
+    phase_sync(2, st);
     // 4. ridge tests of the rows one behind the kappa rows (R6)
     rd_bits = 0;
     rd_y0 = yi0 - KS - 3;
