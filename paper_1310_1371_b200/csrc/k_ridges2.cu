@@ -12,7 +12,9 @@
 //   Ixx|Iyy|Ixy = s5|d2|d1 (x) H along y   5-row register windows          (fp64, exact)
 //   kappa (fixed fp64 recipe, no FMA) and rho of the candidates kappa < t, into row rings
 //   ridge test one row behind against the kappa ring (R6)
-// Three CTA barriers per step of RB rows; the RB rows of a phase are independent chains.
+// Three phase boundaries per step of RB rows, each joining a warp only with its two neighbours
+// (mbarriers; every exchange is between columns < 32 apart); the RB rows of a phase are
+// independent chains.
 // Every integer stage is exact, so evaluation order is free; kappa/rho use the shared
 // explicit-rounding recipe (rd_internal.cuh).  Replicate border: input rows and columns are
 // clamped at load time.
