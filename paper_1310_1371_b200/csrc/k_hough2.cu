@@ -50,9 +50,6 @@ inline size_t al16(size_t v) { return (v + 15) & ~size_t(15); }
 #ifndef RD_K2_HSL_TGT
 #define RD_K2_HSL_TGT 32   // lanes per hotspot: the widest hsl with hsl x (hotspots per warp) <= this (16: 14.29, 64: 14.94, 32: 13.99 us/frame)
 #endif
-#ifndef RD_K2_ROWW
-#define RD_K2_ROWW 1   // window rows: 0 a branch per weight word, 1 all 9 words, 2 five or nine words
-#endif
 #ifndef RD_K2_LP
 #define RD_K2_LP 2   // steps per active-ray listing (rays idle in one step of the pair vote masked)
 #endif
@@ -507,35 +504,16 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
               for (int row = hl; row <= 2 * K; row += hsl) {
                 const uint32_t* rowp = lvlw + (((iy - 1 + hal + row - K) * rawp + cx0 - al) >> 2);
                 uint32_t lo = 0, hi = 0;
-#if RD_K2_ROWW == 0
-#pragma unroll
-                for (int k = 0; k < NWW; ++k)
-                  if (k < nw) {
-                    const uint32_t v = rowp[k];
-                    lo = __dp4a(v, wl[k], lo);
-                    hi = __dp4a(v, wh[k], hi);
-                  }
-#else
-                // every word of the row read unconditionally (one batch of independent loads
-                // instead of a branch per word): words k >= nw have zero weights (wl = wh = 0)
-                // and lie inside shared memory (the raw levels are followed by the hotspot
+                // every word of the row is read unconditionally (a branch per word serialised
+                // the loads: 13.90 vs 13.31 us/frame): words k >= nw have zero weights (wl = wh
+                // = 0) and lie inside shared memory (the raw levels are followed by the hotspot
                 // arrays), so they add 0
-                if (RD_K2_ROWW == 2 && nw <= 5) {
 #pragma unroll
-                  for (int k = 0; k < 5; ++k) {
-                    const uint32_t v = rowp[k];
-                    lo = __dp4a(v, wl[k], lo);
-                    hi = __dp4a(v, wh[k], hi);
-                  }
-                } else {
-#pragma unroll
-                  for (int k = 0; k < NWW; ++k) {
-                    const uint32_t v = rowp[k];
-                    lo = __dp4a(v, wl[k], lo);
-                    hi = __dp4a(v, wh[k], hi);
-                  }
+                for (int k = 0; k < NWW; ++k) {
+                  const uint32_t v = rowp[k];
+                  lo = __dp4a(v, wl[k], lo);
+                  hi = __dp4a(v, wh[k], hi);
                 }
-#endif
                 acc += (unsigned long long)(hi * 64u + lo) * (unsigned long long)w[abs(row - K)];
               }
             }
