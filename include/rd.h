@@ -242,8 +242,11 @@ rd_status rd_kernel_times(rd_detector* det, float* h_ms, int32_t* n_calls);
 rd_status rd_phase_cycles(rd_detector* det, int32_t on, uint64_t* h_cycles);
 
 /* Step A3 in isolation: the fp64 kappa / rho recipe (R3) on n Hessians
- * d_abc[3i..3i+2] = (Ixx, Ixy, Iyy) -> d_out[3i..3i+2] = (kappa, dx, dy), d_degenerate[i] = 1
- * if isotropic.  Device pointers; asynchronous on stream. */
+ * d_abc[3i..3i+2] = (Ixx, Ixy, Iyy) -> d_out[3i..3i+2] = (kappa, dx, dy); d_degenerate[i]: bit 0
+ * set if isotropic, bits 1-2 = llround(dx) + 1 and bits 3-4 = llround(dy) + 1 as the ridge test
+ * takes them (from the unnormalised direction, without the division).  Computed the way the
+ * kernels split it (direction kept unnormalised by the ridge kernel, normalised by the ray
+ * kernel).  Device pointers; asynchronous on stream. */
 rd_status rd_eigen(const double* d_abc, int64_t n, double* d_out, int32_t* d_degenerate, void* stream);
 
 #ifdef __cplusplus

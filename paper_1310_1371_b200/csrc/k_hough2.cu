@@ -450,7 +450,9 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
           // byte counters: HSL lanes per hotspot, lane hl sums window rows hl, hl + HSL, ...;
           // a row is summed over whole 32-bit words with dp4a against the level's byte-plane
           // weights for the row's alignment (w = 64 wh + wl): exact integer S as below
-          constexpr int NWW = 9;   // weight words per row: (3 + 2K + 1 + 3) / 4 <= 9 for K <= 15
+          // weight words per row: (3 + 2K + 1 + 3) / 4 <= 9 for K <= 15; the task loop is
+          // instantiated for 3, 5, 7 and 9 words and the step takes the narrowest that holds its
+          // levels' windows (rows are read NWW words wide unconditionally, see below)
           // S tasks: the step's level lists back to back (task t -> level g, list index h)
           // the step's level counts, once (task decode below uses the prefix sums)
           int pre[G];   // pre[g] = tasks of levels 0 .. g
@@ -471,6 +473,8 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
 #endif
           const int NGW = 32 / hsl;   // hotspots per warp pass
           const int grp = lane / hsl, hl = lane & (hsl - 1);
+          auto run_s = [&](auto NWc) {
+          constexpr int NWW = decltype(NWc)::value;
           for (int t0 = NGW * warp; t0 < ntask; t0 += NGW * NW) {
             const int t = t0 + grp;
             const bool valid = t < ntask;
@@ -552,6 +556,15 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
               }
             }
           }
+          };
+          int Kst = 0;   // the widest window of the step's levels
+#pragma unroll
+          for (int g = 0; g < G; ++g) Kst = max(Kst, tK[min(L0 + g, nlev - 1)]);
+          const int nwst = (3 + 2 * Kst + 4) >> 2;
+          if (nwst <= 3) run_s(std::integral_constant<int, 3>{});
+          else if (nwst <= 5) run_s(std::integral_constant<int, 5>{});
+          else if (nwst <= 7) run_s(std::integral_constant<int, 7>{});
+          else run_s(std::integral_constant<int, 9>{});
         } else {
         const int nsmall = (ABL & 4) ? 0 : s_ntask[0], nlarge = (ABL & 4) ? 0 : s_ntask[1];
         const int half = lane >> 4;

@@ -87,7 +87,11 @@ __global__ void __launch_bounds__(32 * K15_WPB, RD_K15_MINB) k_rays(Params P) {
       if (valid) {
         const int64_t gi = fb * P.ridge_cap + (j >> 1);
         xy = P.bin_xy[gi];
-        d = P.bin_d[gi];
+        const double2 vraw = P.bin_d[gi];
+        // K1 leaves the direction unnormalised: rho = v / |v| here, where ridges are dense in the
+        // lanes (both senses compute it; sense 0 stores it for the dumps)
+        normalise_dir(vraw.x, vraw.y, &d.x, &d.y);
+        if (!(j & 1)) P.bin_d[gi] = d;
       }
       const double sgn = (j & 1) ? -1.0 : 1.0;
       const int x = (int)(xy & 0xFFFFu), y = (int)(xy >> 16);

@@ -44,7 +44,7 @@ constexpr int KS_NB = KS_OUT / 32;  // bins per strip
 #ifndef RD_K1_RB
 #define RD_K1_RB 4   // rows per step (TMA input: 9.8 us/frame vs 10.6 at 2, 10.9 at 3, 10.6 at 6 on cfg3)
 #endif
-constexpr double NOT_CAND = 2.0;    // rho.x of a pixel that is not a ridge candidate (|rho.x| <= 1)
+#define NOT_CAND __longlong_as_double(0x7ff8000000000000LL)   // v.x of a pixel that is not a ridge candidate (NaN)
 #ifndef RD_K1_NSTAGE
 #define RD_K1_NSTAGE 2   // TMA input stages: rows are fetched NSTAGE - 1 steps ahead (3, 4, 6 measured slower)
 #endif
@@ -68,7 +68,7 @@ struct K1SSmem {                       // dynamic shared memory of k_ridges2 (12
   uint64_t empty[NSTAGE];              // TMA: every thread has copied the stage out (local sync)
   uint64_t nbar[3][KS_NW];             // local sync: phase boundary x of warp w, arrived on by
                                        // the threads of warps w - 1, w, w + 1
-  double2 sD[RB + 2][KS_COLS];         // rho ring (x = NOT_CAND: no candidate)
+  double2 sD[RB + 2][KS_COLS];         // ring of unnormalised directions v (x = NaN: no candidate)
   double sK[RB + 2][KS_COLS];          // kappa ring
   double sG[RB][KS_COLS];              // G rows
   int sI[KS_COLS][RB];                 // input rows (as int), a column's RB rows adjacent
@@ -320,15 +320,13 @@ k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, in
           double sq, e;
           kap = kappa_of(Ixx, Ixy, Iyy, &sq, &e);
           double dx, dy;
-          if (kap < t_int && direction_of(Ixy, e, sq, &dx, &dy)) dir = make_double2(dx, dy);   // R3
+          // R3; the direction stays unnormalised here (K1.5 divides by its norm)
+          if (kap < t_int && direction_raw(Ixy, e, sq, &dx, &dy)) dir = make_double2(dx, dy);
         } else {   // edge variant (NEXT-2, R19): Ix = s5_y (x) d1_x, Iy = d1_y (x) s5_x, m2 = |grad|^2
           const double Ix = (wC[0] + wC[4]) + 4.0 * (wC[1] + wC[3]) + 6.0 * wC[2];
           const double Iy = (wB[4] - wB[0]) + 2.0 * (wB[3] - wB[1]);
           kap = __dadd_rn(__dmul_rn(Ix, Ix), __dmul_rn(Iy, Iy));
-          if (kap > t_edge2) {
-            const double n = __dsqrt_rn(kap);
-            dir = make_double2(__ddiv_rn(Ix, n), __ddiv_rn(Iy, n));
-          }
+          if (kap > t_edge2) dir = make_double2(Ix, Iy);   // n = sqrt(kap) divides in K1.5
         }
       }
       const int slot = (yk - ybase) % NR;
@@ -347,9 +345,10 @@ k_ridges2(const uint8_t* __restrict__ frames, int64_t pitch, int64_t fstride, in
       if (colR && yr >= Y0 && yr < Y1 && yr >= 3 && yr <= H - 4) {
         const int s0 = (yr - ybase) % NR, sm = (yr - 1 - ybase) % NR, sp = (yr + 1 - ybase) % NR;
         const double2 dir = sD[s0][tid];
-        if (dir.x != NOT_CAND) {
+        if (dir.x == dir.x) {   // a candidate (not NaN)
           const double kp = sK[s0][tid];
-          const int ox = (int)llround(dir.x), oy = (int)llround(dir.y);
+          int ox, oy;   // llround of rho's components
+          dir_step(dir.x, dir.y, &ox, &oy);
           const bool after_plus = (oy > 0) || (oy == 0 && ox > 0);
           const double kplus = sK[oy > 0 ? sp : (oy < 0 ? sm : s0)][tid + ox];
           const double kminus = sK[oy > 0 ? sm : (oy < 0 ? sp : s0)][tid - ox];
@@ -488,12 +487,19 @@ __global__ void k_eigen(const double* __restrict__ abc, int64_t n, double* __res
   const double a = abc[3 * i], b = abc[3 * i + 1], c = abc[3 * i + 2];
   double s, e;
   const double k = kappa_of(a, b, c, &s, &e);
-  double dx, dy;
-  const bool ok = direction_of(b, e, s, &dx, &dy);
+  // the product's split of the recipe: K1 keeps v unnormalised and takes the ridge test's
+  // neighbour step from dir_step; K1.5 normalises
+  double vx, vy, dx = 0.0, dy = 0.0;
+  int ox = 0, oy = 0;
+  const bool ok = direction_raw(b, e, s, &vx, &vy);
+  if (ok) {
+    normalise_dir(vx, vy, &dx, &dy);
+    dir_step(vx, vy, &ox, &oy);
+  }
   out[3 * i] = k;
   out[3 * i + 1] = dx;
   out[3 * i + 2] = dy;
-  deg[i] = ok ? 0 : 1;
+  deg[i] = (ok ? 0 : 1) | ((ox + 1) << 1) | ((oy + 1) << 3);
 }
 
 cudaError_t launch_eigen(const double* abc, int64_t n, double* out, int* deg, cudaStream_t st) {

@@ -71,7 +71,7 @@ struct Params {
   int ridge_cap;                // per bin
   int* bin_count;               // [F][nby*nbx]
   uint32_t* bin_xy;             // [F][bins][ridge_cap] x | y<<16
-  double2* bin_d;               // [F][bins][ridge_cap] (dx, dy)
+  double2* bin_d;               // [F][bins][ridge_cap] K1: unnormalised v; K1.5 overwrites it with rho = v / |v| (dx, dy)
   // Hough tiles (K2)
   int k2t;                      // Hough tile width (k2t x k2ty accumulator cells per CTA)
   int k2ty;                     // Hough tile height (the persistent K2 balances the tiling; else = k2t)
@@ -159,6 +159,41 @@ __device__ __forceinline__ bool direction_of(double b, double e, double s, doubl
   *dx = __ddiv_rn(vx, n);
   *dy = __ddiv_rn(vy, n);
   return true;
+}
+
+// The same direction before its normalisation: K1 keeps v = (vx, vy) and K1.5 divides by |v|
+// where the ridges are dense in the lanes (the square root and the two divisions are ~95
+// instructions, which K1 ran warp-wide wherever one lane held a candidate).  False if degenerate.
+__device__ __forceinline__ bool direction_raw(double b, double e, double s, double* vx, double* vy) {
+  if (e == 0.0 && b == 0.0) { *vx = 0.0; *vy = 0.0; return false; }
+  if (e >= 0.0) { *vx = -b; *vy = __dmul_rn(0.5, __dadd_rn(e, s)); }
+  else { *vx = __dmul_rn(0.5, __dsub_rn(s, e)); *vy = -b; }
+  return true;
+}
+// rho = v / |v| with direction_of's roundings (v != 0)
+__device__ __forceinline__ void normalise_dir(double vx, double vy, double* dx, double* dy) {
+  const double n = __dsqrt_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)));
+  *dx = __ddiv_rn(vx, n);
+  *dy = __ddiv_rn(vy, n);
+}
+// (llround(rho.x), llround(rho.y)) of rho = normalise_dir(v), each in {-1, 0, 1}, without the
+// division where the squares decide: |rn(vx / n)| >= 1/2 iff vx^2 >= (vx^2 + vy^2)(1 + eta) / 4 with
+// |eta| < 2^-49 (the roundings of the two squares, their sum, the root and the quotient), i.e.
+// iff 3 vx^2 - vy^2 >= eta'(vx^2 + vy^2); outside a 2^-40 band around equality the sign of
+// 3 vx^2 - vy^2 decides, inside it (never seen; v's components are dyadic rationals and sqrt(3)
+// is not) the exact recipe runs.
+__device__ __forceinline__ void dir_step(double vx, double vy, int* ox, int* oy) {
+  const double A = vx * vx, B = vy * vy, band = (A + B) * 0x1p-40;
+  const double tx = 3.0 * A - B, ty = 3.0 * B - A;
+  if (fabs(tx) > band && fabs(ty) > band) {
+    *ox = tx > 0.0 ? (vx > 0.0 ? 1 : -1) : 0;
+    *oy = ty > 0.0 ? (vy > 0.0 ? 1 : -1) : 0;
+  } else {
+    double dx, dy;
+    normalise_dir(vx, vy, &dx, &dy);
+    *ox = (int)llround(dx);
+    *oy = (int)llround(dy);
+  }
 }
 
 // round half away from zero of an exactly computed double (llround semantics)

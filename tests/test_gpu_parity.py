@@ -85,19 +85,36 @@ def _check_batch(det, params, frames, out, n_threads=0):
 # ---------------------------------------------------------------- A3 recipe
 def test_eigen_recipe_bit_exact(rdmod):
     rng = np.random.default_rng(0)
-    M = rng.integers(-10 ** 13, 10 ** 13, size=(10000, 3)).astype(np.float64)
+    M = rng.integers(-10 ** 13, 10 ** 13, size=(12000, 3)).astype(np.float64)
     M[:50] = rng.integers(-3, 4, size=(50, 3))            # small / degenerate-prone
     M[50] = (5.0, 0.0, 5.0)                               # isotropic
     M[51] = (0.0, 1.0, 0.0)
     M[52] = (-2.0, 0.0, -1.0)
+    # directions at 30 / 60 degrees, where a component of rho rounds between 0 and 1 (|rho_x| or
+    # |rho_y| = 1/2 iff |a - c| = 2|b|/sqrt(3)): the ridge test's neighbour step comes from the
+    # squared components there, and inside a 2^-40 band from the exact recipe; magnitudes from
+    # 10 (far outside the band after rounding to integers) to 1e13 (inside it)
+    for j in range(2000):
+        mag = 10.0 ** rng.uniform(1, 13)
+        b = float(np.rint(rng.uniform(-1, 1) * mag)) or 1.0
+        e = float(np.rint(2.0 * abs(b) / np.sqrt(3.0))) * (1 if j & 1 else -1) + float(rng.integers(-1, 2))
+        c = float(np.rint(rng.uniform(-1, 1) * mag))
+        M[10000 + j] = (c + e, b, c)
     out, deg = rdmod.eigen(torch.from_numpy(M).cuda())
     out, deg = out.cpu().numpy(), deg.cpu().numpy()
+    n_close = 0
     for i, (a, b, c) in enumerate(M):
         k, dx, dy, d = oracle.eigen(a, b, c)
-        assert bool(deg[i]) == d
+        assert bool(deg[i] & 1) == d
         assert out[i, 0].tobytes() == np.float64(k).tobytes()
         if not d:
             assert out[i, 1].tobytes() == np.float64(dx).tobytes() and out[i, 2].tobytes() == np.float64(dy).tobytes()
+            # llround (half away from zero) of the oracle's components
+            ox = int(np.sign(dx)) if abs(dx) >= 0.5 else 0
+            oy = int(np.sign(dy)) if abs(dy) >= 0.5 else 0
+            assert ((deg[i] >> 1) & 3) - 1 == ox and ((deg[i] >> 3) & 3) - 1 == oy, (i, a, b, c, dx, dy, deg[i])
+            n_close += min(abs(abs(dx) - 0.5), abs(abs(dy) - 0.5)) < 1e-12
+    assert n_close >= 100   # the band's exact path was exercised
 
 
 # ---------------------------------------------------------------- configs, stage by stage
