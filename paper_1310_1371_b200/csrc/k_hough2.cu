@@ -359,8 +359,9 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
               rr = i < nact ? rr_of16(act[i]) : 0xFFFFu;
             }
             if (i0 + NT < nact) load_ray(i0 + NT + lane, nd, nxy, nrr);
-            const int ga = max((int)(rr & 0xFFFFu) - L0, 0), gb = min((int)(rr >> 16) - L0, G - 1);
-            const unsigned lm = gb >= ga ? (2u << gb) - (1u << ga) : 0u;   // levels of the step inside the ray's interval
+            // levels ga..gb of the step lie inside the ray's interval (empty: ga > gb); compared with
+            // each g directly (chained predicates: a level bitmask cost ~10 more instructions a chunk)
+            const int ga = (int)(rr & 0xFFFFu) - L0, gb = (int)(rr >> 16) - L0;
             const double dx = d.x, dy = d.y;
             const int xr = (int)(xy & 0xFFFFu) - RX0, yr = (int)(xy >> 16) - RY0;
             // targets of the G levels, branch-free: a vote counts if its level is in the ray's
@@ -370,6 +371,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
             uint32_t addr[GL], sh[GL], old[GL];
             const uint32_t pb = raw_base + (uint32_t)(CB * (yr * rawp + xr));   // the ray's own cell (bytes)
             const int ux = xr - bx0, uy = yr - by0;
+            const double hx = copysign(0.5, dx), hy = copysign(0.5, dy);   // (r_lo >= 1)
             int qx = 0, qy = 0;   // (32: timing experiment only, integer fixed-point targets)
             if (ABL & 32) {
               qx = __double2int_rn(dx * 65536.0);
@@ -383,10 +385,11 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
                 ox = ((P.r_lo + L0 + g) * qx + 32768) >> 16;
                 oy = ((P.r_lo + L0 + g) * qy + 32768) >> 16;
               } else {
-                ox = round_half_away_i(__dmul_rn(rd, dx));
-                oy = round_half_away_i(__dmul_rn(rd, dy));
+                // llround: r > 0, so the product has the direction's sign and the half is the ray's
+                ox = __double2int_rz(__dadd_rz(__dmul_rn(rd, dx), hx));
+                oy = __double2int_rz(__dadd_rz(__dmul_rn(rd, dy), hy));
               }
-              const bool ok = ((lm >> g) & 1u) & ((unsigned)(ux + ox) <= (unsigned)bxs) &
+              const bool ok = (g >= ga) & (g <= gb) & ((unsigned)(ux + ox) <= (unsigned)bxs) &
                               ((unsigned)(uy + oy) <= (unsigned)bys);
               const uint32_t bc = pb + (uint32_t)(g * lvlc * CB) + (uint32_t)(CB * (oy * rawp + ox));   // byte address
               // masked votes: shift 32 (shl/shr clamp to 0) on the lane's dummy word
