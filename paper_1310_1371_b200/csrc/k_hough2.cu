@@ -468,14 +468,18 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
           if (ABL & 4) ntask = 0;
 #if RD_K2_HSL == 0
           // lanes per hotspot: the widest power of two that still gives every warp its share
+          // (hsl = 32 >> lgs with lgs = ceil(log2(per_warp)) capped: shifts, no loop and no division)
           const int per_warp = (ntask + NW - 1) / NW;
-          int hsl = 32;
-          while (hsl > RD_K2_HSL_MIN && hsl * per_warp > RD_K2_HSL_TGT) hsl >>= 1;
+          static_assert(RD_K2_HSL_TGT == 32 && (RD_K2_HSL_MIN & (RD_K2_HSL_MIN - 1)) == 0, "closed form below");
+          constexpr int LGS_MAX = RD_K2_HSL_MIN == 1 ? 5 : RD_K2_HSL_MIN == 2 ? 4 : RD_K2_HSL_MIN == 4 ? 3 : RD_K2_HSL_MIN == 8 ? 2 : RD_K2_HSL_MIN == 16 ? 1 : 0;
+          const int lgs = per_warp <= 1 ? 0 : min(32 - __clz(per_warp - 1), LGS_MAX);
+          const int hsl = 32 >> lgs;
 #else
-          const int hsl = HSL;
+          constexpr int hsl = HSL;
+          constexpr int lgs = HSL == 32 ? 0 : HSL == 16 ? 1 : HSL == 8 ? 2 : HSL == 4 ? 3 : HSL == 2 ? 4 : 5;
 #endif
-          const int NGW = 32 / hsl;   // hotspots per warp pass
-          const int grp = lane / hsl, hl = lane & (hsl - 1);
+          const int NGW = 1 << lgs;   // hotspots per warp pass
+          const int grp = lane >> (5 - lgs), hl = lane & (hsl - 1);
           auto run_s = [&](auto NWc) {
           constexpr int NWW = decltype(NWc)::value;
           for (int t0 = NGW * warp; t0 < ntask; t0 += NGW * NW) {
@@ -560,9 +564,9 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
             }
           }
           };
-          int Kst = 0;   // the widest window of the step's levels
-#pragma unroll
-          for (int g = 0; g < G; ++g) Kst = max(Kst, tK[min(L0 + g, nlev - 1)]);
+          // the widest window of the step's levels: its last level's (K_r = ceil(3 sigma(r)) does not
+          // decrease with r: rd_create requires sig_a >= 0)
+          const int Kst = tK[min(L0 + G - 1, nlev - 1)];
           const int nwst = (3 + 2 * Kst + 4) >> 2;
           if (nwst <= 3) run_s(std::integral_constant<int, 3>{});
           else if (nwst <= 5) run_s(std::integral_constant<int, 5>{});
