@@ -501,7 +501,7 @@ __global__ void __launch_bounds__(NT, MINB) k_hough2(const __grid_constant__ Par
             uint32_t wl[NWW], wh[NWW];   // (bulk-copied a step ahead: 32 B per level and word)
 #pragma unroll
             for (int k = 0; k < NWW; ++k) {
-              const uint2 w2 = k < nw ? wp[k] : make_uint2(0u, 0u);
+              const uint2 w2 = wp[k];   // zero beyond the row's nw words (NWW <= wp_nw, which is odd)
               wl[k] = w2.x;
               wh[k] = w2.y;
             }

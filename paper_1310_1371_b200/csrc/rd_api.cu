@@ -257,7 +257,10 @@ rd_status rd_create(const rd_config* cin, int32_t max_batch, int32_t device, rd_
   P.k_icpt = (float)(3.0 * c.sig_b / c.sig_den + 1.0) + 0.01f;
   P.hal = Kmax + 1;
   P.wstride = Kmax + 1;
-  P.wp_nw = (2 * Kmax + 1 + 3 + 3) / 4;   // K2 dp4a weight words per window row (table below)
+  // K2 dp4a weight words per window row (table below), rounded up to odd: the kernel reads 3, 5, 7
+  // or 9 words of a row, the least that holds the step's widest window, and relies on zero words
+  // up to that count
+  P.wp_nw = ((2 * Kmax + 1 + 3 + 3) / 4) | 1;
   std::vector<int> lvlW((size_t)P.n_levels * P.wstride, 0);
   double max_wsum = 0;
   for (int li = 0; li < P.n_levels; ++li) {
